@@ -1,0 +1,175 @@
+/*
+ * epsgraph_b200.h -- C ABI of the B200-native eps-graph build path.
+ *
+ * The reference (`epsgraph` 0.1.0) is a pure-Python package whose hot loops
+ * are numba @njit kernels; it has no FFI layer of its own.  Each entry point
+ * below replaces one reference function (cited file:line, relative to
+ * /root/reference/pkg/src/epsgraph/), and the Python package
+ * `paper_0904_3151_b200` binds them through ctypes exactly where the
+ * reference calls its numba kernels.
+ *
+ * Conventions
+ *  - Every pointer argument named d_* is DEVICE memory owned by the caller;
+ *    h_* pointers are host memory.  The library never allocates or frees
+ *    caller memory; scratch comes from a caller-provided workspace whose size
+ *    is returned by the matching *_workspace() query.
+ *  - `stream` is a cudaStream_t passed as void*; all work is enqueued on it.
+ *    Functions that must return a count synchronise that stream once.
+ *  - Row indices are < 2^32.  Pair keys are uint64 (i << 32) | j with i < j,
+ *    so sorting keys sorts pairs lexicographically by (i, j).
+ *  - Return value: EG_OK or one of the EG_ERR_* codes; eg_last_error()
+ *    returns a message for the last failure on the calling thread.
+ */
+#ifndef EPSGRAPH_B200_H
+#define EPSGRAPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EG_OK 0
+#define EG_ERR_ARG 1          /* invalid argument (-> ValueError)            */
+#define EG_ERR_CUDA 2         /* CUDA runtime failure (-> RuntimeError)      */
+#define EG_ERR_CAPACITY 3     /* output capacity too small; count returned   */
+#define EG_ERR_WORKSPACE 4    /* workspace smaller than *_workspace() says   */
+#define EG_ERR_UNSUPPORTED 5  /* shape outside the kernels' limits           */
+
+#define EG_METRIC_COSINE 0
+#define EG_METRIC_EUCLIDEAN 1
+
+/* Largest string length / block count the enumeration kernels support. */
+#define EG_MAX_LENGTH 256
+#define EG_MAX_BLOCKS 64
+
+const char *eg_last_error(void);
+int eg_version(void);
+/* Number of SMs of the current device (for host-side sizing). */
+int eg_device_sm_count(void);
+
+/* --------------------------------------------------------------------- */
+/* Row statistics.  Replaces the validation in VectorDataset.__init__     */
+/* (lsh.py:48-57), _check_norms (lsh.py:121-125) and the norm pass of     */
+/* filter_exact (pipeline.py:203).                                        */
+/* d_x: n x dim row-major, float32 (x_is_f64 = 0) or float64 (= 1).       */
+/* d_norms[n] = sqrt(sum_q x_q^2) in fp64.  h_bad[0] = first row with a   */
+/* non-finite entry or -1; h_bad[1] = first zero-norm row or -1.          */
+/* --------------------------------------------------------------------- */
+int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
+                 double *d_norms, int64_t *h_bad, void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Projection + sign packing.  Replaces _sign_bits (lsh.py:96-113),       */
+/* _project_words (lsh.py:128-147) and BitStringPool.from_bits            */
+/* (bitpool.py:125-141) for `replicates` replicates at once.              */
+/* d_r: (replicates*length) x dim fp64 directions, replicate-major (the   */
+/* host draws them with numpy exactly as lsh.py:116-118,145 does).        */
+/* d_rnorm[replicates*length]: fp64 Euclidean norms of those rows.        */
+/* d_codes: replicates x n x W uint64, W = ceil(length/64); bit t of a    */
+/* row is word t/64, position t%64; padding bits are zero.                */
+/* Signs are bit-identical to the reference's sequential fp64 sum: a fast */
+/* pass decides every entry whose |dot| exceeds a certified error band;   */
+/* the rest are recomputed with separately rounded fp64 mul/add.          */
+/* h_fixups (optional) receives the number of recomputed entries.         */
+/* --------------------------------------------------------------------- */
+size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t replicates);
+int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
+               const double *d_norms, const double *d_r, const double *d_rnorm,
+               int32_t length, int32_t replicates, uint64_t *d_codes,
+               void *d_workspace, size_t workspace_bytes, int64_t *h_fixups,
+               void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Multiple-sorting-method enumeration over (replicate, mask) units.      */
+/* Replaces, per unit, masked_key_table (bitpool.py:224-253),             */
+/* _counting_pass/_sort_grouped (hamming_join.py:52-82, 252-272),         */
+/* _group_bounds (:85-101), _emit_group_pairs (:104-149), and the         */
+/* cross-replicate first-witness fold (pipeline.py:286-314).              */
+/* d_codes: replicates x n x W (as produced by eg_project, or a pool).    */
+/* h_block_bounds[k+1]: block offsets (bitpool.py:44-69).                 */
+/* h_unit_rep[n_units], h_unit_mask[n_units]: replicate index and block   */
+/* bitmask (bit b set = block b masked) of each unit; |mask| == d.        */
+/* A pair (i<j) is emitted by unit (h, B) iff popcount(c_i^c_j) <= d in   */
+/* replicate h, B is the lexicographically first d-subset containing the  */
+/* blocks where they differ (== the reference's first-witness mask rule), */
+/* and popcount > d in every replicate g < h.                             */
+/* d_out_keys[capacity]: emitted pair keys, in no particular order.       */
+/* h_counts (2*replicates + 2 int64): [0] total emitted (may exceed       */
+/* capacity -> EG_ERR_CAPACITY), [1] largest equal-key group seen,        */
+/* [2+h] raw pairs of replicate h (before the cross-replicate rule),      */
+/* [2+replicates+h] new pairs of replicate h.                             */
+/* --------------------------------------------------------------------- */
+size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates);
+int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
+                 int32_t replicates, const int32_t *h_block_bounds, int32_t k,
+                 int32_t d, const int32_t *h_unit_rep, const uint64_t *h_unit_mask,
+                 int64_t n_units, uint64_t *d_out_keys, int64_t capacity,
+                 int64_t *h_counts, void *d_workspace, size_t workspace_bytes,
+                 void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Grouped sort of one mask.  Replaces grouped_radix_sort                 */
+/* (hamming_join.py:275-297): d_perm[n] is a permutation of rows in which */
+/* equal masked keys are contiguous; h_groups receives the group count    */
+/* and d_bounds[0..groups] the run offsets.  Order is deterministic but   */
+/* (like the reference's) not lexicographic.                              */
+/* --------------------------------------------------------------------- */
+size_t eg_grouped_sort_workspace(int64_t n, int32_t length);
+int eg_grouped_sort(const uint64_t *d_codes, int64_t n, int32_t length,
+                    const int32_t *h_block_bounds, int32_t k, uint64_t mask_bits,
+                    uint32_t *d_perm, int64_t *d_bounds, int64_t *h_groups,
+                    void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Cross-replicate first witness for externally supplied pair sets.       */
+/* Replaces dedup_across_replicates' inner loop (pipeline.py:104-146):    */
+/* d_keep[m] = 1 iff popcount over every pool g in d_pools[0..n_pools)    */
+/* exceeds d.  d_pools is a device array of device pointers.              */
+/* --------------------------------------------------------------------- */
+int eg_first_witness(const uint64_t *d_keys, int64_t m,
+                     const uint64_t *const *d_pools, int32_t n_pools, int32_t W,
+                     int32_t d, uint8_t *d_keep, void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Radix sort of uint64 keys (optionally carrying uint32 values).         */
+/* Replaces the final np.lexsort of enumerate_pairs (hamming_join.py:     */
+/* 369-375) and filter_exact (pipeline.py:222).  Sorts the low key_bits   */
+/* bits; result lands back in d_keys/d_vals.                              */
+/* --------------------------------------------------------------------- */
+size_t eg_sort_workspace(int64_t m, int with_values);
+int eg_sort_keys(uint64_t *d_keys, uint32_t *d_vals, int64_t m, int32_t key_bits,
+                 void *d_workspace, size_t workspace_bytes, void *stream);
+/* Pair keys (i << 32 | j) with i, j < n: only the populated digits of both
+ * halves are sorted.  Workspace: eg_sort_workspace(m, 0). */
+int eg_sort_pair_keys(uint64_t *d_keys, int64_t m, int64_t n, void *d_workspace,
+                      size_t workspace_bytes, void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Stable compaction of keys by a byte flag (keeps input order).          */
+/* --------------------------------------------------------------------- */
+size_t eg_compact_workspace(int64_t m);
+int eg_compact_keys(const uint64_t *d_keys, const uint8_t *d_flags, int64_t m,
+                    uint64_t *d_out, int64_t *h_count, void *d_workspace,
+                    size_t workspace_bytes, void *stream);
+
+/* --------------------------------------------------------------------- */
+/* Exact verification.  Replaces filter_exact (pipeline.py:183-223).      */
+/* Cosine: dist = clip(1 - dot/(n_i n_j), 0, 2); Euclidean: ||x_i-x_j||.  */
+/* fp64 accumulation in a fixed order per pair (per-pair deterministic).  */
+/* Keeps dist <= eps; output keeps the input order (stable), so sorted    */
+/* candidate keys give sorted edges.  h_count receives the edge count.    */
+/* Keys must satisfy i, j < n (checked; EG_ERR_ARG on violation).         */
+/* --------------------------------------------------------------------- */
+size_t eg_verify_workspace(int64_t m);
+int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
+              const double *d_norms, const uint64_t *d_keys, int64_t m,
+              int32_t metric, double eps, uint64_t *d_out_keys, double *d_out_dist,
+              int64_t *h_count, void *d_workspace, size_t workspace_bytes,
+              void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPSGRAPH_B200_H */

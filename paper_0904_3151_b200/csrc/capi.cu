@@ -1,0 +1,509 @@
+// capi.cu -- extern "C" entry points of libepsgraph_b200.so (see
+// include/epsgraph_b200.h) and the host-side launch logic around the
+// kernels.  Single translation unit: nvcc -gencode arch=compute_100a,
+// code=sm_100a -O3 -lineinfo -shared.
+#include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "msm.cuh"
+#include "project.cuh"
+#include "scan_sort.cuh"
+#include "verify.cuh"
+
+namespace eg {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static int arg_error(const char *msg) {
+  set_error("%s", msg);
+  return EG_ERR_ARG;
+}
+
+static int num_sms() {
+  static int cached = 0;
+  if (!cached) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+      cached = 148;
+  }
+  return cached;
+}
+
+// ------------------------------------------------------------ projection
+static int project_tn(int cols) {
+  int g = (cols + 31) / 32;
+  return g > 8 ? 8 : g;
+}
+
+static double projection_tau(int dim) {
+  // |s_fp32 - s_exact| <= ((dim+2) u + O(u^2)) sum|x_q r_q| <= ... ||x|| ||r||
+  // (u = 2^-24: rounding of x and r to fp32, FMA accumulation); plus the
+  // reference's own fp64 error dim * 2^-53; 25% safety margin.
+  return 1.25 * ((double)(dim + 2) * ldexp(1.0, -24) + (double)dim * ldexp(1.0, -52));
+}
+
+static unsigned long long fixup_cap(int64_t n, int cols) {
+  unsigned long long c = (unsigned long long)n * cols / 256;
+  return c < (1ull << 20) ? (1ull << 20) : c;
+}
+
+template <typename TX, int TN>
+static void launch_project(const TX *x, int64_t n, int dim, const float *rt, int cols,
+                           int cols_pad, const double *norms, const double *rnorm, double tau,
+                           int L, int W, uint64_t *codes, FixupList fl, cudaStream_t st) {
+  unsigned grid = (unsigned)((n + PJ_BM - 1) / PJ_BM);
+  k_project<TX, TN><<<grid, PJ_NT, 0, st>>>(x, n, dim, rt, cols, cols_pad, norms, rnorm, tau, L,
+                                            W, codes, fl);
+}
+
+template <typename TX>
+static void dispatch_project(int tn, const TX *x, int64_t n, int dim, const float *rt, int cols,
+                             int cols_pad, const double *norms, const double *rnorm, double tau,
+                             int L, int W, uint64_t *codes, FixupList fl, cudaStream_t st) {
+  switch (tn) {
+#define EG_TN(T)                                                                              \
+  case T:                                                                                     \
+    launch_project<TX, T>(x, n, dim, rt, cols, cols_pad, norms, rnorm, tau, L, W, codes, fl, \
+                          st);                                                                \
+    break;
+    EG_TN(1) EG_TN(2) EG_TN(3) EG_TN(4) EG_TN(5) EG_TN(6) EG_TN(7) EG_TN(8)
+#undef EG_TN
+  }
+}
+
+// ------------------------------------------------------------------ MSM
+static int msm_lgb(int64_t n) {
+  int64_t target = (n + MSM_TARGET - 1) / MSM_TARGET;
+  int l = ilog2_ceil((uint64_t)(target < 1 ? 1 : target));
+  return l > MSM_MAX_LGB ? MSM_MAX_LGB : l;
+}
+
+static int msm_batch_units(int64_t n) {
+  // keep the per-batch scratch (elems + gcnt: 12 B/row/unit) under ~2 GiB
+  int64_t per = n * 12;
+  int64_t u = per > 0 ? (int64_t)(2ll << 30) / per : MSM_MAXU;
+  if (u < 1) u = 1;
+  return (int)(u > MSM_MAXU ? MSM_MAXU : u);
+}
+
+struct MsmLayout {
+  int lgB, B, U;
+  size_t bytes;
+};
+
+static MsmLayout msm_layout(int64_t n, int reps) {
+  MsmLayout l;
+  l.lgB = msm_lgb(n);
+  l.B = 1 << l.lgB;
+  l.U = msm_batch_units(n);
+  size_t b = 0;
+  b += ws_bytes((size_t)l.U * l.B, 4);            // counts
+  b += ws_bytes((size_t)l.U * (l.B + 1), 4);      // starts
+  b += ws_bytes((size_t)l.U * l.B, 4);            // cursor
+  b += ws_bytes((size_t)l.U * n, 8);              // elems
+  b += ws_bytes((size_t)l.U * n, 4);              // gcnt
+  b += ws_bytes(EG_MAX_LENGTH, 1);                // bit2blk
+  b += ws_bytes(3 + 2 * (size_t)reps, 8);         // counters
+  b += ws_bytes((size_t)l.U * (l.B + 1) * 3, 4);  // spill list
+  l.bytes = b + 4096;
+  return l;
+}
+
+template <int W>
+static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch> &batches,
+                   cudaStream_t st) {
+  const size_t smem_hist = (size_t)lay.B * 4, smem_scatter = (size_t)lay.B * 8;
+  const size_t smem_group = sizeof(GroupSmem<W>);
+  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_hist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_hist));
+  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_scatter<W>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_scatter));
+  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_group<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_group));
+  const unsigned tiles = (unsigned)((a.n + MSM_TILE - 1) / MSM_TILE);
+  const unsigned spill_grid = (unsigned)num_sms() * 8;
+  for (const UnitBatch &ub : batches) {
+    dim3 g1(tiles, ub.count);
+    k_msm_hist<W><<<g1, MSM_NT, smem_hist, st>>>(a, ub);
+    k_msm_scan<<<ub.count, 1024, 0, st>>>(a);
+    k_msm_scatter<W><<<g1, MSM_NT, smem_scatter, st>>>(a, ub);
+    dim3 g4(lay.B, ub.count);
+    k_msm_group<W><<<g4, MSM_GNT, smem_group, st>>>(a, ub);
+    k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, st>>>(a, ub);
+    k_msm_spill_maxgroup<<<64, 256, 0, st>>>(a);
+    EG_LAUNCH_CHECK();
+  }
+  return EG_OK;
+}
+
+}  // namespace eg
+
+using namespace eg;
+
+extern "C" {
+
+const char *eg_last_error(void) { return g_err; }
+int eg_version(void) { return 1; }
+int eg_device_sm_count(void) { return num_sms(); }
+
+// ------------------------------------------------------------ row stats
+int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *d_norms,
+                 int64_t *h_bad, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || dim < 1 || !h_bad) return arg_error("eg_row_stats: bad shape");
+  h_bad[0] = h_bad[1] = -1;
+  if (n == 0) return EG_OK;
+  unsigned long long *bad;
+  EG_CUDA_TRY(cudaMallocAsync(&bad, 16, st));
+  EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 16, st));
+  unsigned grid = (unsigned)((n + 7) / 8);
+  if (x_is_f64)
+    k_row_stats<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, bad);
+  else
+    k_row_stats<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, bad);
+  EG_LAUNCH_CHECK();
+  unsigned long long hb[2];
+  EG_CUDA_TRY(cudaMemcpyAsync(hb, bad, 16, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaFreeAsync(bad, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < 2; ++i) h_bad[i] = hb[i] == ~0ull ? -1 : (int64_t)hb[i];
+  return EG_OK;
+}
+
+// ----------------------------------------------------------- projection
+size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t replicates) {
+  int cols = length * replicates;
+  int cols_pad = (cols + 31) / 32 * 32;
+  return ws_bytes((size_t)dim * cols_pad, 4) + ws_bytes(1, 8) +
+         ws_bytes(fixup_cap(n, cols), 8) + 1024;
+}
+
+int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const double *d_norms,
+               const double *d_r, const double *d_rnorm, int32_t length, int32_t replicates,
+               uint64_t *d_codes, void *d_workspace, size_t workspace_bytes, int64_t *h_fixups,
+               void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || dim < 1 || length < 1 || replicates < 1)
+    return arg_error("eg_project: bad shape");
+  if ((int64_t)length * replicates >= (1ll << 31) || n >= (1ll << 32))
+    return arg_error("eg_project: too large");
+  const int W = (length + 63) / 64;
+  const int cols = length * replicates;
+  const int cols_pad = (cols + 31) / 32 * 32;
+  EG_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)replicates * n * W * 8, st));
+  if (h_fixups) *h_fixups = 0;
+  if (n == 0) return EG_OK;
+  Arena ar(d_workspace, workspace_bytes);
+  float *rt = ar.take<float>((size_t)dim * cols_pad);
+  unsigned long long *cnt = ar.take<unsigned long long>(1);
+  const unsigned long long cap = fixup_cap(n, cols);
+  unsigned long long *items = ar.take<unsigned long long>(cap);
+  if (!rt || !cnt || !items) {
+    set_error("eg_project: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
+  EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
+  {
+    int64_t tot = (int64_t)dim * cols_pad;
+    k_prep_directions<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_r, cols, dim, cols_pad, rt);
+    EG_LAUNCH_CHECK();
+  }
+  FixupList fl{cnt, items, cap};
+  const double tau = projection_tau(dim);
+  const int tn = project_tn(cols);
+  if (x_is_f64)
+    dispatch_project<double>(tn, (const double *)d_x, n, dim, rt, cols, cols_pad, d_norms, d_rnorm,
+                             tau, length, W, d_codes, fl, st);
+  else
+    dispatch_project<float>(tn, (const float *)d_x, n, dim, rt, cols, cols_pad, d_norms, d_rnorm,
+                            tau, length, W, d_codes, fl, st);
+  EG_LAUNCH_CHECK();
+  const unsigned fgrid = (unsigned)num_sms() * 8;
+  if (x_is_f64)
+    k_fixup<double><<<fgrid, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W, d_codes,
+                                           items, cnt, cap, cols, 0);
+  else
+    k_fixup<float><<<fgrid, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W, d_codes,
+                                          items, cnt, cap, cols, 0);
+  EG_LAUNCH_CHECK();
+  unsigned long long hcnt = 0;
+  EG_CUDA_TRY(cudaMemcpyAsync(&hcnt, cnt, 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hcnt > cap) {
+    // Band list overflowed (adversarial data): recompute every sign exactly.
+    EG_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)replicates * n * W * 8, st));
+    if (x_is_f64)
+      k_fixup<double><<<fgrid * 4, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W,
+                                                 d_codes, items, cnt, cap, cols, 1);
+    else
+      k_fixup<float><<<fgrid * 4, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W,
+                                                d_codes, items, cnt, cap, cols, 1);
+    EG_LAUNCH_CHECK();
+  }
+  if (h_fixups) *h_fixups = (int64_t)hcnt;
+  return EG_OK;
+}
+
+// ------------------------------------------------------------------ MSM
+size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates) {
+  (void)length;
+  return msm_layout(n, replicates).bytes;
+}
+
+int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t replicates,
+                 const int32_t *h_block_bounds, int32_t k, int32_t d, const int32_t *h_unit_rep,
+                 const uint64_t *h_unit_mask, int64_t n_units, uint64_t *d_out_keys,
+                 int64_t capacity, int64_t *h_counts, void *d_workspace, size_t workspace_bytes,
+                 void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || n >= (1ll << 32)) return arg_error("eg_msm_pairs: need 1 <= n < 2^32");
+  if (length < 1 || length > EG_MAX_LENGTH)
+    return arg_error("eg_msm_pairs: length outside [1, 256]");
+  if (!(0 <= d && d < k && k <= length) || k > EG_MAX_BLOCKS)
+    return arg_error("eg_msm_pairs: need 0 <= d < k <= min(length, 64)");
+  if (replicates < 1) return arg_error("eg_msm_pairs: replicates < 1");
+  const int W = (length + 63) / 64;
+  if (h_block_bounds[0] != 0 || h_block_bounds[k] != length)
+    return arg_error("eg_msm_pairs: block bounds must span [0, length]");
+  uint8_t b2b[EG_MAX_LENGTH];
+  memset(b2b, 0, sizeof(b2b));
+  for (int b = 0; b < k; ++b) {
+    if (h_block_bounds[b + 1] <= h_block_bounds[b])
+      return arg_error("eg_msm_pairs: block bounds must increase");
+    for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t) b2b[t] = (uint8_t)b;
+  }
+  uint64_t all_bits[4] = {0, 0, 0, 0};
+  for (int t = 0; t < length; ++t) all_bits[t >> 6] |= 1ull << (t & 63);
+
+  MsmLayout lay = msm_layout(n, replicates);
+  Arena ar(d_workspace, workspace_bytes);
+  MsmArgs a;
+  memset(&a, 0, sizeof(a));
+  a.codes = d_codes;
+  a.n = n;
+  a.L = length;
+  a.W = W;
+  a.k = k;
+  a.d = d;
+  a.lgB = lay.lgB;
+  a.reps = replicates;
+  a.counts = ar.take<uint32_t>((size_t)lay.U * lay.B);
+  a.starts = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1));
+  a.cursor = ar.take<uint32_t>((size_t)lay.U * lay.B);
+  a.elems = ar.take<uint64_t>((size_t)lay.U * n);
+  a.gcnt = ar.take<uint32_t>((size_t)lay.U * n);
+  uint8_t *b2b_d = ar.take<uint8_t>(EG_MAX_LENGTH);
+  a.bit2blk = b2b_d;
+  a.ctr = ar.take<unsigned long long>(3 + 2 * (size_t)replicates);
+  a.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 3);
+  a.spill_cap = (int64_t)lay.U * (lay.B + 1);
+  a.out_keys = (unsigned long long *)d_out_keys;
+  a.out_cap = capacity > 0 ? (unsigned long long)capacity : 0ull;
+  if (!a.counts || !a.starts || !a.cursor || !a.elems || !a.gcnt || !b2b_d || !a.ctr || !a.spill) {
+    set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
+    return EG_ERR_WORKSPACE;
+  }
+  EG_CUDA_TRY(cudaMemsetAsync(a.counts, 0, (size_t)lay.U * lay.B * 4, st));
+  EG_CUDA_TRY(cudaMemsetAsync(a.ctr, 0, (3 + 2 * (size_t)replicates) * 8, st));
+  EG_CUDA_TRY(cudaMemcpyAsync(b2b_d, b2b, EG_MAX_LENGTH, cudaMemcpyHostToDevice, st));
+
+  std::vector<UnitBatch> batches;
+  for (int64_t u0 = 0; u0 < n_units; u0 += lay.U) {
+    UnitBatch ub;
+    memset(&ub, 0, sizeof(ub));
+    ub.count = (int)std::min<int64_t>(lay.U, n_units - u0);
+    for (int j = 0; j < ub.count; ++j) {
+      const int rep = h_unit_rep[u0 + j];
+      const uint64_t mb = h_unit_mask[u0 + j];
+      if (rep < 0 || rep >= replicates) return arg_error("eg_msm_pairs: unit replicate out of range");
+      if (__builtin_popcountll(mb) != d || (k < 64 && (mb >> k)))
+        return arg_error("eg_msm_pairs: unit mask must select exactly d of the k blocks");
+      ub.rep[j] = rep;
+      ub.maskbits[j] = mb;
+      for (int w = 0; w < 4; ++w) ub.kept[j][w] = all_bits[w];
+      for (int b = 0; b < k; ++b)
+        if (mb >> b & 1)
+          for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t)
+            ub.kept[j][t >> 6] &= ~(1ull << (t & 63));
+      ub.salt[j] = 0x2545f4914f6cdd1dULL * (uint64_t)(u0 + j + 1);
+    }
+    batches.push_back(ub);
+  }
+  int rc = EG_OK;
+  switch (W) {
+    case 1: rc = msm_run<1>(a, lay, batches, st); break;
+    case 2: rc = msm_run<2>(a, lay, batches, st); break;
+    case 3: rc = msm_run<3>(a, lay, batches, st); break;
+    default: rc = msm_run<4>(a, lay, batches, st); break;
+  }
+  if (rc) return rc;
+  std::vector<unsigned long long> hc(3 + 2 * (size_t)replicates);
+  EG_CUDA_TRY(cudaMemcpyAsync(hc.data(), a.ctr, hc.size() * 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  h_counts[0] = (int64_t)hc[0];
+  h_counts[1] = (int64_t)hc[1];
+  for (int h = 0; h < 2 * replicates; ++h) h_counts[2 + h] = (int64_t)hc[3 + h];
+  if (hc[0] > a.out_cap) {
+    set_error("eg_msm_pairs: %llu pairs exceed capacity %llu", hc[0], a.out_cap);
+    return EG_ERR_CAPACITY;
+  }
+  return EG_OK;
+}
+
+// --------------------------------------------------------- grouped sort
+size_t eg_grouped_sort_workspace(int64_t n, int32_t length) {
+  (void)length;
+  return ws_bytes(n, 8) * 2 + ws_bytes(n, 1) + radix_workspace(n, true) + compact_workspace(n) +
+         4096;
+}
+
+int eg_grouped_sort(const uint64_t *d_codes, int64_t n, int32_t length,
+                    const int32_t *h_block_bounds, int32_t k, uint64_t mask_bits, uint32_t *d_perm,
+                    int64_t *d_bounds, int64_t *h_groups, void *d_workspace,
+                    size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || n >= (1ll << 32)) return arg_error("eg_grouped_sort: need 1 <= n < 2^32");
+  if (length < 1 || length > EG_MAX_LENGTH || k < 1 || k > length || k > EG_MAX_BLOCKS)
+    return arg_error("eg_grouped_sort: bad length/k");
+  const int W = (length + 63) / 64;
+  UnitBatch ub;
+  memset(&ub, 0, sizeof(ub));
+  ub.count = 1;
+  for (int t = 0; t < length; ++t) ub.kept[0][t >> 6] |= 1ull << (t & 63);
+  for (int b = 0; b < k; ++b)
+    if (mask_bits >> b & 1)
+      for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t)
+        ub.kept[0][t >> 6] &= ~(1ull << (t & 63));
+  Arena ar(d_workspace, workspace_bytes);
+  uint64_t *keyw = ar.take<uint64_t>(n);
+  uint64_t *idx = ar.take<uint64_t>(n);
+  uint8_t *flags = ar.take<uint8_t>(n);
+  if (!keyw || !idx || !flags) return EG_ERR_WORKSPACE;
+  const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
+  k_iota<<<grid, 256, 0, st>>>(d_perm, n);
+  EG_LAUNCH_CHECK();
+  size_t mark = ar.used;
+  for (int w = W - 1; w >= 0; --w) {
+    const uint64_t kw = ub.kept[0][w];
+    if (!kw) continue;
+    k_masked_word<<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, w, kw, keyw);
+    EG_LAUNCH_CHECK();
+    int shifts[8], np = 0;
+    for (int s = 0; s < 64; s += 8)
+      if ((kw >> s) & 0xff) shifts[np++] = s;
+    ar.used = mark;
+    int rc = radix_sort(keyw, d_perm, n, shifts, np, ar, st);
+    if (rc) return rc;
+  }
+  ar.used = mark;
+  k_group_flags<4><<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, ub, flags, idx);
+  EG_LAUNCH_CHECK();
+  int64_t groups = 0;
+  int rc = compact<uint32_t>(idx, (const uint32_t *)nullptr, flags, n, (uint64_t *)d_bounds,
+                             (uint32_t *)nullptr, &groups, ar, st);
+  if (rc) return rc;
+  int64_t nn = n;
+  EG_CUDA_TRY(cudaMemcpyAsync(d_bounds + groups, &nn, 8, cudaMemcpyHostToDevice, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  *h_groups = groups;
+  return EG_OK;
+}
+
+// -------------------------------------------------------- first witness
+int eg_first_witness(const uint64_t *d_keys, int64_t m, const uint64_t *const *d_pools,
+                     int32_t n_pools, int32_t W, int32_t d, uint8_t *d_keep, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m <= 0) return EG_OK;
+  unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, 8192);
+  k_first_witness<<<grid, 256, 0, st>>>(d_keys, m, d_pools, n_pools, W, d, d_keep);
+  EG_LAUNCH_CHECK();
+  return EG_OK;
+}
+
+// ----------------------------------------------------------------- sort
+size_t eg_sort_workspace(int64_t m, int with_values) { return radix_workspace(m, with_values != 0); }
+
+int eg_sort_keys(uint64_t *d_keys, uint32_t *d_vals, int64_t m, int32_t key_bits,
+                 void *d_workspace, size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (key_bits < 0 || key_bits > 64) return arg_error("eg_sort_keys: key_bits outside [0, 64]");
+  int shifts[8], np = 0;
+  for (int s = 0; s < key_bits; s += 8) shifts[np++] = s;
+  Arena ar(d_workspace, workspace_bytes);
+  return radix_sort(d_keys, d_vals, m, shifts, np, ar, st);
+}
+
+int eg_sort_pair_keys(uint64_t *d_keys, int64_t m, int64_t n, void *d_workspace,
+                      size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int shifts[8];
+  int np = pair_key_shifts(n, shifts);
+  Arena ar(d_workspace, workspace_bytes);
+  return radix_sort(d_keys, nullptr, m, shifts, np, ar, st);
+}
+
+// ------------------------------------------------------------ compaction
+size_t eg_compact_workspace(int64_t m) { return compact_workspace(m); }
+
+int eg_compact_keys(const uint64_t *d_keys, const uint8_t *d_flags, int64_t m, uint64_t *d_out,
+                    int64_t *h_count, void *d_workspace, size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  Arena ar(d_workspace, workspace_bytes);
+  return compact<uint32_t>(d_keys, (const uint32_t *)nullptr, d_flags, m, d_out,
+                           (uint32_t *)nullptr, h_count, ar, st);
+}
+
+// --------------------------------------------------------------- verify
+size_t eg_verify_workspace(int64_t m) {
+  return ws_bytes(m, 1) + ws_bytes(m, 8) + ws_bytes(1, 8) + compact_workspace(m) + 1024;
+}
+
+int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const double *d_norms,
+              const uint64_t *d_keys, int64_t m, int32_t metric, double eps, uint64_t *d_out_keys,
+              double *d_out_dist, int64_t *h_count, void *d_workspace, size_t workspace_bytes,
+              void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *h_count = 0;
+  if (m <= 0) return EG_OK;
+  if (metric != EG_METRIC_COSINE && metric != EG_METRIC_EUCLIDEAN)
+    return arg_error("eg_verify: unknown metric");
+  Arena ar(d_workspace, workspace_bytes);
+  uint8_t *flags = ar.take<uint8_t>(m);
+  double *dist = ar.take<double>(m);
+  unsigned long long *bad = ar.take<unsigned long long>(1);
+  if (!flags || !dist || !bad) return EG_ERR_WORKSPACE;
+  EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 8, st));
+  unsigned grid = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)num_sms() * 64);
+  if (x_is_f64)
+    k_verify<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, d_keys, m,
+                                           metric, eps, flags, dist, bad);
+  else
+    k_verify<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m, metric,
+                                          eps, flags, dist, bad);
+  EG_LAUNCH_CHECK();
+  int rc = compact<double>(d_keys, dist, flags, m, d_out_keys, d_out_dist, h_count, ar, st);
+  if (rc) return rc;
+  unsigned long long hb = 0;
+  EG_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hb != ~0ull) {
+    set_error("eg_verify: candidate %llu has an index out of range", hb);
+    return EG_ERR_ARG;
+  }
+  return EG_OK;
+}
+
+}  // extern "C"

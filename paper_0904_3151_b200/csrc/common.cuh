@@ -1,0 +1,148 @@
+// common.cuh -- shared device helpers for the eps-graph kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "../../include/epsgraph_b200.h"
+
+namespace eg {
+
+// ---------------------------------------------------------------- errors
+void set_error(const char *fmt, ...);
+
+#define EG_CUDA_TRY(expr)                                                     \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess) {                                                  \
+      ::eg::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,              \
+                      cudaGetErrorString(_e));                                \
+      return EG_ERR_CUDA;                                                     \
+    }                                                                         \
+  } while (0)
+
+#define EG_LAUNCH_CHECK() EG_CUDA_TRY(cudaGetLastError())
+
+// ------------------------------------------------------------- workspace
+// Bump allocator over the caller's workspace (256-byte aligned slices).
+struct Arena {
+  char *base;
+  size_t size, used;
+  __host__ Arena(void *b, size_t s) : base((char *)b), size(s), used(0) {}
+  template <typename T>
+  __host__ T *take(size_t count) {
+    size_t bytes = (count * sizeof(T) + 255) & ~size_t(255);
+    if (used + bytes > size) return nullptr;
+    T *p = reinterpret_cast<T *>(base + used);
+    used += bytes;
+    return p;
+  }
+};
+__host__ inline size_t ws_bytes(size_t count, size_t elem) {
+  return (count * elem + 255) & ~size_t(255);
+}
+
+// ----------------------------------------------------------------- hashing
+// 64-bit finaliser (murmur3 fmix64): equal keys -> equal hashes; distinct
+// keys spread uniformly, so hash digits give balanced buckets even when the
+// LSH bits themselves are heavily skewed (all-positive data, config 3).
+__device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+  z ^= z >> 33;
+  z *= 0xff51afd7ed558ccdULL;
+  z ^= z >> 33;
+  z *= 0xc4ceb9fe1a85ec53ULL;
+  z ^= z >> 33;
+  return z;
+}
+
+template <int W>
+__device__ __forceinline__ uint64_t hash_key(const uint64_t (&c)[W], const uint64_t *kept,
+                                             uint64_t salt) {
+  uint64_t h = salt;
+#pragma unroll
+  for (int w = 0; w < W; ++w) h = fmix64(h ^ (c[w] & kept[w]) ^ (0x9e3779b97f4a7c15ULL * (w + 1)));
+  return h;
+}
+
+// ------------------------------------------------------------ block scan
+// Exclusive scan of one value per thread over the CTA; returns the total.
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t &total,
+                                                         uint32_t *smem_warp /*[NT/32]*/) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t s = lane < NT / 32 ? smem_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) smem_warp[lane] = s;
+  }
+  __syncthreads();
+  total = smem_warp[NT / 32 - 1];
+  uint32_t warp_base = wid ? smem_warp[wid - 1] : 0;
+  __syncthreads();
+  return warp_base + x - v;
+}
+
+template <int NT>
+__device__ __forceinline__ unsigned long long block_exclusive_scan64(
+    unsigned long long v, unsigned long long &total, unsigned long long *smem_warp) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    unsigned long long s = lane < NT / 32 ? smem_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) smem_warp[lane] = s;
+  }
+  __syncthreads();
+  total = smem_warp[NT / 32 - 1];
+  unsigned long long warp_base = wid ? smem_warp[wid - 1] : 0;
+  __syncthreads();
+  return warp_base + x - v;
+}
+
+// Warp-aggregated append: every converged lane with `pred` gets a unique
+// slot (safe inside divergent loops: only the currently active lanes vote).
+__device__ __forceinline__ unsigned long long warp_append(bool pred,
+                                                          unsigned long long *counter) {
+  const unsigned active = __activemask();
+  const unsigned mask = __ballot_sync(active, pred);
+  const int lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (mask) {
+    const int leader = __ffs(mask) - 1;
+    if (lane == leader) base = atomicAdd(counter, (unsigned long long)__popc(mask));
+    base = __shfl_sync(active, base, leader);
+  }
+  return base + __popc(mask & ((1u << lane) - 1u));
+}
+
+__host__ __device__ inline int ilog2_ceil(uint64_t v) {
+  int l = 0;
+  while ((1ull << l) < v) ++l;
+  return l;
+}
+
+}  // namespace eg

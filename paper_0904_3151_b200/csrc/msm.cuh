@@ -1,0 +1,612 @@
+// msm.cuh -- the multiple sorting method on B200: per-(replicate, mask) unit
+// masked sort, group detection and in-group pair enumeration.
+//
+// Reference (hamming_join.py): masked_key_table (bitpool.py:224-253) ->
+// LSD counting passes (_counting_pass :52-82) -> _group_bounds (:85-101) ->
+// _emit_group_pairs (:104-149), one mask at a time (:339), then the
+// cross-replicate first-witness fold (pipeline.py:286-314).
+//
+// B200 design (per batch of up to MSM_MAXU units sharing one launch):
+//  1. k_msm_hist    : masked key -> 64-bit hash; the top lgB bits are an MSD
+//                     radix digit ("coarse bucket").  Shared-memory digit
+//                     histograms, one global atomic per (CTA, digit).
+//  2. k_msm_scan    : bucket offsets (exclusive scan), cursors reset.
+//  3. k_msm_scatter : stable-enough MSD scatter of (h2 << 32 | row) into the
+//                     buckets (only grouping matters, as in the reference,
+//                     whose bucket order is first-seen, not lexicographic).
+//  4. k_msm_group   : one CTA per bucket, entirely in shared memory: counting
+//                     sort on the next hash digits, run detection (equal
+//                     keys are exactly the runs), code gather for multi-row
+//                     runs only, then a flattened, load-balanced pair loop
+//                     with popcount <= d, the O(1) canonical-mask rule and
+//                     the cross-replicate rule, warp-aggregated emission.
+//  5. k_msm_spill   : buckets larger than the shared-memory capacity (giant
+//                     groups) are enumerated by 128x128 tile pairs.
+// Equal masked keys always share a bucket and a run, so every reference
+// group is visited; hash collisions are filtered by an exact key compare.
+#pragma once
+
+#include "common.cuh"
+
+namespace eg {
+
+constexpr int MSM_MAXU = 16;            // units per launch batch
+constexpr int MSM_IPT = 8;              // items per thread, hist/scatter
+constexpr int MSM_NT = 512;             // threads, hist/scatter
+constexpr int MSM_TILE = MSM_IPT * MSM_NT;
+constexpr int MSM_GNT = 256;            // threads, group kernel
+constexpr int MSM_CAP = 2048;           // shared-memory bucket capacity
+constexpr int MSM_TARGET = 512;         // target mean bucket size
+constexpr int MSM_SPILL_T = 128;        // spill tile edge
+constexpr int MSM_MAX_LGB = 13;         // at most 8192 buckets per unit
+
+struct UnitBatch {
+  int count;
+  int rep[MSM_MAXU];
+  unsigned long long maskbits[MSM_MAXU];
+  unsigned long long kept[MSM_MAXU][4];
+  unsigned long long salt[MSM_MAXU];
+};
+
+struct MsmArgs {
+  const uint64_t *codes;         // [reps][n][W]
+  int64_t n;
+  int L, W, k, d, lgB, reps;
+  uint32_t *counts;              // [MAXU][B]
+  uint32_t *starts;              // [MAXU][B+1]
+  uint32_t *cursor;              // [MAXU][B]
+  uint64_t *elems;               // [MAXU][n]
+  uint32_t *gcnt;                // [MAXU][n] (spill group counts)
+  const uint8_t *bit2blk;        // [EG_MAX_LENGTH]
+  unsigned long long *out_keys;
+  unsigned long long out_cap;
+  unsigned long long *ctr;       // [0] emitted, [1] max group, [2] spill count,
+                                 // [3..3+reps) raw, [3+reps..) new
+  uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
+  int64_t spill_cap;
+};
+
+template <int W>
+__device__ __forceinline__ void load_code(const uint64_t *__restrict__ codes, int64_t row,
+                                          uint64_t (&c)[W]) {
+  if (W == 1) {
+    c[0] = __ldg(codes + row);
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) c[w] = __ldg(codes + row * W + w);
+  }
+}
+
+// ------------------------------------------------------------------ 1
+template <int W>
+__global__ void __launch_bounds__(MSM_NT) k_msm_hist(const __grid_constant__ MsmArgs a,
+                                                         const __grid_constant__ UnitBatch ub) {
+  extern __shared__ uint32_t hist[];
+  const int u = blockIdx.y;
+  const int B = 1 << a.lgB;
+  for (int i = threadIdx.x; i < B; i += MSM_NT) hist[i] = 0;
+  __syncthreads();
+  const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
+  const unsigned long long *kept = ub.kept[u];
+  const uint64_t salt = ub.salt[u];
+  const int sh = 64 - a.lgB;
+  const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
+#pragma unroll
+  for (int i = 0; i < MSM_IPT; ++i) {
+    int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
+    if (row < a.n) {
+      uint64_t c[W];
+      load_code<W>(codes, row, c);
+      uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
+      uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
+      atomicAdd(&hist[b], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t *cnt = a.counts + (int64_t)u * B;
+  for (int i = threadIdx.x; i < B; i += MSM_NT)
+    if (hist[i]) atomicAdd(&cnt[i], hist[i]);
+}
+
+// ------------------------------------------------------------------ 2
+__global__ void __launch_bounds__(1024) k_msm_scan(const __grid_constant__ MsmArgs a) {
+  __shared__ uint32_t sw[32];
+  const int u = blockIdx.x;
+  const int B = 1 << a.lgB;
+  uint32_t *cnt = a.counts + (int64_t)u * B;
+  uint32_t *st = a.starts + (int64_t)u * (B + 1);
+  uint32_t *cur = a.cursor + (int64_t)u * B;
+  const int per = (B + 1023) / 1024;
+  uint32_t local = 0;
+  for (int i = 0; i < per; ++i) {
+    int b = threadIdx.x * per + i;
+    if (b < B) local += cnt[b];
+  }
+  uint32_t tot;
+  uint32_t run = block_exclusive_scan<1024>(local, tot, sw);
+  for (int i = 0; i < per; ++i) {
+    int b = threadIdx.x * per + i;
+    if (b < B) {
+      uint32_t c = cnt[b];
+      st[b] = run;
+      cur[b] = run;
+      cnt[b] = 0;
+      run += c;
+    }
+  }
+  if (threadIdx.x == 0) st[B] = tot;
+  if (u == 0 && threadIdx.x == 0) a.ctr[2] = 0;   // spill list reset for this batch
+}
+
+// ------------------------------------------------------------------ 3
+template <int W>
+__global__ void __launch_bounds__(MSM_NT) k_msm_scatter(const __grid_constant__ MsmArgs a,
+                                                            const __grid_constant__ UnitBatch ub) {
+  extern __shared__ uint32_t sm[];
+  const int u = blockIdx.y;
+  const int B = 1 << a.lgB;
+  uint32_t *hist = sm;
+  uint32_t *bbase = sm + B;
+  for (int i = threadIdx.x; i < B; i += MSM_NT) hist[i] = 0;
+  __syncthreads();
+  const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
+  const unsigned long long *kept = ub.kept[u];
+  const uint64_t salt = ub.salt[u];
+  const int sh = 64 - a.lgB;
+  const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
+  uint32_t bk[MSM_IPT], rk[MSM_IPT], h2[MSM_IPT];
+#pragma unroll
+  for (int i = 0; i < MSM_IPT; ++i) {
+    int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
+    bk[i] = 0xffffffffu;
+    if (row < a.n) {
+      uint64_t c[W];
+      load_code<W>(codes, row, c);
+      uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
+      bk[i] = a.lgB ? (uint32_t)(h >> sh) : 0u;
+      h2[i] = (uint32_t)h;
+      rk[i] = atomicAdd(&hist[bk[i]], 1u);
+    }
+  }
+  __syncthreads();
+  uint32_t *cur = a.cursor + (int64_t)u * B;
+  for (int i = threadIdx.x; i < B; i += MSM_NT) {
+    uint32_t c = hist[i];
+    bbase[i] = c ? atomicAdd(&cur[i], c) : 0u;
+  }
+  __syncthreads();
+  uint64_t *el = a.elems + (int64_t)u * a.n;
+#pragma unroll
+  for (int i = 0; i < MSM_IPT; ++i) {
+    int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
+    if (row < a.n) el[bbase[bk[i]] + rk[i]] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
+  }
+}
+
+// ------------------------------------------------------- pair predicate
+// Canonical mask of a differing-bit pattern x (popcount(x) <= d): the blocks
+// where the pair differs, filled up with the smallest untouched blocks --
+// the lexicographically first d-subset containing them, i.e. the first mask
+// (itertools.combinations order, hamming_join.py:333) under which the
+// reference's _emit_group_pairs (hamming_join.py:130-141) emits the pair.
+template <int W>
+__device__ __forceinline__ uint64_t canonical_mask(const uint64_t (&x)[W], const uint8_t *b2b,
+                                                   int k, int d) {
+  uint64_t delta = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    uint64_t y = x[w];
+    while (y) {
+      int t = __ffsll((long long)y) - 1;
+      delta |= 1ull << b2b[w * 64 + t];
+      y &= y - 1;
+    }
+  }
+  int need = d - __popcll(delta);
+  uint64_t comp = ~delta & (k == 64 ? ~0ull : ((1ull << k) - 1));
+  for (int i = 0; i < need; ++i) {
+    uint64_t low = comp & (~comp + 1);
+    delta |= low;
+    comp ^= low;
+  }
+  return delta;
+}
+
+// Full predicate for one in-group pair.  Returns 0 = rejected, 1 = raw only
+// (an earlier replicate owns it), 2 = emit.
+template <int W>
+__device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint64_t (&cb)[W],
+                                            uint32_t ra, uint32_t rb, const MsmArgs &a,
+                                            const unsigned long long *kept, uint64_t maskbits,
+                                            int rep, const uint8_t *b2b) {
+  uint64_t x[W];
+  int pc = 0;
+  uint64_t keydiff = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    x[w] = ca[w] ^ cb[w];
+    pc += __popcll(x[w]);
+    keydiff |= x[w] & kept[w];
+  }
+  if (keydiff || pc > a.d) return 0;
+  if (canonical_mask<W>(x, b2b, a.k, a.d) != maskbits) return 0;
+  for (int g = 0; g < rep; ++g) {
+    const uint64_t *cg = a.codes + (int64_t)g * a.n * W;
+    int pg = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      pg += __popcll(__ldg(cg + (int64_t)ra * W + w) ^ __ldg(cg + (int64_t)rb * W + w));
+    if (pg <= a.d) return 1;
+  }
+  return 2;
+}
+
+__device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia, uint32_t &ib) {
+  // pairs (0,1),(0,2),..,(0,c-1),(1,2),...; T(a) = a*c - a*(a+1)/2
+  float disc = (float)(2 * c - 1) * (float)(2 * c - 1) - 8.0f * (float)q;
+  int ai = (int)floorf(((float)(2 * c - 1) - sqrtf(fmaxf(disc, 0.f))) * 0.5f);
+  ai = max(0, min(ai, (int)c - 2));
+  auto T = [c](int x) { return (uint32_t)x * c - (uint32_t)x * (uint32_t)(x + 1) / 2; };
+  while (ai > 0 && T(ai) > q) --ai;
+  while (ai + 1 <= (int)c - 2 && T(ai + 1) <= q) ++ai;
+  ia = (uint32_t)ai;
+  ib = q - T(ai) + ai + 1;
+}
+
+// ------------------------------------------------------------------ 4
+template <int W>
+struct GroupSmem {
+  uint64_t A[MSM_CAP * W];        // bucket elements, later gathered codes
+  uint64_t Bv[MSM_CAP];           // elements ordered by fine digit / runs
+  uint32_t off[2 * MSM_CAP + 1];  // fine-digit offsets
+  uint32_t runs[MSM_CAP / 2];     // (start << 16) | len
+  uint32_t pp[MSM_CAP / 2 + 1];   // pair prefix per run
+  uint8_t inrun[MSM_CAP];
+  uint8_t b2b[EG_MAX_LENGTH];
+  uint32_t sw[MSM_GNT / 32];
+  uint32_t nruns, maxrun, raw, neu;
+};
+
+template <int W>
+__global__ void __launch_bounds__(MSM_GNT) k_msm_group(const __grid_constant__ MsmArgs a,
+                                                            const __grid_constant__ UnitBatch ub) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  GroupSmem<W> &S = *reinterpret_cast<GroupSmem<W> *>(smraw);
+  const int u = blockIdx.y;
+  const int b = blockIdx.x;
+  const int B = 1 << a.lgB;
+  const uint32_t *st = a.starts + (int64_t)u * (B + 1);
+  const uint32_t s0 = st[b], s = st[b + 1] - s0;
+  if (s < 2) return;
+  if (s > MSM_CAP) {
+    if (threadIdx.x == 0) {
+      unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+      if ((int64_t)slot < a.spill_cap) {
+        a.spill[slot * 3 + 0] = (uint32_t)u;
+        a.spill[slot * 3 + 1] = s0;
+        a.spill[slot * 3 + 2] = s;
+      }
+    }
+    if ((int64_t)s * 4 > a.n) {   // reference-visible group size check
+      uint32_t *g = a.gcnt + (int64_t)u * a.n + s0;
+      for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) g[i] = 0;
+    }
+    return;
+  }
+  const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
+  const int rep = ub.rep[u];
+  const int lgF = max(1, ilog2_ceil(2ull * s));
+  const uint32_t F = 1u << lgF;
+  for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) S.A[i] = el[i];
+  for (uint32_t i = threadIdx.x; i <= F; i += MSM_GNT) S.off[i] = 0;
+  for (int i = threadIdx.x; i < a.L; i += MSM_GNT) S.b2b[i] = a.bit2blk[i];
+  if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; }
+  __syncthreads();
+  // fine digit = top lgF bits of h2 (independent of the bucket digit)
+  constexpr int PT = MSM_CAP / MSM_GNT;
+  uint32_t rk[PT];
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    uint32_t i = threadIdx.x + j * MSM_GNT;
+    if (i < s) rk[j] = atomicAdd(&S.off[(uint32_t)(S.A[i] >> 32) >> (32 - lgF)], 1u);
+  }
+  __syncthreads();
+  {  // exclusive scan of F counts (blocked, F/GNT per thread)
+    const uint32_t per = (F + MSM_GNT - 1) / MSM_GNT;
+    uint32_t loc = 0;
+    for (uint32_t j = 0; j < per; ++j) {
+      uint32_t f = threadIdx.x * per + j;
+      if (f < F) loc += S.off[f];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<MSM_GNT>(loc, tot, S.sw);
+    for (uint32_t j = 0; j < per; ++j) {
+      uint32_t f = threadIdx.x * per + j;
+      if (f < F) {
+        uint32_t c = S.off[f];
+        S.off[f] = run;
+        run += c;
+      }
+    }
+    if (threadIdx.x == 0) S.off[F] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    uint32_t i = threadIdx.x + j * MSM_GNT;
+    if (i < s) {
+      uint64_t e = S.A[i];
+      S.Bv[S.off[(uint32_t)(e >> 32) >> (32 - lgF)] + rk[j]] = e;
+    }
+  }
+  for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) S.inrun[i] = 0;
+  __syncthreads();
+  // runs: one thread per multi-row digit bin; sort the bin by (h2,row) if
+  // it mixes hashes (insertion sort, bins are tiny), then split into runs.
+  for (uint32_t f = threadIdx.x; f < F; f += MSM_GNT) {
+    const uint32_t lo = S.off[f], hi = S.off[f + 1];
+    if (hi - lo < 2) continue;
+    const uint32_t h0 = (uint32_t)(S.Bv[lo] >> 32);
+    bool mixed = false;
+    for (uint32_t i = lo + 1; i < hi; ++i) mixed |= (uint32_t)(S.Bv[i] >> 32) != h0;
+    if (mixed) {
+      for (uint32_t i = lo + 1; i < hi; ++i) {
+        uint64_t v = S.Bv[i];
+        uint32_t j = i;
+        while (j > lo && (S.Bv[j - 1] >> 32) > (v >> 32)) { S.Bv[j] = S.Bv[j - 1]; --j; }
+        S.Bv[j] = v;
+      }
+    }
+    uint32_t rs = lo;
+    while (rs < hi) {
+      uint32_t re = rs + 1;
+      const uint32_t hr = (uint32_t)(S.Bv[rs] >> 32);
+      while (re < hi && (uint32_t)(S.Bv[re] >> 32) == hr) ++re;
+      const uint32_t len = re - rs;
+      if (len >= 2) {
+        uint32_t slot = atomicAdd(&S.nruns, 1u);
+        S.runs[slot] = (rs << 16) | len;
+        atomicMax(&S.maxrun, len);
+        for (uint32_t i = rs; i < re; ++i) S.inrun[i] = 1;
+      }
+      rs = re;
+    }
+  }
+  __syncthreads();
+  const uint32_t R = S.nruns;
+  // gather codes of rows that sit in runs (A is free now)
+  const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
+  for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) {
+    if (S.inrun[i]) {
+      const uint32_t row = (uint32_t)S.Bv[i];
+#pragma unroll
+      for (int w = 0; w < W; ++w) S.A[i * W + w] = __ldg(codes + (int64_t)row * W + w);
+    }
+  }
+  {  // pair prefix over runs
+    const uint32_t per = (R + MSM_GNT - 1) / MSM_GNT;
+    uint32_t loc = 0;
+    for (uint32_t j = 0; j < per; ++j) {
+      uint32_t r = threadIdx.x * per + j;
+      if (r < R) {
+        uint32_t len = S.runs[r] & 0xffffu;
+        loc += len * (len - 1) / 2;
+      }
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<MSM_GNT>(loc, tot, S.sw);
+    for (uint32_t j = 0; j < per; ++j) {
+      uint32_t r = threadIdx.x * per + j;
+      if (r < R) {
+        S.pp[r] = run;
+        uint32_t len = S.runs[r] & 0xffffu;
+        run += len * (len - 1) / 2;
+      }
+    }
+    if (threadIdx.x == 0) S.pp[R] = tot;
+  }
+  __syncthreads();
+  const uint32_t P = S.pp[R];
+  const unsigned long long *kept = ub.kept[u];
+  const uint64_t maskbits = ub.maskbits[u];
+  uint32_t my_raw = 0, my_new = 0;
+  for (uint32_t p = threadIdx.x; p < P; p += MSM_GNT) {
+    uint32_t lo = 0, hi = R;  // find r: pp[r] <= p < pp[r+1]
+    while (hi - lo > 1) {
+      uint32_t mid = (lo + hi) >> 1;
+      if (S.pp[mid] <= p) lo = mid; else hi = mid;
+    }
+    const uint32_t rr = S.runs[lo];
+    const uint32_t start = rr >> 16, len = rr & 0xffffu;
+    uint32_t ia, ib;
+    tri_decode(p - S.pp[lo], len, ia, ib);
+    ia += start;
+    ib += start;
+    uint64_t ca[W], cb[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) { ca[w] = S.A[ia * W + w]; cb[w] = S.A[ib * W + w]; }
+    const uint32_t ra = (uint32_t)S.Bv[ia], rb = (uint32_t)S.Bv[ib];
+    int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
+    my_raw += v > 0;
+    my_new += v == 2;
+    const bool emit = v == 2;
+    unsigned long long slot = warp_append(emit, &a.ctr[0]);
+    if (emit && slot < a.out_cap) {
+      uint32_t lo_r = min(ra, rb), hi_r = max(ra, rb);
+      a.out_keys[slot] = ((unsigned long long)lo_r << 32) | hi_r;
+    }
+  }
+  if (my_raw) atomicAdd(&S.raw, my_raw);
+  if (my_new) atomicAdd(&S.neu, my_new);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (S.raw) atomicAdd(&a.ctr[3 + rep], (unsigned long long)S.raw);
+    if (S.neu) atomicAdd(&a.ctr[3 + a.reps + rep], (unsigned long long)S.neu);
+    atomicMax(&a.ctr[1], (unsigned long long)S.maxrun);
+  }
+}
+
+// ------------------------------------------------------------------ 5
+// Oversized buckets: all pairs by 128 x 128 tile pairs, grid-strided.  A
+// bucket of size s costs O(s^2) hash compares -- the same order as the
+// reference's in-group visits for the giant group that caused the spill.
+template <int W>
+__global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant__ MsmArgs a,
+                                                                const __grid_constant__ UnitBatch ub) {
+  __shared__ uint64_t ea[MSM_SPILL_T], eb[MSM_SPILL_T];
+  __shared__ uint64_t cb_s[MSM_SPILL_T * W];
+  __shared__ uint8_t b2b[EG_MAX_LENGTH];
+  __shared__ uint32_t sraw, sneu;
+  for (int i = threadIdx.x; i < a.L; i += MSM_SPILL_T) b2b[i] = a.bit2blk[i];
+  const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
+  for (unsigned long long sb = 0; sb < nspill; ++sb) {
+    const int u = (int)a.spill[sb * 3 + 0];
+    const uint32_t s0 = a.spill[sb * 3 + 1], s = a.spill[sb * 3 + 2];
+    const uint32_t nt = (s + MSM_SPILL_T - 1) / MSM_SPILL_T;
+    const unsigned long long ntp = (unsigned long long)nt * (nt + 1) / 2;
+    const int rep = ub.rep[u];
+    const unsigned long long *kept = ub.kept[u];
+    const uint64_t maskbits = ub.maskbits[u];
+    const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
+    const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
+    const bool count_groups = (int64_t)s * 4 > a.n;
+    uint32_t *gc = a.gcnt + (int64_t)u * a.n + s0;
+    for (unsigned long long tp = blockIdx.x; tp < ntp; tp += gridDim.x) {
+      // decode tile pair (ta <= tb), row-major over the upper triangle
+      uint32_t ta = 0;
+      {
+        double dd = (double)(2 * nt + 1);
+        double disc = dd * dd - 8.0 * (double)tp;
+        ta = (uint32_t)floor((dd - sqrt(disc > 0 ? disc : 0)) * 0.5);
+        auto T = [nt](unsigned long long x) { return x * nt - x * (x - 1) / 2; };
+        while (ta > 0 && T(ta) > tp) --ta;
+        while (ta + 1 < nt && T(ta + 1) <= tp) ++ta;
+      }
+      const uint32_t tb = ta + (uint32_t)(tp - ((unsigned long long)ta * nt -
+                                                  (unsigned long long)ta * (ta - 1) / 2));
+      __syncthreads();
+      if (threadIdx.x == 0) { sraw = 0; sneu = 0; }
+      const uint32_t ia0 = ta * MSM_SPILL_T, ib0 = tb * MSM_SPILL_T;
+      {
+        uint32_t i = threadIdx.x;
+        ea[i] = ia0 + i < s ? el[ia0 + i] : ~0ull;
+        eb[i] = ib0 + i < s ? el[ib0 + i] : ~0ull;
+        if (ib0 + i < s) {
+          const uint32_t row = (uint32_t)eb[i];
+#pragma unroll
+          for (int w = 0; w < W; ++w) cb_s[i * W + w] = __ldg(codes + (int64_t)row * W + w);
+        }
+      }
+      __syncthreads();
+      const uint32_t i = threadIdx.x;
+      uint32_t my_raw = 0, my_new = 0, my_eq = 0;
+      if (ia0 + i < s) {
+        const uint64_t e = ea[i];
+        const uint32_t h2 = (uint32_t)(e >> 32), ra = (uint32_t)e;
+        uint64_t ca[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) ca[w] = __ldg(codes + (int64_t)ra * W + w);
+        const uint32_t jlo = (ta == tb) ? i + 1 : 0;
+        for (uint32_t j = jlo; j < MSM_SPILL_T; ++j) {
+          const uint64_t f = eb[j];
+          bool emit = false;
+          if (ib0 + j < s && (uint32_t)(f >> 32) == h2) {
+            uint64_t cb[W];
+            uint64_t kd = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) { cb[w] = cb_s[j * W + w]; kd |= (ca[w] ^ cb[w]) & kept[w]; }
+            if (!kd) {
+              ++my_eq;
+              if (count_groups) atomicAdd(&gc[ib0 + j], 1u);
+              const uint32_t rb = (uint32_t)f;
+              int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, b2b);
+              my_raw += v > 0;
+              my_new += v == 2;
+              emit = v == 2;
+              if (emit) {
+                unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
+                if (slot < a.out_cap)
+                  a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+              }
+            }
+          }
+        }
+        if (count_groups && my_eq) atomicAdd(&gc[ia0 + i], my_eq);
+      }
+      if (my_raw) atomicAdd(&sraw, my_raw);
+      if (my_new) atomicAdd(&sneu, my_new);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (sraw) atomicAdd(&a.ctr[3 + rep], (unsigned long long)sraw);
+        if (sneu) atomicAdd(&a.ctr[3 + a.reps + rep], (unsigned long long)sneu);
+      }
+    }
+  }
+}
+
+// Largest group inside spilled buckets that could trip the reference's
+// oversized warning (hamming_join.py:341-344): max(gcnt) + 1.
+__global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
+  const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
+  for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
+    const int u = (int)a.spill[sb * 3 + 0];
+    const uint32_t s0 = a.spill[sb * 3 + 1], s = a.spill[sb * 3 + 2];
+    if ((int64_t)s * 4 <= a.n) continue;
+    const uint32_t *gc = a.gcnt + (int64_t)u * a.n + s0;
+    uint32_t mx = 0;
+    for (uint32_t i = threadIdx.x; i < s; i += blockDim.x) mx = max(mx, gc[i]);
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(&a.ctr[1], (unsigned long long)mx + 1);
+  }
+}
+
+// ------------------------------------------------------ first witness
+__global__ void k_first_witness(const uint64_t *__restrict__ keys, int64_t m,
+                                const uint64_t *const *__restrict__ pools, int npools, int W,
+                                int d, uint8_t *__restrict__ keep) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[p];
+    const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+    uint8_t ok = 1;
+    for (int g = 0; g < npools && ok; ++g) {
+      int pc = 0;
+      for (int w = 0; w < W; ++w) pc += __popcll(pools[g][i * W + w] ^ pools[g][j * W + w]);
+      if (pc <= d) ok = 0;
+    }
+    keep[p] = ok;
+  }
+}
+
+// ------------------------------------------------------- grouped sort API
+__global__ void k_masked_word(const uint64_t *__restrict__ codes, const uint32_t *__restrict__ perm,
+                              int64_t n, int W, int w, uint64_t kept, uint64_t *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = codes[(int64_t)perm[i] * W + w] & kept;
+}
+
+__global__ void k_iota(uint32_t *__restrict__ p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (uint32_t)i;
+}
+
+template <int WMAX>
+__global__ void k_group_flags(const uint64_t *__restrict__ codes, const uint32_t *__restrict__ perm,
+                              int64_t n, int W, const __grid_constant__ UnitBatch ub, uint8_t *__restrict__ flags,
+                              uint64_t *__restrict__ idx) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    bool start = i == 0;
+    if (!start) {
+      const int64_t ra = perm[i - 1], rb = perm[i];
+      for (int w = 0; w < W; ++w)
+        start |= ((codes[ra * W + w] ^ codes[rb * W + w]) & ub.kept[0][w]) != 0;
+    }
+    flags[i] = start;
+    idx[i] = (uint64_t)i;
+  }
+}
+
+}  // namespace eg

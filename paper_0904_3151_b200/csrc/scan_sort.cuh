@@ -1,0 +1,327 @@
+// scan_sort.cuh -- device-wide exclusive scan, stable LSD radix sort and
+// stable compaction (hand-written, sm_100a).
+//
+// These replace the host-side np.lexsort calls of the reference
+// (hamming_join.py:369-375, pipeline.py:222) and provide the prefix sums the
+// count -> allocate -> write kernels need.
+#pragma once
+
+#include "common.cuh"
+
+namespace eg {
+
+// ------------------------------------------------------------------ scan
+// Reduce-then-scan over uint32 (totals must fit in uint32).
+constexpr int SCAN_NT = 256;
+constexpr int SCAN_IPT = 16;
+constexpr int SCAN_TILE = SCAN_NT * SCAN_IPT;
+
+__global__ void __launch_bounds__(SCAN_NT) k_scan_reduce(const uint32_t *__restrict__ in,
+                                                         int64_t L, uint32_t *__restrict__ sums) {
+  __shared__ uint32_t sw[SCAN_NT / 32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    int64_t idx = base + (int64_t)i * SCAN_NT + threadIdx.x;
+    if (idx < L) s += in[idx];
+  }
+  uint32_t tot;
+  block_exclusive_scan<SCAN_NT>(s, tot, sw);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_NT) k_scan_tiles(const uint32_t *__restrict__ in,
+                                                        int64_t L, uint32_t *__restrict__ out,
+                                                        const uint32_t *__restrict__ tile_base) {
+  __shared__ uint32_t sw[SCAN_NT / 32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_TILE;
+  // blocked arrangement: thread t owns [t*IPT, t*IPT+IPT) of the tile
+  uint32_t v[SCAN_IPT];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    int64_t idx = base + (int64_t)threadIdx.x * SCAN_IPT + i;
+    v[i] = idx < L ? in[idx] : 0;
+    s += v[i];
+  }
+  uint32_t tot;
+  uint32_t ex = block_exclusive_scan<SCAN_NT>(s, tot, sw);
+  uint32_t run = ex + (tile_base ? tile_base[blockIdx.x] : 0);
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    int64_t idx = base + (int64_t)threadIdx.x * SCAN_IPT + i;
+    if (idx < L) out[idx] = run;
+    run += v[i];
+  }
+}
+
+__host__ inline size_t scan_workspace(int64_t L) {
+  size_t total = 0;
+  while (L > SCAN_TILE) {
+    int64_t nb = (L + SCAN_TILE - 1) / SCAN_TILE;
+    total += ws_bytes(nb, 4) * 2;
+    L = nb;
+  }
+  return total + 256;
+}
+
+// out[i] = sum_{j<i} in[j]; in/out may alias.  Recursive over tile sums.
+__host__ inline int scan_exclusive_u32(const uint32_t *in, uint32_t *out, int64_t L, Arena &ar,
+                                       cudaStream_t st) {
+  if (L <= 0) return EG_OK;
+  int64_t nb = (L + SCAN_TILE - 1) / SCAN_TILE;
+  if (nb == 1) {
+    k_scan_tiles<<<1, SCAN_NT, 0, st>>>(in, L, out, nullptr);
+    EG_LAUNCH_CHECK();
+    return EG_OK;
+  }
+  uint32_t *sums = ar.take<uint32_t>(nb);
+  uint32_t *sums_x = ar.take<uint32_t>(nb);
+  if (!sums || !sums_x) return EG_ERR_WORKSPACE;
+  k_scan_reduce<<<(unsigned)nb, SCAN_NT, 0, st>>>(in, L, sums);
+  EG_LAUNCH_CHECK();
+  int rc = scan_exclusive_u32(sums, sums_x, nb, ar, st);
+  if (rc) return rc;
+  k_scan_tiles<<<(unsigned)nb, SCAN_NT, 0, st>>>(in, L, out, sums_x);
+  EG_LAUNCH_CHECK();
+  return EG_OK;
+}
+
+// ------------------------------------------------------------ radix sort
+// Stable LSD radix sort, 8-bit digits.  Per pass: upsweep (tile digit
+// histograms, digit-major), exclusive scan, downsweep (warp-level
+// match_any ranking, tile-local reorder in shared memory, coalesced-run
+// scatter).  Keys uint64, optional uint32 values.
+constexpr int RS_NT = 256;
+constexpr int RS_IPT = 8;
+constexpr int RS_TILE = RS_NT * RS_IPT;
+constexpr int RS_WARPS = RS_NT / 32;
+
+__global__ void __launch_bounds__(RS_NT) k_radix_upsweep(const uint64_t *__restrict__ keys,
+                                                         int64_t m, int shift, int64_t ntiles,
+                                                         uint32_t *__restrict__ counts) {
+  __shared__ uint32_t hist[256];
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * RS_TILE;
+#pragma unroll
+  for (int i = 0; i < RS_IPT; ++i) {
+    int64_t idx = base + (int64_t)i * RS_NT + threadIdx.x;
+    if (idx < m) atomicAdd(&hist[(keys[idx] >> shift) & 0xff], 1u);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * ntiles + blockIdx.x] = hist[threadIdx.x];
+}
+
+template <bool VALS>
+__global__ void __launch_bounds__(RS_NT) k_radix_downsweep(
+    const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+    uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t m, int shift,
+    int64_t ntiles, const uint32_t *__restrict__ offsets) {
+  __shared__ uint64_t skeys[RS_TILE];
+  __shared__ uint32_t svals[VALS ? RS_TILE : 1];
+  __shared__ uint32_t wcnt[RS_WARPS][256];
+  __shared__ uint32_t tstart[256];
+  __shared__ uint32_t gbase[256];
+  __shared__ uint32_t sw[RS_NT / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_NT) (&wcnt[0][0])[i] = 0;
+  gbase[threadIdx.x] = offsets[(int64_t)threadIdx.x * ntiles + blockIdx.x];
+  __syncthreads();
+
+  const int64_t base = (int64_t)blockIdx.x * RS_TILE + (int64_t)wid * 32 * RS_IPT;
+  uint64_t k[RS_IPT];
+  uint32_t v[RS_IPT];
+  uint32_t rank[RS_IPT];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < RS_IPT; ++i) {
+    int64_t idx = base + i * 32 + lane;
+    bool ok = idx < m;
+    k[i] = ok ? keys_in[idx] : 0;
+    if (VALS) v[i] = ok ? vals_in[idx] : 0;
+    uint32_t dg = ok ? (uint32_t)((k[i] >> shift) & 0xff) : 0x100u;
+    unsigned peers = __match_any_sync(0xffffffffu, dg);
+    uint32_t before = 0;
+    if (ok) before = wcnt[wid][dg];
+    rank[i] = before + __popc(peers & lt);
+    __syncwarp();
+    if (ok && (peers & lt) == 0) wcnt[wid][dg] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per-digit prefix over warps, then tile-local digit starts
+  {
+    const int dgt = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      uint32_t c = wcnt[w][dgt];
+      wcnt[w][dgt] = run;
+      run += c;
+    }
+    uint32_t tot;
+    uint32_t ex = block_exclusive_scan<RS_NT>(run, tot, sw);
+    tstart[dgt] = ex;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < RS_IPT; ++i) {
+    int64_t idx = base + i * 32 + lane;
+    if (idx < m) {
+      uint32_t dg = (uint32_t)((k[i] >> shift) & 0xff);
+      uint32_t pos = tstart[dg] + wcnt[wid][dg] + rank[i];
+      skeys[pos] = k[i];
+      if (VALS) svals[pos] = v[i];
+    }
+  }
+  __syncthreads();
+  int64_t tile0 = (int64_t)blockIdx.x * RS_TILE;
+  int valid = (int)min((int64_t)RS_TILE, m - tile0);
+  for (int j = threadIdx.x; j < valid; j += RS_NT) {
+    uint64_t key = skeys[j];
+    uint32_t dg = (uint32_t)((key >> shift) & 0xff);
+    uint32_t dst = gbase[dg] + (j - tstart[dg]);
+    keys_out[dst] = key;
+    if (VALS) vals_out[dst] = svals[j];
+  }
+}
+
+__host__ inline size_t radix_workspace(int64_t m, bool vals) {
+  int64_t ntiles = (m + RS_TILE - 1) / RS_TILE;
+  size_t b = ws_bytes(m, 8) + (vals ? ws_bytes(m, 4) : 0);
+  b += ws_bytes(ntiles * 256, 4);
+  b += scan_workspace(ntiles * 256);
+  return b + 1024;
+}
+
+// Sort keys (and vals) by the 8-bit digits at the given shifts, least
+// significant first.  Result ends in keys/vals.
+__host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const int *shifts,
+                               int npass, Arena &ar, cudaStream_t st) {
+  if (m <= 1 || npass == 0) return EG_OK;
+  if (m >= (1ll << 32)) return EG_ERR_UNSUPPORTED;
+  int64_t ntiles = (m + RS_TILE - 1) / RS_TILE;
+  uint64_t *kalt = ar.take<uint64_t>(m);
+  uint32_t *valt = vals ? ar.take<uint32_t>(m) : nullptr;
+  uint32_t *counts = ar.take<uint32_t>(ntiles * 256);
+  if (!kalt || (vals && !valt) || !counts) return EG_ERR_WORKSPACE;
+  size_t mark = ar.used;
+  uint64_t *ksrc = keys, *kdst = kalt;
+  uint32_t *vsrc = vals, *vdst = valt;
+  for (int p = 0; p < npass; ++p) {
+    ar.used = mark;
+    k_radix_upsweep<<<(unsigned)ntiles, RS_NT, 0, st>>>(ksrc, m, shifts[p], ntiles, counts);
+    EG_LAUNCH_CHECK();
+    int rc = scan_exclusive_u32(counts, counts, ntiles * 256, ar, st);
+    if (rc) return rc;
+    if (vals)
+      k_radix_downsweep<true><<<(unsigned)ntiles, RS_NT, 0, st>>>(ksrc, vsrc, kdst, vdst, m,
+                                                                 shifts[p], ntiles, counts);
+    else
+      k_radix_downsweep<false><<<(unsigned)ntiles, RS_NT, 0, st>>>(ksrc, nullptr, kdst, nullptr,
+                                                                  m, shifts[p], ntiles, counts);
+    EG_LAUNCH_CHECK();
+    uint64_t *t = ksrc; ksrc = kdst; kdst = t;
+    uint32_t *tv = vsrc; vsrc = vdst; vdst = tv;
+  }
+  if (ksrc != keys) {
+    EG_CUDA_TRY(cudaMemcpyAsync(keys, ksrc, m * 8, cudaMemcpyDeviceToDevice, st));
+    if (vals) EG_CUDA_TRY(cudaMemcpyAsync(vals, vsrc, m * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return EG_OK;
+}
+
+// Digit shifts for pair keys (i << 32 | j) with i, j < n: only the low
+// ceil(log2 n) bits of each half are non-zero.
+__host__ inline int pair_key_shifts(int64_t n, int *shifts) {
+  int b = ilog2_ceil((uint64_t)(n > 1 ? n : 2));
+  int np = 0;
+  for (int s = 0; s < b; s += 8) shifts[np++] = s;
+  for (int s = 0; s < b; s += 8) shifts[np++] = 32 + s;
+  return np;
+}
+
+// ------------------------------------------------------------ compaction
+constexpr int CP_NT = 256;
+constexpr int CP_IPT = 16;
+constexpr int CP_TILE = CP_NT * CP_IPT;
+
+__global__ void __launch_bounds__(CP_NT) k_flag_count(const uint8_t *__restrict__ flags, int64_t m,
+                                                      uint32_t *__restrict__ tile_counts) {
+  __shared__ uint32_t sw[CP_NT / 32];
+  int64_t base = (int64_t)blockIdx.x * CP_TILE;
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < CP_IPT; ++i) {
+    int64_t idx = base + (int64_t)i * CP_NT + threadIdx.x;
+    if (idx < m) c += flags[idx] ? 1 : 0;
+  }
+  uint32_t tot;
+  block_exclusive_scan<CP_NT>(c, tot, sw);
+  if (threadIdx.x == 0) tile_counts[blockIdx.x] = tot;
+}
+
+// Stable scatter: blocked arrangement inside each tile keeps input order.
+template <typename V>
+__global__ void __launch_bounds__(CP_NT) k_flag_scatter(const uint64_t *__restrict__ keys,
+                                                        const V *__restrict__ vals,
+                                                        const uint8_t *__restrict__ flags,
+                                                        int64_t m,
+                                                        const uint32_t *__restrict__ tile_off,
+                                                        uint64_t *__restrict__ out_keys,
+                                                        V *__restrict__ out_vals) {
+  __shared__ uint32_t sw[CP_NT / 32];
+  int64_t base = (int64_t)blockIdx.x * CP_TILE + (int64_t)threadIdx.x * CP_IPT;
+  uint32_t c = 0;
+#pragma unroll
+  for (int i = 0; i < CP_IPT; ++i) {
+    int64_t idx = base + i;
+    if (idx < m && flags[idx]) ++c;
+  }
+  uint32_t tot;
+  uint32_t pos = block_exclusive_scan<CP_NT>(c, tot, sw) + tile_off[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < CP_IPT; ++i) {
+    int64_t idx = base + i;
+    if (idx < m && flags[idx]) {
+      out_keys[pos] = keys[idx];
+      if (vals) out_vals[pos] = vals[idx];
+      ++pos;
+    }
+  }
+}
+
+__host__ inline size_t compact_workspace(int64_t m) {
+  int64_t nt = (m + CP_TILE - 1) / CP_TILE;
+  return ws_bytes(nt + 1, 4) + scan_workspace(nt + 1) + 512;
+}
+
+// Returns the kept count via *h_count (synchronises `st`).
+template <typename V>
+__host__ inline int compact(const uint64_t *keys, const V *vals, const uint8_t *flags, int64_t m,
+                            uint64_t *out_keys, V *out_vals, int64_t *h_count, Arena &ar,
+                            cudaStream_t st) {
+  if (m <= 0) {
+    *h_count = 0;
+    return EG_OK;
+  }
+  int64_t nt = (m + CP_TILE - 1) / CP_TILE;
+  uint32_t *tc = ar.take<uint32_t>(nt + 1);
+  if (!tc) return EG_ERR_WORKSPACE;
+  EG_CUDA_TRY(cudaMemsetAsync(tc + nt, 0, 4, st));
+  k_flag_count<<<(unsigned)nt, CP_NT, 0, st>>>(flags, m, tc);
+  EG_LAUNCH_CHECK();
+  int rc = scan_exclusive_u32(tc, tc, nt + 1, ar, st);
+  if (rc) return rc;
+  k_flag_scatter<V><<<(unsigned)nt, CP_NT, 0, st>>>(keys, vals, flags, m, tc, out_keys, out_vals);
+  EG_LAUNCH_CHECK();
+  uint32_t total = 0;
+  EG_CUDA_TRY(cudaMemcpyAsync(&total, tc + nt, 4, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  *h_count = total;
+  return EG_OK;
+}
+
+}  // namespace eg

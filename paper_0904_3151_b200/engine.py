@@ -1,0 +1,284 @@
+"""Device-side stages of the build: thin wrappers over the C ABI.
+
+Each function takes/returns torch CUDA tensors (PyTorch is used only for
+device memory and streams) and calls one ``eg_*`` entry point on the current
+stream.  Workspaces come from the torch caching allocator.
+"""
+
+from __future__ import annotations
+
+import itertools
+import math
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import check
+from .errors import DataError
+
+_capacity_hint: dict = {}
+
+
+def require_device(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_0904_3151_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def _stream(dev) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def _ws(nbytes: int, dev) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+
+
+def _p(t) -> int:
+    return t.data_ptr() if t is not None else 0
+
+
+def as_device_rows(data, dev):
+    """(n, D) float rows on ``dev``: float32 stays float32, everything else
+    becomes float64 (the reference casts to float64, lsh.py:160)."""
+    if isinstance(data, torch.Tensor):
+        t = data
+        if t.dtype not in (torch.float32, torch.float64):
+            t = t.to(torch.float64)
+        t = t.to(dev, non_blocking=True).contiguous()
+    else:
+        arr = np.asarray(data)
+        if arr.dtype != np.float32:
+            arr = np.asarray(arr, dtype=np.float64)
+        arr = np.ascontiguousarray(arr)
+        t = torch.from_numpy(arr).to(dev, non_blocking=True)
+    if t.dim() != 2:
+        raise DataError("vectors must form a 2-D array")
+    return t
+
+
+def row_stats(x: torch.Tensor):
+    """fp64 row norms plus the first non-finite / zero-norm row (or -1)."""
+    n, dim = x.shape
+    norms = torch.empty(n, dtype=torch.float64, device=x.device)
+    bad = (ctypes_i64 * 2)()
+    check(_native.lib().eg_row_stats(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms),
+                                     ctypes_addr(bad), _stream(x.device)), "row_stats")
+    return norms, int(bad[0]), int(bad[1])
+
+
+def validate_rows(x: torch.Tensor):
+    """Reference error shapes: lsh.py:55-56 then lsh.py:121-125."""
+    norms, nonfinite, zero = row_stats(x)
+    if nonfinite >= 0:
+        raise DataError(f"row {nonfinite} has a non-finite entry")
+    if zero >= 0:
+        raise DataError(f"row {zero} has zero norm and cannot be projected")
+    return norms
+
+
+def directions(length: int, dim: int, seed: int, replicate_id: int) -> np.ndarray:
+    """Gaussian directions of one replicate, drawn on the host with the same
+    numpy call as the reference (lsh.py:116-118, 142-146).  Column-blocked
+    draws from one generator are a seamless stream, so one ``(length, dim)``
+    draw equals the reference's blocked draws."""
+    ss = np.random.SeedSequence([int(seed), int(replicate_id)])
+    return np.random.Generator(np.random.PCG64(ss)).standard_normal((length, dim))
+
+
+def project_codes(x: torch.Tensor, norms: torch.Tensor, length: int, seed: int,
+                  replicate_ids) -> tuple[torch.Tensor, int]:
+    """Packed codes ``(r, n, W)`` uint64 for the given replicate ids."""
+    dev = x.device
+    n, dim = x.shape
+    reps = len(replicate_ids)
+    W = max(1, -(-length // 64))
+    r = np.concatenate([directions(length, dim, seed, h) for h in replicate_ids], axis=0)
+    rnorm = np.sqrt(np.einsum("ij,ij->i", r, r))
+    r_d = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
+    rn_d = torch.from_numpy(rnorm).to(dev)
+    codes = torch.empty((reps, n, W), dtype=torch.int64, device=dev)
+    lib = _native.lib()
+    ws = _ws(lib.eg_project_workspace(n, dim, length, reps), dev)
+    fix = ctypes_i64(0)
+    check(lib.eg_project(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms), _p(r_d),
+                         _p(rn_d), length, reps, _p(codes), _p(ws), ws.numel(),
+                         ctypes_addr(fix), _stream(dev)), "project")
+    return codes, int(fix.value)
+
+
+def masks_for(k: int, d: int):
+    """Lexicographic d-subsets of range(k) (hamming_join.py:333)."""
+    return list(itertools.combinations(range(k), d))
+
+
+def units_for(replicates, k: int, d: int):
+    """(replicate index, block bitmask) for every unit, in reference order."""
+    reps, bits = [], []
+    for h in replicates:
+        for m in masks_for(k, d):
+            b = 0
+            for blk in m:
+                b |= 1 << blk
+            reps.append(h)
+            bits.append(b)
+    return np.asarray(reps, dtype=np.int32), np.asarray(bits, dtype=np.uint64)
+
+
+def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps, unit_masks,
+              capacity: int | None = None):
+    """Run the MSM units; returns (keys tensor, counts dict)."""
+    dev = codes.device
+    reps, n, W = codes.shape
+    k = len(block_bounds) - 1
+    if length > _native.MAX_LENGTH or k > _native.MAX_BLOCKS:
+        raise NotImplementedError(
+            f"enumeration kernels support length <= {_native.MAX_LENGTH} and "
+            f"k <= {_native.MAX_BLOCKS} (got length={length}, k={k})")
+    lib = _native.lib()
+    bb = np.ascontiguousarray(block_bounds, dtype=np.int32)
+    ur = np.ascontiguousarray(unit_reps, dtype=np.int32)
+    um = np.ascontiguousarray(unit_masks, dtype=np.uint64)
+    hint_key = (n, length, k, d, reps, len(ur))
+    if capacity is None:
+        capacity = _capacity_hint.get(hint_key, max(1 << 16, 2 * n))
+    ws = _ws(lib.eg_msm_workspace(n, length, reps), dev)
+    counts = (ctypes_i64 * (2 * reps + 2))()
+    while True:
+        out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+        rc = lib.eg_msm_pairs(_p(codes), n, length, reps, bb.ctypes.data, k, d, ur.ctypes.data,
+                              um.ctypes.data, len(ur), _p(out), capacity, ctypes_addr(counts),
+                              _p(ws), ws.numel(), _stream(dev))
+        if rc == _native.EG_ERR_CAPACITY:
+            capacity = int(counts[0])
+            del out
+            continue
+        check(rc, "msm_pairs")
+        break
+    total = int(counts[0])
+    _capacity_hint[hint_key] = max(1 << 16, int(total * 1.25) + 1024)
+    info = {
+        "emitted": total,
+        "max_group": int(counts[1]),
+        "raw": tuple(int(counts[2 + h]) for h in range(reps)),
+        "new": tuple(int(counts[2 + reps + h]) for h in range(reps)),
+    }
+    return out[:total], info
+
+
+def sort_pair_keys(keys: torch.Tensor, n: int) -> torch.Tensor:
+    m = keys.numel()
+    if m > 1:
+        lib = _native.lib()
+        ws = _ws(lib.eg_sort_workspace(m, 0), keys.device)
+        check(lib.eg_sort_pair_keys(_p(keys), m, n, _p(ws), ws.numel(), _stream(keys.device)),
+              "sort_pair_keys")
+    return keys
+
+
+def sort_keys(keys: torch.Tensor, key_bits: int = 64, vals: torch.Tensor | None = None):
+    m = keys.numel()
+    if m > 1:
+        lib = _native.lib()
+        ws = _ws(lib.eg_sort_workspace(m, int(vals is not None)), keys.device)
+        check(lib.eg_sort_keys(_p(keys), _p(vals), m, key_bits, _p(ws), ws.numel(),
+                               _stream(keys.device)), "sort_keys")
+    return keys, vals
+
+
+def verify(x: torch.Tensor, norms: torch.Tensor, keys: torch.Tensor, metric: int, eps: float):
+    """Exact filter of sorted candidate keys -> (edge keys, distances)."""
+    dev = x.device
+    n, dim = x.shape
+    m = keys.numel()
+    out_k = torch.empty(max(m, 1), dtype=torch.int64, device=dev)
+    out_d = torch.empty(max(m, 1), dtype=torch.float64, device=dev)
+    if m == 0:
+        return out_k[:0], out_d[:0]
+    lib = _native.lib()
+    ws = _ws(lib.eg_verify_workspace(m), dev)
+    cnt = ctypes_i64(0)
+    rc = lib.eg_verify(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms), _p(keys), m,
+                       metric, float(eps), _p(out_k), _p(out_d), ctypes_addr(cnt), _p(ws),
+                       ws.numel(), _stream(dev))
+    if rc == _native.EG_ERR_ARG:
+        raise IndexError("candidate index out of range")
+    check(rc, "verify")
+    c = int(cnt.value)
+    return out_k[:c], out_d[:c]
+
+
+def first_witness(keys: torch.Tensor, pools, W: int, d: int) -> torch.Tensor:
+    """keep[p] = Hamming > d in every pool of ``pools`` (device word arrays)."""
+    dev = keys.device
+    m = keys.numel()
+    keep = torch.ones(max(m, 1), dtype=torch.uint8, device=dev)
+    if m == 0 or not pools:
+        return keep[:m]
+    ptrs = torch.tensor([p.data_ptr() for p in pools], dtype=torch.int64, device=dev)
+    check(_native.lib().eg_first_witness(_p(keys), m, _p(ptrs), len(pools), W, d, _p(keep),
+                                         _stream(dev)), "first_witness")
+    return keep[:m]
+
+
+def compact_keys(keys: torch.Tensor, flags: torch.Tensor) -> torch.Tensor:
+    m = keys.numel()
+    out = torch.empty(max(m, 1), dtype=torch.int64, device=keys.device)
+    if m == 0:
+        return out[:0]
+    lib = _native.lib()
+    ws = _ws(lib.eg_compact_workspace(m), keys.device)
+    cnt = ctypes_i64(0)
+    check(lib.eg_compact_keys(_p(keys), _p(flags), m, _p(out), ctypes_addr(cnt), _p(ws),
+                              ws.numel(), _stream(keys.device)), "compact")
+    return out[:int(cnt.value)]
+
+
+def grouped_sort(codes_1: torch.Tensor, length: int, block_bounds, mask_bits: int):
+    """(perm int64 tensor, bounds int64 tensor) grouping equal masked keys."""
+    dev = codes_1.device
+    n, W = codes_1.shape
+    k = len(block_bounds) - 1
+    lib = _native.lib()
+    bb = np.ascontiguousarray(block_bounds, dtype=np.int32)
+    perm = torch.empty(n, dtype=torch.int32, device=dev)
+    bounds = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    ws = _ws(lib.eg_grouped_sort_workspace(n, length), dev)
+    g = ctypes_i64(0)
+    check(lib.eg_grouped_sort(_p(codes_1), n, length, bb.ctypes.data, k, mask_bits, _p(perm),
+                              _p(bounds), ctypes_addr(g), _p(ws), ws.numel(), _stream(dev)),
+          "grouped_sort")
+    return perm, bounds[:int(g.value) + 1]
+
+
+def keys_to_pairs(keys_host: np.ndarray) -> np.ndarray:
+    """uint64 (i << 32 | j) keys -> int64 (m, 2) pairs (boundary format)."""
+    k = keys_host.view(np.uint64)
+    out = np.empty((k.shape[0], 2), dtype=np.int64)
+    out[:, 0] = (k >> np.uint64(32)).astype(np.int64)
+    out[:, 1] = (k & np.uint64(0xFFFFFFFF)).astype(np.int64)
+    return out
+
+
+def pairs_to_keys(pairs: np.ndarray) -> np.ndarray:
+    p = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+    return ((p[:, 0].astype(np.uint64) << np.uint64(32)) | p[:, 1].astype(np.uint64)).view(np.int64)
+
+
+import ctypes  # noqa: E402
+
+ctypes_i64 = ctypes.c_int64
+
+
+def ctypes_addr(obj) -> int:
+    return ctypes.addressof(obj)
+
+
+def log2_ceil(v: int) -> int:
+    return max(0, math.ceil(math.log2(max(v, 1))))

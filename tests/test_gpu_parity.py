@@ -1,0 +1,317 @@
+"""CUDA path vs the pinned oracle / reference fixtures (needs a B200).
+
+Every comparison goes through the package's public API, which calls the
+C ABI of libepsgraph_b200.so.  Integer outputs (codes, pair sets, counts)
+must be bit-exact; distances agree to 1e-12 (fp64, different summation
+order) and edge sets must be identical except for pairs within 1e-6 of eps.
+"""
+
+import logging
+
+import numpy as np
+import pytest
+
+from conftest import FIG2_CLOSE_PAIRS, golden, pack_bits
+
+pytestmark = pytest.mark.gpu
+
+DIST_TOL = 1e-12
+BAND = 1e-6
+
+
+@pytest.fixture(scope="module")
+def eg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_0904_3151_b200 as eg
+    from paper_0904_3151_b200 import _native
+    _native.lib()
+    return eg
+
+
+def pairs_equal_except_band(got_pairs, got_dist, ref_pairs, ref_dist, eps):
+    gk = {tuple(p): d for p, d in zip(got_pairs.tolist(), got_dist.tolist())}
+    rk = {tuple(p): d for p, d in zip(ref_pairs.tolist(), ref_dist.tolist())}
+    for p in set(gk) ^ set(rk):
+        d = gk.get(p, rk.get(p))
+        assert abs(d - eps) <= BAND, (p, d)
+    for p in set(gk) & set(rk):
+        assert abs(gk[p] - rk[p]) <= DIST_TOL, (p, gk[p], rk[p])
+
+
+# ------------------------------------------------------------- enumeration
+
+def test_fig2_pool(eg):
+    g = golden("fig2")
+    pool = eg.BitStringPool(g["words"], 16).partitioned(4)
+    for d in range(4):
+        got = eg.enumerate_pairs(pool, d)
+        np.testing.assert_array_equal(got.array, g[f"pairs_d{d}"])
+    assert eg.enumerate_pairs(pool, 2).to_set() == FIG2_CLOSE_PAIRS
+
+
+def test_random_pools_match_reference(eg, manifest):
+    g = golden("random_pools")
+    for case in manifest["random_pools"]:
+        c = case["case"]
+        pool = eg.BitStringPool(g[f"words_{c}"], case["length"]).partitioned(case["k"])
+        got = eg.enumerate_pairs(pool, case["d"])
+        np.testing.assert_array_equal(got.array, g[f"pairs_{c}"], err_msg=str(case))
+
+
+def test_grouped_sort_groups(eg, manifest):
+    g = golden("random_pools")
+    for case in manifest["random_pools"][:24]:
+        c = case["case"]
+        pool = eg.BitStringPool(g[f"words_{c}"], case["length"]).partitioned(case["k"])
+        perm, bounds = eg.grouped_radix_sort(pool, case["mask"])
+        ref_bounds = g[f"gbounds_{c}"]
+        assert sorted(perm.tolist()) == list(range(pool.count))
+        assert len(bounds) == len(ref_bounds)          # same number of groups
+        kept = eg.kept_word_mask(pool.length, pool.block_bounds, case["mask"])
+        keys = [tuple(int(v) for v in (pool.words[i] & kept)) for i in range(pool.count)]
+        seen = set()
+        for a, b in zip(bounds[:-1], bounds[1:]):
+            ks = {keys[i] for i in perm[a:b]}
+            assert len(ks) == 1
+            kk = ks.pop()
+            assert kk not in seen
+            seen.add(kk)
+        # same multiset of group sizes as the reference grouping
+        assert sorted(np.diff(bounds).tolist()) == sorted(np.diff(ref_bounds).tolist())
+
+
+def test_duplicates_and_oversized_warning(eg, caplog):
+    bits = np.zeros((64, 16), dtype=np.uint8)
+    pool = eg.BitStringPool.from_bits(bits).partitioned(4)
+    with caplog.at_level(logging.WARNING, logger="paper_0904_3151_b200"):
+        got = eg.enumerate_pairs(pool, 1)
+    assert len(got) == 64 * 63 // 2
+    assert any("group" in r.message for r in caplog.records)
+
+
+def test_d_zero_duplicates(eg):
+    strings = ["1010", "0101", "1010", "1111", "0101", "1010"]
+    pool = eg.BitStringPool.from_bits(np.array([[int(c) for c in s] for s in strings])).partitioned(2)
+    assert eg.enumerate_pairs(pool, 0).to_set() == {(0, 2), (0, 5), (2, 5), (1, 4)}
+
+
+def test_single_row_and_validation(eg):
+    pool = eg.BitStringPool.from_bits(np.array([[1, 0, 1, 0, 1, 0, 1, 0]])).partitioned(2)
+    assert len(eg.enumerate_pairs(pool, 1)) == 0
+    with pytest.raises(ValueError):
+        eg.enumerate_pairs(pool, 2)
+    with pytest.raises(ValueError):
+        eg.enumerate_pairs(pool, -1)
+    empty = eg.BitStringPool(np.zeros((0, 1), np.uint64), 8).partitioned(2)
+    with pytest.raises(ValueError):
+        eg.enumerate_pairs(empty, 1)
+
+
+@pytest.mark.parametrize("n,length,k,d,density", [
+    (3000, 64, 8, 2, 0.5),
+    (5000, 48, 12, 3, 0.5),
+    (4000, 128, 16, 3, 0.5),      # two words
+    (2500, 256, 32, 2, 0.5),      # four words, max length
+    (3000, 70, 7, 2, 0.3),        # unequal blocks across a word boundary
+    (4000, 20, 20, 4, 0.5),       # one bit per block
+    (6000, 24, 4, 1, 0.1),        # skewed bits: big groups
+])
+def test_random_pools_vs_oracle(eg, oracle, n, length, k, d, density):
+    rng = np.random.default_rng(n + length + k + d)
+    base = (rng.random((n // 3, length)) < density).astype(np.uint8)
+    bits = base[rng.integers(0, base.shape[0], n)]
+    flip = rng.random(bits.shape) < 0.02
+    bits = bits ^ flip.astype(np.uint8)
+    words = pack_bits(bits)
+    pool = eg.BitStringPool(words, length).partitioned(k)
+    got = eg.enumerate_pairs(pool, d)
+    want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+    np.testing.assert_array_equal(got.array, want)
+
+
+def test_spill_path_giant_group(eg, oracle):
+    # 5000 rows sharing most bits -> buckets far above shared-memory capacity
+    rng = np.random.default_rng(5)
+    n, length = 6000, 64
+    base = rng.integers(0, 2**63, dtype=np.int64).astype(np.uint64)
+    words = np.full((n, 1), base, dtype=np.uint64)
+    flips = rng.integers(0, 64, size=(n, 3))
+    for j in range(3):
+        sel = rng.random(n) < 0.5
+        words[sel, 0] ^= (np.uint64(1) << flips[sel, j].astype(np.uint64))
+    words[5000:, 0] = rng.integers(0, 2**63, size=1000, dtype=np.int64).astype(np.uint64)
+    pool = eg.BitStringPool(words, length).partitioned(8)
+    for d in (1, 2):
+        got = eg.enumerate_pairs(pool, d)
+        want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+        np.testing.assert_array_equal(got.array, want)
+
+
+def test_hamming_builder_variants(eg, oracle):
+    rng = np.random.default_rng(31)
+    bits = (rng.random((200, 32)) < 0.5).astype(np.uint8)
+    pool = eg.BitStringPool.from_bits(bits).partitioned(4)
+    for d in (0, 1, 3):
+        np.testing.assert_array_equal(eg.build_graph_hamming(pool, d).array,
+                                      oracle.brute_force_hamming(pool.words, d))
+    one = eg.BitStringPool.from_bits((rng.random((60, 16)) < 0.5).astype(np.uint8))
+    np.testing.assert_array_equal(eg.build_graph_hamming(one, 2).array,
+                                  oracle.brute_force_hamming(one.words, 2))
+    assert len(eg.build_graph_hamming(one, 16)) == 60 * 59 // 2
+
+
+# --------------------------------------------------------------- projection
+
+def test_projection_bits_match_reference(eg, manifest):
+    g = golden("projection")
+    for case in manifest["projection"]:
+        c = case["case"]
+        pool = eg.project(g[f"x_{c}"], eg.ProjectionSpec(case["length"], case["seed"],
+                                                          case["replicate_id"]))
+        np.testing.assert_array_equal(pool.words, g[f"words_{c}"], err_msg=str(case))
+
+
+def test_projection_vs_oracle_large(eg, oracle):
+    from paper_0904_3151_b200 import workloads
+    x = workloads.cfg3_points(30_000, planted_rows=3000)
+    for rep in (1, 2):
+        got = eg.project(x, eg.ProjectionSpec(48, 0, rep)).words
+        want = oracle.project_words(x, 48, 0, rep)
+        np.testing.assert_array_equal(got, want)
+
+
+def test_projection_validation(eg):
+    with pytest.raises(eg.DataError, match="row 1"):
+        eg.project(np.array([[1.0, 1.0], [0.0, 0.0]], dtype=np.float32), eg.ProjectionSpec(8))
+    with pytest.raises(eg.DataError, match="row 1"):
+        eg.project(np.array([[1.0, 2.0], [np.nan, 0.0]], dtype=np.float32), eg.ProjectionSpec(8))
+    with pytest.raises(eg.DataError):
+        eg.project(np.zeros((0, 4), dtype=np.float32), eg.ProjectionSpec(8))
+
+
+def test_sign_convention(eg):
+    data = np.array([[1.0, 2.0], [-1.0, -2.0], [2.0, 4.0]], dtype=np.float32)
+    bits = eg.project(data, eg.ProjectionSpec(length=96)).to_bits()
+    assert np.all(bits[0] != bits[1])
+    np.testing.assert_array_equal(bits[0], bits[2])
+
+
+def test_long_projection(eg, oracle):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((7, 5))
+    got = eg.project(x, eg.ProjectionSpec(length=3000, seed=4, replicate_id=2)).words
+    np.testing.assert_array_equal(got, oracle.project_words(x, 3000, 4, 2))
+
+
+# -------------------------------------------------------------------- build
+
+def test_small_build_matches_reference(eg, manifest):
+    g = golden("small_build")
+    rec = manifest["small_build"]
+    p = rec["params"]
+    params = eg.MsmParams(epsilon=p["epsilon"], gamma=1e-3, length=p["length"],
+                          mismatch=p["mismatch"], blocks=p["blocks"],
+                          replicates=p["replicates"], seed=p["seed"])
+    graph = eg.build_graph(g["x"], params)
+    assert graph.stats.per_replicate_raw == tuple(rec["per_replicate_raw"])
+    assert graph.stats.per_replicate_new == tuple(rec["per_replicate_new"])
+    assert graph.stats.candidate_count == rec["candidate_count"]
+    assert graph.stats.edge_count == rec["edge_count"]
+    np.testing.assert_array_equal(graph.edge_list.pairs, g["edges"])
+    np.testing.assert_allclose(graph.edge_list.distances, g["dist"], rtol=0, atol=DIST_TOL)
+    assert abs(graph.stats.achieved_bound - rec["achieved_bound"]) <= 1e-12 * rec["achieved_bound"]
+    again = eg.build_graph(g["x"], params, threads=3)
+    assert again.edge_list == graph.edge_list      # bit-exact, per-pair deterministic
+
+
+def test_dedup_and_filter_match_reference(eg):
+    g = golden("small_build")
+    pools = [eg.BitStringPool(g[f"codes_{h}"], 24).partitioned(4) for h in range(4)]
+    raw = [eg.PairSet(g[f"raw_{h}"], assume_normalized=True) for h in range(4)]
+    merged = eg.dedup_across_replicates(pools, raw, 2)
+    np.testing.assert_array_equal(merged.pairs, g["merged"])
+    edges = eg.filter_exact(g["x"], g["filter_cand"], 0.05)
+    np.testing.assert_array_equal(edges.pairs, g["filter_edges"])
+    np.testing.assert_allclose(edges.distances, g["filter_dist"], rtol=0, atol=DIST_TOL)
+    with pytest.raises(IndexError):
+        eg.filter_exact(g["x"], np.array([[0, 400]]), 0.1)
+
+
+def test_lsh_only_matches_reference(eg, manifest):
+    g = golden("small_build")
+    graph = eg.build_graph_lsh_only(g["x"], 0.05, 1e-3, replicates=50)
+    rec = manifest["small_build"]["lsh_only"]
+    assert graph.params.length == rec["length"]
+    assert graph.stats.candidate_count == rec["candidate_count"]
+    np.testing.assert_array_equal(graph.edge_list.pairs, g["lsh_edges"])
+
+
+def test_build_edge_cases(eg):
+    params = eg.MsmParams(0.05, 1e-3, 24, 2, 4, 2, 7)
+    with pytest.raises(eg.DataError):
+        eg.build_graph(np.zeros((0, 4), dtype=np.float32), params)
+    one = eg.build_graph(np.ones((1, 4), dtype=np.float32), params)
+    assert one.edge_count == 0 and one.node_count == 1
+    x = np.ones((5, 3), dtype=np.float32)
+    x[3] = 0
+    with pytest.raises(eg.DataError, match="row 3"):
+        eg.build_graph(x, params)
+
+
+def _config_build(eg, oracle, manifest, name, x, metric="cosine"):
+    rec = manifest[name]
+    p = rec["params"]
+    eps = p["epsilon"]
+    if metric == "euclidean":
+        eps = float(np.sqrt(2.0 * eps))
+    params = eg.MsmParams(epsilon=eps, gamma=1e-6, length=p["length"], mismatch=p["mismatch"],
+                          blocks=p["blocks"], replicates=p["replicates"], seed=0)
+    graph = eg.build_graph(x, params, metric=metric)
+    assert graph.stats.per_replicate_raw == tuple(rec["per_replicate_raw"])
+    assert graph.stats.per_replicate_new == tuple(rec["per_replicate_new"])
+    assert graph.stats.candidate_count == rec["candidate_count"]
+    if metric == "cosine":
+        assert oracle.pair_digest(graph.edge_list.pairs) == rec["pairs_sha256"]
+    else:
+        ref = oracle.build_graph(x, p["epsilon"], p["length"], p["mismatch"], p["blocks"],
+                                 p["replicates"], 0)
+        # Euclidean on unit rows agrees with the cosine route except in the band
+        d_cos = graph.edge_list.distances ** 2 / 2.0
+        pairs_equal_except_band(graph.edge_list.pairs, d_cos, ref.pairs, ref.distances,
+                                p["epsilon"])
+    return graph
+
+
+def test_cfg1_full(eg, oracle, manifest):
+    from paper_0904_3151_b200 import workloads
+    x = workloads.cfg1_points()
+    graph = _config_build(eg, oracle, manifest, "cfg1", x)
+    assert graph.edge_count == 809_648
+    pool = eg.project(x, eg.ProjectionSpec(32, 0, 1))
+    assert oracle.words_digest(pool.words) == manifest["cfg1"]["codes_sha256"][0]
+
+
+def test_cfg2_small(eg, oracle, manifest):
+    from paper_0904_3151_b200 import workloads
+    words = workloads.cfg2_words(200_000, 10_000)
+    got = eg.build_graph_hamming(eg.BitStringPool(words, 64).partitioned(8), 2)
+    assert len(got) == manifest["cfg2_small"]["count"]
+    assert oracle.pair_digest(got.array) == manifest["cfg2_small"]["pairs_sha256"]
+
+
+def test_cfg3_small(eg, oracle, manifest):
+    from paper_0904_3151_b200 import workloads
+    _config_build(eg, oracle, manifest, "cfg3_small", workloads.cfg3_points(20_000))
+
+
+def test_cfg4_small(eg, oracle, manifest):
+    from paper_0904_3151_b200 import workloads
+    _config_build(eg, oracle, manifest, "cfg4_small", workloads.cfg4_points(60_000, largest=2_000))
+
+
+def test_cfg5_small_euclidean(eg, oracle, manifest):
+    from paper_0904_3151_b200 import workloads
+    _config_build(eg, oracle, manifest, "cfg5_small",
+                  workloads.cfg5_points(40_000, clusters=2_000), metric="euclidean")
