@@ -1,0 +1,372 @@
+"""Benchmark of the eps-graph build (BASELINE.json metric: points/sec at
+n=1.6M, D=384 -- config 3), per the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg3]
+
+One "step" = one full build (projection of all replicates, every
+(replicate, mask) unit, candidate sort, exact verify) over the resident
+synthetic dataset.  ``value`` = points / device time per step with inputs
+resident in HBM; ``e2e`` = the same metric through the public API
+``build_graph(pinned host array)`` including H2D of the rows and D2H of the
+edge list.  Under torchrun the (replicate, mask) units are sharded across
+ranks (see paper_0904_3151_b200/distributed.py) and time is the max over
+ranks.  ``--impl reference`` times the CPU oracle port (the reference's
+algorithm restated in C, oracle/) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_0904_3151_b200 import workloads  # noqa: E402
+from paper_0904_3151_b200.workloads import CONFIGS  # noqa: E402
+
+METRIC = "eps-graph build points/sec (n=1.6M, D=384)"
+UNIT = "points/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def make_inputs(name: str):
+    if name == "cfg1":
+        return workloads.cfg1_points()
+    if name == "cfg2":
+        return workloads.cfg2_words()
+    if name == "cfg3":
+        return workloads.cfg3_points()
+    if name == "cfg4":
+        return workloads.cfg4_points()
+    if name == "cfg5":
+        return workloads.cfg5_points()
+    raise ValueError(name)
+
+
+def sample_inputs(name: str, rows: int):
+    """CPU-baseline sample: the same generator at a bounded row count."""
+    if name == "cfg1":
+        return workloads.cfg1_points(min(rows, 20_000))
+    if name == "cfg2":
+        return workloads.cfg2_words(rows, max(1, rows // 20))
+    if name == "cfg3":
+        return workloads.cfg3_points(rows)
+    if name == "cfg4":
+        return workloads.cfg4_points(4_000_000, subset=rows)
+    if name == "cfg5":
+        return workloads.cfg5_points(rows, clusters=max(1, rows // 20))
+    raise ValueError(name)
+
+
+def params_for(cfg, eg):
+    return eg.MsmParams(epsilon=cfg.epsilon if cfg.metric != "hamming" else 0.0, gamma=1e-6,
+                        length=cfg.length, mismatch=cfg.mismatch, blocks=cfg.blocks,
+                        replicates=cfg.replicates, seed=cfg.seed)
+
+
+def sort_bytes_per_unit(n: int, cfg) -> int:
+    """B_sort = n (8W + P * 2 (kb + 4)), kb = P = ceil(kappa/8)."""
+    W = max(1, -(-cfg.length // 64))
+    base, rem = divmod(cfg.length, cfg.blocks)
+    # every config has equal blocks; kappa = length - d * block size (worst case)
+    kappa = cfg.length - sum(sorted([base + (1 if b < rem else 0) for b in range(cfg.blocks)])
+                             [:cfg.mismatch])
+    kb = -(-kappa // 8)
+    return n * (8 * W + kb * 2 * (kb + 4))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (profiling recipe)."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.index)],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# -------------------------------------------------------------- reference
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from oracle import oracle
+    oracle.build()
+    cfg = CONFIGS[args.config]
+    rows = args.cpu_sample_rows
+    x = sample_inputs(args.config, rows)
+    cores = os.cpu_count() or 1
+    n = x.shape[0]
+
+    def step():
+        if cfg.metric == "hamming":
+            oracle.enumerate_pairs(x, 64, oracle.block_partition(64, cfg.blocks), cfg.mismatch,
+                                   threads=cores)
+        else:
+            eps = cfg.epsilon if cfg.metric == "cosine" else cfg.epsilon ** 2 / 2.0
+            oracle.build_graph(x, eps, cfg.length, cfg.mismatch, cfg.blocks, cfg.replicates,
+                               cfg.seed, threads=cores)
+
+    for _ in range(args.warmup):
+        step()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    sec = sum(times) / len(times)
+    value = n / sec
+    sample = f"{args.config} generator at n={n} rows (full params), C oracle port, {cores} threads"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(args, cfg, n, world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def config_block(args, cfg, n, world):
+    return {"workload": f"{args.config}: n={n}, " + (
+        f"D={384 if args.config == 'cfg3' else 'var'}, " if cfg.metric != "hamming" else "")
+        + f"{cfg.metric} eps={cfg.epsilon}, l={cfg.length}, k={cfg.blocks}, d={cfg.mismatch}, "
+        f"r={cfg.replicates}, units={cfg.replicates * math.comb(cfg.blocks, cfg.mismatch)}",
+        "n": n, "parallelism": f"units sharded over {world} GPU(s)" if world > 1 else "1 GPU",
+        "l2": "rows (2.46 GB) exceed L2; 256 MiB L2 flush between timed steps"}
+
+
+# ------------------------------------------------------------------- ours
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-sample-rows", type=int, default=100_000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as tdist
+
+    import paper_0904_3151_b200 as eg
+    from paper_0904_3151_b200 import _native, distributed
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    params = params_for(cfg, eg)
+    data = make_inputs(args.config)
+    n = data.shape[0]
+    hamming = cfg.metric == "hamming"
+    if hamming:
+        x_dev = torch.from_numpy(data.view(np.int64)).to(dev).reshape(1, n, 1)
+    else:
+        x_dev = torch.from_numpy(data).to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        if hamming:
+            return distributed.hamming_step(x_dev, params, world, rank)
+        return distributed.build_step(x_dev, params, cfg.metric, world, rank)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    prof = _native.Profile()
+    l0 = _native.launch_count()
+    prof.start()
+    if world > 1:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    times = []
+    last = None
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        last = step()
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        tdist.barrier()
+    kprof = prof.stop()
+    launches = _native.launch_count() - l0
+    step_ms = sum(times) / len(times)
+    if world > 1:
+        t = torch.tensor([step_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        step_ms = float(t.item())
+    value = n / (step_ms / 1e3)
+
+    # ---------------------------------------------------------------- e2e
+    e2e = None
+    if rank == 0:
+        if hamming:
+            host = torch.from_numpy(data.view(np.int64)).pin_memory()
+        else:
+            host = torch.from_numpy(data).pin_memory()
+        e2e_times, h2d, d2h = [], host.numel() * host.element_size(), 0
+        for i in range(args.e2e_steps + 1):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            if hamming:
+                pool = eg.BitStringPool(host.numpy().view(np.uint64).reshape(n, 1), 64)
+                res = eg.build_graph_hamming(pool.partitioned(cfg.blocks), cfg.mismatch)
+                d2h = res.array.shape[0] * 8
+            else:
+                g = eg.build_graph(host, params, metric=cfg.metric if cfg.metric != "hamming" else "cosine")
+                d2h = g.edge_count * 16
+            e1.record()
+            e1.synchronize()
+            if i:                       # first call warms the pinned path
+                e2e_times.append(e0.elapsed_time(e1))
+        e2e_ms = sum(e2e_times) / len(e2e_times)
+        e2e = {"value": n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
+    clk = clocks.stop()
+
+    # ------------------------------------------------------------ roofline
+    peak, peak_kind = peaks()
+    units_total = cfg.replicates * math.comb(cfg.blocks, cfg.mismatch)
+    units_mine = len(distributed.my_units(units_total, world, rank))
+    batch = kprof.get("msm_batch", {"ms": 0.0, "count": 0})
+    roof = None
+    if batch["count"]:
+        batches_per_step = batch["count"] / args.steps
+        units_per_launch = units_mine / batches_per_step
+        avg_ms = batch["ms"] / batch["count"]
+        alg = sort_bytes_per_unit(n, cfg) * units_per_launch
+        achieved = alg / (avg_ms / 1e3) / 1e9
+        roof = {"kernel": "msm unit pipeline (hist+scan+scatter+group+spill), one launch batch",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg),
+                "units_per_launch": units_per_launch, "avg_launch_ms": avg_ms}
+    stage_ms = {k: v["ms"] / args.steps for k, v in kprof.items()}
+
+    # -------------------------------------------------------- cpu baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle
+        oracle.build()
+        rows = args.cpu_sample_rows
+        xs = sample_inputs(args.config, rows)
+        cores = os.cpu_count() or 1
+        t0 = time.perf_counter()
+        if hamming:
+            oracle.enumerate_pairs(xs, 64, oracle.block_partition(64, cfg.blocks), cfg.mismatch,
+                                   threads=cores)
+        else:
+            eps = cfg.epsilon if cfg.metric == "cosine" else cfg.epsilon ** 2 / 2.0
+            oracle.build_graph(xs, eps, cfg.length, cfg.mismatch, cfg.blocks, cfg.replicates,
+                               cfg.seed, threads=cores)
+        sec = time.perf_counter() - t0
+        cpu = {"value": xs.shape[0] / sec, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{args.config} generator at n={xs.shape[0]} rows, full params, "
+                         f"C oracle port (oracle/), {sec:.1f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u64" if hamming else "f32-in/f64-verify",
+            "data": "synthetic (seeded generator, SURVEY.md App. C)",
+            "config": config_block(args, cfg, n, world),
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+            "cpu_baseline": cpu, "stage_ms": stage_ms,
+            "counts": distributed.last_counts(last),
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        tdist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

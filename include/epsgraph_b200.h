@@ -49,6 +49,15 @@ int eg_version(void);
 /* Number of SMs of the current device (for host-side sizing). */
 int eg_device_sm_count(void);
 
+/* Instrumentation (bench.py): number of kernels this library has launched,
+ * and optional per-kernel-class CUDA-event timing.  eg_profile_read
+ * synchronises the recorded events, fills ms/count per class (class names
+ * from eg_profile_class_name) and clears the record; returns #classes. */
+long long eg_launch_count(void);
+void eg_profile_enable(int on);
+const char *eg_profile_class_name(int cls);
+int eg_profile_read(double *ms_out, long long *count_out, int max_classes);
+
 /* --------------------------------------------------------------------- */
 /* Row statistics.  Replaces the validation in VectorDataset.__init__     */
 /* (lsh.py:48-57), _check_norms (lsh.py:121-125) and the norm pass of     */

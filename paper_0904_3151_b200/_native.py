@@ -57,6 +57,10 @@ def _declare(lib):
         "eg_last_error": ([], ctypes.c_char_p),
         "eg_version": ([], I),
         "eg_device_sm_count": ([], I),
+        "eg_launch_count": ([], ctypes.c_longlong),
+        "eg_profile_enable": ([I], None),
+        "eg_profile_class_name": ([I], ctypes.c_char_p),
+        "eg_profile_read": ([P, P, I], I),
         "eg_row_stats": ([P, I, i64, i32, P, P, P], I),
         "eg_project_workspace": ([i64, i32, i32, i32], sz),
         "eg_project": ([P, I, i64, i32, P, P, P, i32, i32, P, P, sz, P, P], I),
@@ -109,3 +113,30 @@ def check(rc: int, what: str):
     if rc == EG_ERR_UNSUPPORTED:
         raise NotImplementedError(f"{what}: {msg}")
     raise NativeError(f"{what} failed ({rc}): {msg}")
+
+
+class Profile:
+    """Per-kernel-class CUDA-event timing collected inside the library."""
+
+    def __init__(self):
+        self.lib = lib()
+
+    def start(self):
+        self.lib.eg_profile_read(None, None, 0)   # drop stale records
+        self.lib.eg_profile_enable(1)
+
+    def stop(self) -> dict:
+        self.lib.eg_profile_enable(0)
+        nc = 32
+        ms = (ctypes.c_double * nc)()
+        cnt = (ctypes.c_longlong * nc)()
+        k = self.lib.eg_profile_read(ctypes.addressof(ms), ctypes.addressof(cnt), nc)
+        out = {}
+        for c in range(k):
+            if cnt[c]:
+                out[self.lib.eg_profile_class_name(c).decode()] = {"ms": ms[c], "count": int(cnt[c])}
+        return out
+
+
+def launch_count() -> int:
+    return int(lib().eg_launch_count())

@@ -6,6 +6,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -23,6 +25,52 @@ void set_error(const char *fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+// ------------------------------------------------------- instrumentation
+struct ProfRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+static std::mutex g_prof_mu;
+static std::atomic<long long> g_launches{0};
+static std::atomic<int> g_prof_on{0};
+static std::vector<ProfRec> g_prof_open[PC_COUNT];   // per class stack (nesting)
+static std::vector<ProfRec> g_prof_done;
+static std::vector<cudaEvent_t> g_event_pool;
+static const char *g_prof_names[PC_COUNT] = {
+    "row_stats", "project", "fixup", "msm_hist", "msm_scan", "msm_scatter", "msm_group",
+    "msm_spill", "msm_batch", "sort_upsweep", "scan", "sort_downsweep", "verify", "compact",
+    "misc"};
+
+static cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void prof_begin(int cls, cudaStream_t st, int launches) {
+  g_launches += launches;
+  if (!g_prof_on.load()) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfRec r{cls, take_event(), take_event()};
+  cudaEventRecord(r.a, st);
+  g_prof_open[cls].push_back(r);
+}
+
+void prof_end(int cls, cudaStream_t st) {
+  if (!g_prof_on.load()) return;
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  if (g_prof_open[cls].empty()) return;
+  ProfRec r = g_prof_open[cls].back();
+  g_prof_open[cls].pop_back();
+  cudaEventRecord(r.b, st);
+  g_prof_done.push_back(r);
 }
 
 static int arg_error(const char *msg) {
@@ -64,6 +112,7 @@ static void launch_project(const TX *x, int64_t n, int dim, const float *rt, int
                            int cols_pad, const double *norms, const double *rnorm, double tau,
                            int L, int W, uint64_t *codes, FixupList fl, cudaStream_t st) {
   unsigned grid = (unsigned)((n + PJ_BM - 1) / PJ_BM);
+  EG_PROF(PC_PROJECT, st);
   k_project<TX, TN><<<grid, PJ_NT, 0, st>>>(x, n, dim, rt, cols, cols_pad, norms, rnorm, tau, L,
                                             W, codes, fl);
 }
@@ -136,14 +185,33 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
   const unsigned tiles = (unsigned)((a.n + MSM_TILE - 1) / MSM_TILE);
   const unsigned spill_grid = (unsigned)num_sms() * 8;
   for (const UnitBatch &ub : batches) {
+    EG_PROF_GROUP(PC_MSM_BATCH, st);
     dim3 g1(tiles, ub.count);
-    k_msm_hist<W><<<g1, MSM_NT, smem_hist, st>>>(a, ub);
-    k_msm_scan<<<ub.count, 1024, 0, st>>>(a);
-    k_msm_scatter<W><<<g1, MSM_NT, smem_scatter, st>>>(a, ub);
+    {
+      EG_PROF(PC_MSM_HIST, st);
+      k_msm_hist<W><<<g1, MSM_NT, smem_hist, st>>>(a, ub);
+    }
+    {
+      EG_PROF(PC_MSM_SCAN, st);
+      k_msm_scan<<<ub.count, 1024, 0, st>>>(a);
+    }
+    {
+      EG_PROF(PC_MSM_SCATTER, st);
+      k_msm_scatter<W><<<g1, MSM_NT, smem_scatter, st>>>(a, ub);
+    }
     dim3 g4(lay.B, ub.count);
-    k_msm_group<W><<<g4, MSM_GNT, smem_group, st>>>(a, ub);
-    k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, st>>>(a, ub);
-    k_msm_spill_maxgroup<<<64, 256, 0, st>>>(a);
+    {
+      EG_PROF(PC_MSM_GROUP, st);
+      k_msm_group<W><<<g4, MSM_GNT, smem_group, st>>>(a, ub);
+    }
+    {
+      EG_PROF(PC_MSM_SPILL, st);
+      k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, st>>>(a, ub);
+    }
+    {
+      EG_PROF(PC_MSM_SPILL, st);
+      k_msm_spill_maxgroup<<<64, 256, 0, st>>>(a);
+    }
     EG_LAUNCH_CHECK();
   }
   return EG_OK;
@@ -156,6 +224,35 @@ using namespace eg;
 extern "C" {
 
 const char *eg_last_error(void) { return g_err; }
+
+long long eg_launch_count(void) { return g_launches.load(); }
+
+void eg_profile_enable(int on) { g_prof_on = on ? 1 : 0; }
+
+const char *eg_profile_class_name(int cls) {
+  return (cls >= 0 && cls < PC_COUNT) ? g_prof_names[cls] : "";
+}
+
+int eg_profile_read(double *ms_out, long long *count_out, int max_classes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  for (int c = 0; c < max_classes && c < PC_COUNT; ++c) {
+    ms_out[c] = 0.0;
+    count_out[c] = 0;
+  }
+  for (ProfRec &r : g_prof_done) {
+    cudaEventSynchronize(r.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    if (r.cls < max_classes) {
+      ms_out[r.cls] += ms;
+      count_out[r.cls] += 1;
+    }
+    g_event_pool.push_back(r.a);
+    g_event_pool.push_back(r.b);
+  }
+  g_prof_done.clear();
+  return PC_COUNT;
+}
 int eg_version(void) { return 1; }
 int eg_device_sm_count(void) { return num_sms(); }
 
@@ -170,6 +267,7 @@ int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *
   EG_CUDA_TRY(cudaMallocAsync(&bad, 16, st));
   EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 16, st));
   unsigned grid = (unsigned)((n + 7) / 8);
+  EG_PROF(PC_ROW_STATS, st);
   if (x_is_f64)
     k_row_stats<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, bad);
   else
@@ -218,6 +316,7 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
   {
     int64_t tot = (int64_t)dim * cols_pad;
+    EG_PROF(PC_MISC, st);
     k_prep_directions<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_r, cols, dim, cols_pad, rt);
     EG_LAUNCH_CHECK();
   }
@@ -232,12 +331,15 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
                             tau, length, W, d_codes, fl, st);
   EG_LAUNCH_CHECK();
   const unsigned fgrid = (unsigned)num_sms() * 8;
+  {
+  EG_PROF(PC_FIXUP, st);
   if (x_is_f64)
     k_fixup<double><<<fgrid, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W, d_codes,
                                            items, cnt, cap, cols, 0);
   else
     k_fixup<float><<<fgrid, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W, d_codes,
                                           items, cnt, cap, cols, 0);
+  }
   EG_LAUNCH_CHECK();
   unsigned long long hcnt = 0;
   EG_CUDA_TRY(cudaMemcpyAsync(&hcnt, cnt, 8, cudaMemcpyDeviceToHost, st));
@@ -245,6 +347,7 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   if (hcnt > cap) {
     // Band list overflowed (adversarial data): recompute every sign exactly.
     EG_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)replicates * n * W * 8, st));
+    EG_PROF(PC_FIXUP, st);
     if (x_is_f64)
       k_fixup<double><<<fgrid * 4, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W,
                                                  d_codes, items, cnt, cap, cols, 1);
@@ -393,13 +496,19 @@ int eg_grouped_sort(const uint64_t *d_codes, int64_t n, int32_t length,
   uint8_t *flags = ar.take<uint8_t>(n);
   if (!keyw || !idx || !flags) return EG_ERR_WORKSPACE;
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
-  k_iota<<<grid, 256, 0, st>>>(d_perm, n);
+  {
+    EG_PROF(PC_MISC, st);
+    k_iota<<<grid, 256, 0, st>>>(d_perm, n);
+  }
   EG_LAUNCH_CHECK();
   size_t mark = ar.used;
   for (int w = W - 1; w >= 0; --w) {
     const uint64_t kw = ub.kept[0][w];
     if (!kw) continue;
-    k_masked_word<<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, w, kw, keyw);
+    {
+      EG_PROF(PC_MISC, st);
+      k_masked_word<<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, w, kw, keyw);
+    }
     EG_LAUNCH_CHECK();
     int shifts[8], np = 0;
     for (int s = 0; s < 64; s += 8)
@@ -409,6 +518,7 @@ int eg_grouped_sort(const uint64_t *d_codes, int64_t n, int32_t length,
     if (rc) return rc;
   }
   ar.used = mark;
+  EG_PROF(PC_MISC, st);
   k_group_flags<4><<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, ub, flags, idx);
   EG_LAUNCH_CHECK();
   int64_t groups = 0;
@@ -428,6 +538,7 @@ int eg_first_witness(const uint64_t *d_keys, int64_t m, const uint64_t *const *d
   cudaStream_t st = (cudaStream_t)stream;
   if (m <= 0) return EG_OK;
   unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, 8192);
+  EG_PROF(PC_MISC, st);
   k_first_witness<<<grid, 256, 0, st>>>(d_keys, m, d_pools, n_pools, W, d, d_keep);
   EG_LAUNCH_CHECK();
   return EG_OK;
@@ -487,12 +598,15 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   if (!flags || !dist || !bad) return EG_ERR_WORKSPACE;
   EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 8, st));
   unsigned grid = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)num_sms() * 64);
+  {
+  EG_PROF(PC_VERIFY, st);
   if (x_is_f64)
     k_verify<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, d_keys, m,
                                            metric, eps, flags, dist, bad);
   else
     k_verify<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m, metric,
                                           eps, flags, dist, bad);
+  }
   EG_LAUNCH_CHECK();
   int rc = compact<double>(d_keys, dist, flags, m, d_out_keys, d_out_dist, h_count, ar, st);
   if (rc) return rc;

@@ -24,6 +24,28 @@ void set_error(const char *fmt, ...);
 
 #define EG_LAUNCH_CHECK() EG_CUDA_TRY(cudaGetLastError())
 
+// ------------------------------------------------------- instrumentation
+// Every kernel launch is counted (eg_launch_count); when profiling is on,
+// a pair of CUDA events brackets each launch (or launch group) on its
+// stream and eg_profile_read() folds them into per-class milliseconds.
+enum ProfClass {
+  PC_ROW_STATS, PC_PROJECT, PC_FIXUP, PC_MSM_HIST, PC_MSM_SCAN, PC_MSM_SCATTER, PC_MSM_GROUP,
+  PC_MSM_SPILL, PC_MSM_BATCH, PC_SORT_UPSWEEP, PC_SCAN, PC_SORT_DOWNSWEEP, PC_VERIFY,
+  PC_COMPACT, PC_MISC, PC_COUNT
+};
+void prof_begin(int cls, cudaStream_t st, int launches);
+void prof_end(int cls, cudaStream_t st);
+struct ProfScope {
+  int cls;
+  cudaStream_t st;
+  ProfScope(int c, cudaStream_t s, int launches = 1) : cls(c), st(s) { prof_begin(c, s, launches); }
+  ~ProfScope() { prof_end(cls, st); }
+};
+#define EG_CAT2(a, b) a##b
+#define EG_CAT(a, b) EG_CAT2(a, b)
+#define EG_PROF(cls, st) ::eg::ProfScope EG_CAT(_eg_prof_, __LINE__)((cls), (st))
+#define EG_PROF_GROUP(cls, st) ::eg::ProfScope EG_CAT(_eg_prof_, __LINE__)((cls), (st), 0)
+
 // ------------------------------------------------------------- workspace
 // Bump allocator over the caller's workspace (256-byte aligned slices).
 struct Arena {

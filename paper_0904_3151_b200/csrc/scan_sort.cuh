@@ -72,6 +72,7 @@ __host__ inline int scan_exclusive_u32(const uint32_t *in, uint32_t *out, int64_
   if (L <= 0) return EG_OK;
   int64_t nb = (L + SCAN_TILE - 1) / SCAN_TILE;
   if (nb == 1) {
+    EG_PROF(PC_SCAN, st);
     k_scan_tiles<<<1, SCAN_NT, 0, st>>>(in, L, out, nullptr);
     EG_LAUNCH_CHECK();
     return EG_OK;
@@ -79,11 +80,17 @@ __host__ inline int scan_exclusive_u32(const uint32_t *in, uint32_t *out, int64_
   uint32_t *sums = ar.take<uint32_t>(nb);
   uint32_t *sums_x = ar.take<uint32_t>(nb);
   if (!sums || !sums_x) return EG_ERR_WORKSPACE;
-  k_scan_reduce<<<(unsigned)nb, SCAN_NT, 0, st>>>(in, L, sums);
+  {
+    EG_PROF(PC_SCAN, st);
+    k_scan_reduce<<<(unsigned)nb, SCAN_NT, 0, st>>>(in, L, sums);
+  }
   EG_LAUNCH_CHECK();
   int rc = scan_exclusive_u32(sums, sums_x, nb, ar, st);
   if (rc) return rc;
-  k_scan_tiles<<<(unsigned)nb, SCAN_NT, 0, st>>>(in, L, out, sums_x);
+  {
+    EG_PROF(PC_SCAN, st);
+    k_scan_tiles<<<(unsigned)nb, SCAN_NT, 0, st>>>(in, L, out, sums_x);
+  }
   EG_LAUNCH_CHECK();
   return EG_OK;
 }
@@ -212,10 +219,14 @@ __host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const 
   uint32_t *vsrc = vals, *vdst = valt;
   for (int p = 0; p < npass; ++p) {
     ar.used = mark;
-    k_radix_upsweep<<<(unsigned)ntiles, RS_NT, 0, st>>>(ksrc, m, shifts[p], ntiles, counts);
+    {
+      EG_PROF(PC_SORT_UPSWEEP, st);
+      k_radix_upsweep<<<(unsigned)ntiles, RS_NT, 0, st>>>(ksrc, m, shifts[p], ntiles, counts);
+    }
     EG_LAUNCH_CHECK();
     int rc = scan_exclusive_u32(counts, counts, ntiles * 256, ar, st);
     if (rc) return rc;
+    EG_PROF(PC_SORT_DOWNSWEEP, st);
     if (vals)
       k_radix_downsweep<true><<<(unsigned)ntiles, RS_NT, 0, st>>>(ksrc, vsrc, kdst, vdst, m,
                                                                  shifts[p], ntiles, counts);
@@ -311,11 +322,18 @@ __host__ inline int compact(const uint64_t *keys, const V *vals, const uint8_t *
   uint32_t *tc = ar.take<uint32_t>(nt + 1);
   if (!tc) return EG_ERR_WORKSPACE;
   EG_CUDA_TRY(cudaMemsetAsync(tc + nt, 0, 4, st));
-  k_flag_count<<<(unsigned)nt, CP_NT, 0, st>>>(flags, m, tc);
+  {
+    EG_PROF(PC_COMPACT, st);
+    k_flag_count<<<(unsigned)nt, CP_NT, 0, st>>>(flags, m, tc);
+  }
   EG_LAUNCH_CHECK();
   int rc = scan_exclusive_u32(tc, tc, nt + 1, ar, st);
   if (rc) return rc;
-  k_flag_scatter<V><<<(unsigned)nt, CP_NT, 0, st>>>(keys, vals, flags, m, tc, out_keys, out_vals);
+  {
+    EG_PROF(PC_COMPACT, st);
+    k_flag_scatter<V><<<(unsigned)nt, CP_NT, 0, st>>>(keys, vals, flags, m, tc, out_keys,
+                                                      out_vals);
+  }
   EG_LAUNCH_CHECK();
   uint32_t total = 0;
   EG_CUDA_TRY(cudaMemcpyAsync(&total, tc + nt, 4, cudaMemcpyDeviceToHost, st));

@@ -1,0 +1,175 @@
+"""Multi-GPU build: one process per GPU, torch.distributed (NCCL) plumbing.
+
+Sharding: every output pair has exactly one owning
+(replicate, mask) unit -- the canonical-mask rule inside a replicate and the
+first-witness rule across replicates -- so units can be split across ranks
+with disjoint outputs and no cross-rank dedup.
+
+    1. rows are split into equal shards; each rank projects its shard
+       (eg_project) and computes its row norms (eg_row_stats);
+    2. codes and norms are all-gathered over NVLink (NCCL all_gather);
+    3. units are assigned cyclically (unit u -> rank u % world), each rank
+       runs eg_msm_pairs on its units, sorts and verifies its candidates
+       (rows are resident on every rank for the verify gathers);
+    4. per-rank sorted edge runs are gathered to rank 0 and merged by one
+       key sort.
+
+The collective/merge logic is written against a small ``ops`` interface so
+the same code runs with the CUDA ops (``DeviceOps``) and, in tests, with the
+CPU oracle over gloo.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as tdist
+
+from . import engine
+
+
+def my_units(total: int, world: int, rank: int):
+    """Cyclic unit assignment: balanced to within one unit per rank."""
+    return list(range(rank, total, world))
+
+
+def row_shard(n: int, world: int, rank: int):
+    per = -(-n // world)
+    lo = min(n, rank * per)
+    return lo, min(n, lo + per), per
+
+
+class DeviceOps:
+    """CUDA implementations of the per-rank stages."""
+
+    def norms(self, x):
+        return engine.validate_rows(x)
+
+    def project(self, x, norms, params):
+        codes, _ = engine.project_codes(x, norms, params.length, params.seed,
+                                        list(range(1, params.replicates + 1)))
+        return codes
+
+    def candidates(self, codes, params, units):
+        from .bitpool import block_partition
+        bounds = block_partition(params.length, params.blocks)
+        reps, masks = engine.units_for(range(params.replicates), params.blocks, params.mismatch)
+        sel = np.asarray(units, dtype=np.int64)
+        keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch,
+                                      reps[sel], masks[sel])
+        return keys, info
+
+    def sort(self, keys, n):
+        return engine.sort_pair_keys(keys, n)
+
+    def verify(self, x, norms, keys, metric, eps):
+        from .pipeline import _metric_id
+        return engine.verify(x, norms, keys, _metric_id(metric), eps)
+
+    def merge(self, keys, dists, n):
+        """Sort concatenated per-rank runs by key, carrying distances."""
+        m = keys.numel()
+        if m <= 1:
+            return keys, dists
+        idx = torch.arange(m, dtype=torch.int32, device=keys.device)
+        from . import _native
+        lib = _native.lib()
+        ws = engine._ws(lib.eg_sort_workspace(m, 1), keys.device)
+        _native.check(lib.eg_sort_keys(keys.data_ptr(), idx.data_ptr(), m, 64, ws.data_ptr(),
+                                       ws.numel(), engine._stream(keys.device)), "merge")
+        return keys, dists.index_select(0, idx.long())
+
+
+def _all_gather_rows(t: torch.Tensor, per: int, world: int) -> torch.Tensor:
+    """All-gather equal-size row shards (dim 0 padded to ``per``)."""
+    pad = per - t.shape[0]
+    if pad:
+        t = torch.cat([t, t.new_zeros((pad,) + tuple(t.shape[1:]))])
+    out = t.new_empty((per * world,) + tuple(t.shape[1:]))
+    tdist.all_gather_into_tensor(out, t.contiguous())
+    return out
+
+
+def gather_codes(codes_shard, norms_shard, n, world, rank):
+    """(reps, n_r, W) shards -> (reps, n, W) full codes + full norms."""
+    lo, hi, per = row_shard(n, world, rank)
+    reps = codes_shard.shape[0]
+    full = []
+    for h in range(reps):
+        full.append(_all_gather_rows(codes_shard[h], per, world)[:n])
+    norms = _all_gather_rows(norms_shard, per, world)[:n]
+    return torch.stack(full).contiguous(), norms.contiguous()
+
+
+def gather_edges(keys, dists, world, rank, ops, n):
+    """Per-rank sorted edge runs -> merged sorted edges on rank 0."""
+    cnt = torch.tensor([keys.numel()], dtype=torch.int64, device=keys.device)
+    counts = [torch.zeros_like(cnt) for _ in range(world)]
+    tdist.all_gather(counts, cnt)
+    counts = [int(c.item()) for c in counts]
+    mx = max(counts) if counts else 0
+    if mx == 0:
+        return keys[:0], dists[:0]
+    kp = torch.cat([keys, keys.new_zeros(mx - keys.numel())])
+    dp = torch.cat([dists, dists.new_zeros(mx - dists.numel())])
+    ka = kp.new_empty(mx * world)
+    da = dp.new_empty(mx * world)
+    tdist.all_gather_into_tensor(ka, kp)
+    tdist.all_gather_into_tensor(da, dp)
+    if rank != 0:
+        return None, None
+    ks = torch.cat([ka[r * mx:r * mx + counts[r]] for r in range(world)])
+    ds = torch.cat([da[r * mx:r * mx + counts[r]] for r in range(world)])
+    return ops.merge(ks, ds, n)
+
+
+def build_step(x, params, metric: str, world: int, rank: int, ops=None):
+    """One full build of ``x`` (resident rows) on ``world`` ranks.
+
+    Returns a dict with rank 0's merged ``keys``/``dist`` (None on other
+    ranks) and this rank's counters."""
+    ops = ops or DeviceOps()
+    n = x.shape[0]
+    if world == 1:
+        from .pipeline import build_graph_device
+        out = build_graph_device(x, params, metric=metric)
+        return {"keys": out["keys"], "dist": out["dist"], "info": out["info"]}
+    lo, hi, per = row_shard(n, world, rank)
+    xs = x[lo:hi]
+    norms_s = ops.norms(xs)
+    codes_s = ops.project(xs, norms_s, params)
+    codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
+    from math import comb
+    units = my_units(params.replicates * comb(params.blocks, params.mismatch), world, rank)
+    from .pipeline import lsh_radius  # noqa: F401  (metric mapping lives there)
+    keys, info = ops.candidates(codes, params, units)
+    keys = ops.sort(keys, n)
+    ek, ed = ops.verify(x, norms, keys, metric, params.epsilon)
+    mk, md = gather_edges(ek, ed, world, rank, ops, n)
+    return {"keys": mk, "dist": md, "info": info}
+
+
+def hamming_step(codes, params, world: int, rank: int):
+    """Config 2: enumerate_pairs over resident words, units sharded."""
+    from .bitpool import block_partition
+    n = codes.shape[1]
+    bounds = block_partition(params.length, params.blocks)
+    reps, masks = engine.units_for([0], params.blocks, params.mismatch)
+    sel = np.asarray(my_units(len(reps), world, rank), dtype=np.int64)
+    keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, reps[sel],
+                                  masks[sel])
+    engine.sort_pair_keys(keys, n)
+    if world > 1:
+        dummy = torch.zeros(keys.numel(), dtype=torch.float64, device=keys.device)
+        keys, _ = gather_edges(keys, dummy, world, rank, DeviceOps(), n)
+    return {"keys": keys, "dist": None, "info": info}
+
+
+def last_counts(res):
+    if not res:
+        return None
+    info = res.get("info") or {}
+    keys = res.get("keys")
+    return {"candidates": info.get("emitted"), "raw": info.get("raw"), "new": info.get("new"),
+            "edges": int(keys.numel()) if keys is not None else None,
+            "max_group": info.get("max_group")}

@@ -30,14 +30,14 @@ def eg():
     return eg
 
 
-def pairs_equal_except_band(got_pairs, got_dist, ref_pairs, ref_dist, eps):
+def pairs_equal_except_band(got_pairs, got_dist, ref_pairs, ref_dist, eps, dist_tol=DIST_TOL):
     gk = {tuple(p): d for p, d in zip(got_pairs.tolist(), got_dist.tolist())}
     rk = {tuple(p): d for p, d in zip(ref_pairs.tolist(), ref_dist.tolist())}
     for p in set(gk) ^ set(rk):
         d = gk.get(p, rk.get(p))
         assert abs(d - eps) <= BAND, (p, d)
     for p in set(gk) & set(rk):
-        assert abs(gk[p] - rk[p]) <= DIST_TOL, (p, gk[p], rk[p])
+        assert abs(gk[p] - rk[p]) <= dist_tol, (p, gk[p], rk[p])
 
 
 # ------------------------------------------------------------- enumeration
@@ -277,10 +277,12 @@ def _config_build(eg, oracle, manifest, name, x, metric="cosine"):
     else:
         ref = oracle.build_graph(x, p["epsilon"], p["length"], p["mismatch"], p["blocks"],
                                  p["replicates"], 0)
-        # Euclidean on unit rows agrees with the cosine route except in the band
+        # Euclidean on fp32-normalised rows agrees with the cosine route to
+        # ~1e-7 (|x| = 1 only to fp32 precision): identical edge sets except
+        # within the 1e-6 band, distances equal to 1e-6.
         d_cos = graph.edge_list.distances ** 2 / 2.0
         pairs_equal_except_band(graph.edge_list.pairs, d_cos, ref.pairs, ref.distances,
-                                p["epsilon"])
+                                p["epsilon"], dist_tol=BAND)
     return graph
 
 
