@@ -174,7 +174,10 @@ template <int W>
 static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch> &batches,
                    cudaStream_t st) {
   const size_t smem_hist = (size_t)lay.B * 4, smem_scatter = (size_t)lay.B * 8;
-  const size_t smem_group = sizeof(GroupSmem<W>);
+  const size_t smem_group = sizeof(HGroupSmem<W, MSM_SCAP, MSM_SNT>);
+  const size_t smem_medium =
+      sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>);
+  a.gcnt_min = MediumCfg<W>::CAP;
   EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_hist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_hist));
   EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_scatter<W>,
@@ -182,6 +185,8 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
                                    (int)smem_scatter));
   EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_group<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem_group));
+  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_medium<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_medium));
   const unsigned tiles = (unsigned)((a.n + MSM_TILE - 1) / MSM_TILE);
   const unsigned spill_grid = (unsigned)num_sms() * 8;
   for (const UnitBatch &ub : batches) {
@@ -202,7 +207,11 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
     dim3 g4(lay.B, ub.count);
     {
       EG_PROF(PC_MSM_GROUP, st);
-      k_msm_group<W><<<g4, MSM_GNT, smem_group, st>>>(a, ub);
+      k_msm_group<W><<<g4, MSM_SNT, smem_group, st>>>(a, ub);
+    }
+    {
+      EG_PROF(PC_MSM_SPILL, st);
+      k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, st>>>(a, ub);
     }
     {
       EG_PROF(PC_MSM_SPILL, st);

@@ -34,9 +34,7 @@ constexpr int MSM_MAXU = 16;            // units per launch batch
 constexpr int MSM_IPT = 8;              // items per thread, hist/scatter
 constexpr int MSM_NT = 512;             // threads, hist/scatter
 constexpr int MSM_TILE = MSM_IPT * MSM_NT;
-constexpr int MSM_GNT = 256;            // threads, group kernel
-constexpr int MSM_CAP = 2048;           // shared-memory bucket capacity
-constexpr int MSM_TARGET = 512;         // target mean bucket size
+constexpr int MSM_TARGET = 384;         // target mean bucket size
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 13;         // at most 8192 buckets per unit
 
@@ -64,6 +62,7 @@ struct MsmArgs {
                                  // [3..3+reps) raw, [3+reps..) new
   uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
   int64_t spill_cap;
+  int gcnt_min;                  // spilled buckets above this size count groups
 };
 
 template <int W>
@@ -254,166 +253,143 @@ __device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia,
 }
 
 // ------------------------------------------------------------------ 4
-template <int W>
-struct GroupSmem {
-  uint64_t A[MSM_CAP * W];        // bucket elements, later gathered codes
-  uint64_t Bv[MSM_CAP];           // elements ordered by fine digit / runs
-  uint32_t off[2 * MSM_CAP + 1];  // fine-digit offsets
-  uint32_t runs[MSM_CAP / 2];     // (start << 16) | len
-  uint32_t pp[MSM_CAP / 2 + 1];   // pair prefix per run
-  uint8_t inrun[MSM_CAP];
+// Bucket processing, entirely in shared memory.  An open-addressing table
+// keyed by the 32-bit secondary hash groups the bucket's rows exactly by
+// (h2), which is the masked key up to 2^-32 collisions (filtered later by an
+// exact key compare).  Only rows of multi-row groups are materialised
+// (rows + gathered codes, grouped contiguously); singletons -- the vast
+// majority -- cost one table insert.  A flattened, load-balanced pair loop
+// then visits every in-group pair once (the reference's group visits,
+// hamming_join.py:116-122) and applies pair_verdict.
+template <int W, int CAP, int NT>
+struct HGroupSmem {
+  uint32_t key[2 * CAP];     // h2 per slot (EMPTY = ~0), then member offsets
+  uint32_t cnt[2 * CAP];     // rows per slot
+  uint32_t members[CAP];     // rows of multi-row groups, grouped
+  uint64_t codes[CAP * W];   // their codes
+  uint32_t runs[CAP / 2];    // (start << 16) | len
+  uint32_t pp[CAP / 2 + 1];  // pair prefix per run
   uint8_t b2b[EG_MAX_LENGTH];
-  uint32_t sw[MSM_GNT / 32];
+  uint32_t sw[NT / 32];
   uint32_t nruns, maxrun, raw, neu;
 };
 
-template <int W>
-__global__ void __launch_bounds__(MSM_GNT) k_msm_group(const __grid_constant__ MsmArgs a,
-                                                            const __grid_constant__ UnitBatch ub) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  GroupSmem<W> &S = *reinterpret_cast<GroupSmem<W> *>(smraw);
-  const int u = blockIdx.y;
-  const int b = blockIdx.x;
-  const int B = 1 << a.lgB;
-  const uint32_t *st = a.starts + (int64_t)u * (B + 1);
-  const uint32_t s0 = st[b], s = st[b + 1] - s0;
-  if (s < 2) return;
-  if (s > MSM_CAP) {
-    if (threadIdx.x == 0) {
-      unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
-      if ((int64_t)slot < a.spill_cap) {
-        a.spill[slot * 3 + 0] = (uint32_t)u;
-        a.spill[slot * 3 + 1] = s0;
-        a.spill[slot * 3 + 2] = s;
-      }
-    }
-    if ((int64_t)s * 4 > a.n) {   // reference-visible group size check
-      uint32_t *g = a.gcnt + (int64_t)u * a.n + s0;
-      for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) g[i] = 0;
-    }
-    return;
-  }
+constexpr uint32_t HG_EMPTY = 0xffffffffu;
+
+template <int W, int CAP, int NT>
+__device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const MsmArgs &a,
+                                               const UnitBatch &ub, int u, uint32_t s0,
+                                               uint32_t s) {
+  constexpr int PT = CAP / NT;
   const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
   const int rep = ub.rep[u];
-  const int lgF = max(1, ilog2_ceil(2ull * s));
-  const uint32_t F = 1u << lgF;
-  for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) S.A[i] = el[i];
-  for (uint32_t i = threadIdx.x; i <= F; i += MSM_GNT) S.off[i] = 0;
-  for (int i = threadIdx.x; i < a.L; i += MSM_GNT) S.b2b[i] = a.bit2blk[i];
+  const uint32_t T = 1u << max(1, ilog2_ceil(2ull * s));
+  for (uint32_t i = threadIdx.x; i < T; i += NT) {
+    S.key[i] = HG_EMPTY;
+    S.cnt[i] = 0;
+  }
   if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; }
-  __syncthreads();
-  // fine digit = top lgF bits of h2 (independent of the bucket digit)
-  constexpr int PT = MSM_CAP / MSM_GNT;
-  uint32_t rk[PT];
+  uint64_t e[PT];
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
-    uint32_t i = threadIdx.x + j * MSM_GNT;
-    if (i < s) rk[j] = atomicAdd(&S.off[(uint32_t)(S.A[i] >> 32) >> (32 - lgF)], 1u);
+    const uint32_t i = threadIdx.x + j * NT;
+    e[j] = i < s ? el[i] : 0ull;
   }
   __syncthreads();
-  {  // exclusive scan of F counts (blocked, F/GNT per thread)
-    const uint32_t per = (F + MSM_GNT - 1) / MSM_GNT;
+  uint32_t sl[PT], rk[PT];
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    const uint32_t i = threadIdx.x + j * NT;
+    if (i < s) {
+      uint32_t h2 = (uint32_t)(e[j] >> 32);
+      if (h2 == HG_EMPTY) h2 = HG_EMPTY - 1;
+      uint32_t slot = h2 & (T - 1);
+      while (true) {
+        const uint32_t old = atomicCAS(&S.key[slot], HG_EMPTY, h2);
+        if (old == HG_EMPTY || old == h2) break;
+        slot = (slot + 1) & (T - 1);
+      }
+      sl[j] = slot;
+      rk[j] = atomicAdd(&S.cnt[slot], 1u);
+    }
+  }
+  __syncthreads();
+  {  // member offsets of multi-row slots (blocked scan), run list
+    const uint32_t per = (T + NT - 1) / NT;
     uint32_t loc = 0;
-    for (uint32_t j = 0; j < per; ++j) {
-      uint32_t f = threadIdx.x * per + j;
-      if (f < F) loc += S.off[f];
+    for (uint32_t q = 0; q < per; ++q) {
+      const uint32_t t = threadIdx.x * per + q;
+      if (t < T) {
+        const uint32_t c = S.cnt[t];
+        loc += c >= 2 ? c : 0;
+      }
     }
     uint32_t tot;
-    uint32_t run = block_exclusive_scan<MSM_GNT>(loc, tot, S.sw);
-    for (uint32_t j = 0; j < per; ++j) {
-      uint32_t f = threadIdx.x * per + j;
-      if (f < F) {
-        uint32_t c = S.off[f];
-        S.off[f] = run;
-        run += c;
+    uint32_t run = block_exclusive_scan<NT>(loc, tot, S.sw);
+    for (uint32_t q = 0; q < per; ++q) {
+      const uint32_t t = threadIdx.x * per + q;
+      if (t < T) {
+        const uint32_t c = S.cnt[t];
+        if (c >= 2) {
+          S.key[t] = run;
+          const uint32_t r = atomicAdd(&S.nruns, 1u);
+          S.runs[r] = (run << 16) | c;
+          atomicMax(&S.maxrun, c);
+          run += c;
+        }
       }
-    }
-    if (threadIdx.x == 0) S.off[F] = s;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int j = 0; j < PT; ++j) {
-    uint32_t i = threadIdx.x + j * MSM_GNT;
-    if (i < s) {
-      uint64_t e = S.A[i];
-      S.Bv[S.off[(uint32_t)(e >> 32) >> (32 - lgF)] + rk[j]] = e;
-    }
-  }
-  for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) S.inrun[i] = 0;
-  __syncthreads();
-  // runs: one thread per multi-row digit bin; sort the bin by (h2,row) if
-  // it mixes hashes (insertion sort, bins are tiny), then split into runs.
-  for (uint32_t f = threadIdx.x; f < F; f += MSM_GNT) {
-    const uint32_t lo = S.off[f], hi = S.off[f + 1];
-    if (hi - lo < 2) continue;
-    const uint32_t h0 = (uint32_t)(S.Bv[lo] >> 32);
-    bool mixed = false;
-    for (uint32_t i = lo + 1; i < hi; ++i) mixed |= (uint32_t)(S.Bv[i] >> 32) != h0;
-    if (mixed) {
-      for (uint32_t i = lo + 1; i < hi; ++i) {
-        uint64_t v = S.Bv[i];
-        uint32_t j = i;
-        while (j > lo && (S.Bv[j - 1] >> 32) > (v >> 32)) { S.Bv[j] = S.Bv[j - 1]; --j; }
-        S.Bv[j] = v;
-      }
-    }
-    uint32_t rs = lo;
-    while (rs < hi) {
-      uint32_t re = rs + 1;
-      const uint32_t hr = (uint32_t)(S.Bv[rs] >> 32);
-      while (re < hi && (uint32_t)(S.Bv[re] >> 32) == hr) ++re;
-      const uint32_t len = re - rs;
-      if (len >= 2) {
-        uint32_t slot = atomicAdd(&S.nruns, 1u);
-        S.runs[slot] = (rs << 16) | len;
-        atomicMax(&S.maxrun, len);
-        for (uint32_t i = rs; i < re; ++i) S.inrun[i] = 1;
-      }
-      rs = re;
     }
   }
   __syncthreads();
   const uint32_t R = S.nruns;
-  // gather codes of rows that sit in runs (A is free now)
+  if (R == 0) {
+    __syncthreads();
+    return;
+  }
   const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
-  for (uint32_t i = threadIdx.x; i < s; i += MSM_GNT) {
-    if (S.inrun[i]) {
-      const uint32_t row = (uint32_t)S.Bv[i];
 #pragma unroll
-      for (int w = 0; w < W; ++w) S.A[i * W + w] = __ldg(codes + (int64_t)row * W + w);
+  for (int j = 0; j < PT; ++j) {
+    const uint32_t i = threadIdx.x + j * NT;
+    if (i < s && S.cnt[sl[j]] >= 2) {
+      const uint32_t pos = S.key[sl[j]] + rk[j];
+      const uint32_t row = (uint32_t)e[j];
+      S.members[pos] = row;
+#pragma unroll
+      for (int w = 0; w < W; ++w) S.codes[pos * W + w] = __ldg(codes + (int64_t)row * W + w);
     }
   }
   {  // pair prefix over runs
-    const uint32_t per = (R + MSM_GNT - 1) / MSM_GNT;
+    const uint32_t per = (R + NT - 1) / NT;
     uint32_t loc = 0;
-    for (uint32_t j = 0; j < per; ++j) {
-      uint32_t r = threadIdx.x * per + j;
+    for (uint32_t q = 0; q < per; ++q) {
+      const uint32_t r = threadIdx.x * per + q;
       if (r < R) {
-        uint32_t len = S.runs[r] & 0xffffu;
+        const uint32_t len = S.runs[r] & 0xffffu;
         loc += len * (len - 1) / 2;
       }
     }
     uint32_t tot;
-    uint32_t run = block_exclusive_scan<MSM_GNT>(loc, tot, S.sw);
-    for (uint32_t j = 0; j < per; ++j) {
-      uint32_t r = threadIdx.x * per + j;
+    uint32_t run = block_exclusive_scan<NT>(loc, tot, S.sw);
+    for (uint32_t q = 0; q < per; ++q) {
+      const uint32_t r = threadIdx.x * per + q;
       if (r < R) {
         S.pp[r] = run;
-        uint32_t len = S.runs[r] & 0xffffu;
+        const uint32_t len = S.runs[r] & 0xffffu;
         run += len * (len - 1) / 2;
       }
     }
     if (threadIdx.x == 0) S.pp[R] = tot;
+    // S.b2b was filled by the caller before the first bucket
   }
   __syncthreads();
   const uint32_t P = S.pp[R];
   const unsigned long long *kept = ub.kept[u];
   const uint64_t maskbits = ub.maskbits[u];
   uint32_t my_raw = 0, my_new = 0;
-  for (uint32_t p = threadIdx.x; p < P; p += MSM_GNT) {
-    uint32_t lo = 0, hi = R;  // find r: pp[r] <= p < pp[r+1]
+  for (uint32_t p = threadIdx.x; p < P; p += NT) {
+    uint32_t lo = 0, hi = R;  // r with pp[r] <= p < pp[r+1]
     while (hi - lo > 1) {
-      uint32_t mid = (lo + hi) >> 1;
+      const uint32_t mid = (lo + hi) >> 1;
       if (S.pp[mid] <= p) lo = mid; else hi = mid;
     }
     const uint32_t rr = S.runs[lo];
@@ -424,17 +400,15 @@ __global__ void __launch_bounds__(MSM_GNT) k_msm_group(const __grid_constant__ M
     ib += start;
     uint64_t ca[W], cb[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) { ca[w] = S.A[ia * W + w]; cb[w] = S.A[ib * W + w]; }
-    const uint32_t ra = (uint32_t)S.Bv[ia], rb = (uint32_t)S.Bv[ib];
-    int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
+    for (int w = 0; w < W; ++w) { ca[w] = S.codes[ia * W + w]; cb[w] = S.codes[ib * W + w]; }
+    const uint32_t ra = S.members[ia], rb = S.members[ib];
+    const int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
     my_raw += v > 0;
     my_new += v == 2;
     const bool emit = v == 2;
-    unsigned long long slot = warp_append(emit, &a.ctr[0]);
-    if (emit && slot < a.out_cap) {
-      uint32_t lo_r = min(ra, rb), hi_r = max(ra, rb);
-      a.out_keys[slot] = ((unsigned long long)lo_r << 32) | hi_r;
-    }
+    const unsigned long long slot = warp_append(emit, &a.ctr[0]);
+    if (emit && slot < a.out_cap)
+      a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
   }
   if (my_raw) atomicAdd(&S.raw, my_raw);
   if (my_new) atomicAdd(&S.neu, my_new);
@@ -443,6 +417,66 @@ __global__ void __launch_bounds__(MSM_GNT) k_msm_group(const __grid_constant__ M
     if (S.raw) atomicAdd(&a.ctr[3 + rep], (unsigned long long)S.raw);
     if (S.neu) atomicAdd(&a.ctr[3 + a.reps + rep], (unsigned long long)S.neu);
     atomicMax(&a.ctr[1], (unsigned long long)S.maxrun);
+  }
+  __syncthreads();
+}
+
+constexpr int MSM_SCAP = 1024;   // small buckets: one CTA each, many CTAs per SM
+constexpr int MSM_SNT = 128;
+template <int W>
+struct MediumCfg {
+  static constexpr int CAP = W <= 2 ? 4096 : 2048;
+  static constexpr int NT = 512;
+};
+
+// Small buckets (s <= MSM_SCAP): grid (B, units).  Larger buckets are queued
+// on the spill list for k_msm_medium / k_msm_spill.
+template <int W>
+__global__ void __launch_bounds__(MSM_SNT) k_msm_group(const __grid_constant__ MsmArgs a,
+                                                       const __grid_constant__ UnitBatch ub) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  using Smem = HGroupSmem<W, MSM_SCAP, MSM_SNT>;
+  Smem &S = *reinterpret_cast<Smem *>(smraw);
+  const int u = blockIdx.y;
+  const int b = blockIdx.x;
+  const int B = 1 << a.lgB;
+  const uint32_t *st = a.starts + (int64_t)u * (B + 1);
+  const uint32_t s0 = st[b], s = st[b + 1] - s0;
+  if (s < 2) return;
+  if (s > MSM_SCAP) {
+    if (threadIdx.x == 0) {
+      const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+      if ((int64_t)slot < a.spill_cap) {
+        a.spill[slot * 3 + 0] = (uint32_t)u;
+        a.spill[slot * 3 + 1] = s0;
+        a.spill[slot * 3 + 2] = s;
+      }
+    }
+    if (s > (uint32_t)MediumCfg<W>::CAP && (int64_t)s * 4 > a.n) {
+      uint32_t *g = a.gcnt + (int64_t)u * a.n + s0;   // group counts for the warning
+      for (uint32_t i = threadIdx.x; i < s; i += MSM_SNT) g[i] = 0;
+    }
+    return;
+  }
+  for (int i = threadIdx.x; i < a.L; i += MSM_SNT) S.b2b[i] = a.bit2blk[i];
+  process_bucket<W, MSM_SCAP, MSM_SNT>(S, a, ub, u, s0, s);
+}
+
+// Medium buckets (MSM_SCAP < s <= MediumCfg::CAP) from the spill list,
+// persistent CTAs.
+template <int W>
+__global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
+    const __grid_constant__ MsmArgs a, const __grid_constant__ UnitBatch ub) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  using Smem = HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>;
+  Smem &S = *reinterpret_cast<Smem *>(smraw);
+  const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
+  for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
+  for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
+    const uint32_t s = a.spill[sb * 3 + 2];
+    if (s > (uint32_t)MediumCfg<W>::CAP) continue;
+    process_bucket<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>(S, a, ub, (int)a.spill[sb * 3],
+                                                           a.spill[sb * 3 + 1], s);
   }
 }
 
@@ -462,6 +496,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
   for (unsigned long long sb = 0; sb < nspill; ++sb) {
     const int u = (int)a.spill[sb * 3 + 0];
     const uint32_t s0 = a.spill[sb * 3 + 1], s = a.spill[sb * 3 + 2];
+    if (s <= (uint32_t)MediumCfg<W>::CAP) continue;
     const uint32_t nt = (s + MSM_SPILL_T - 1) / MSM_SPILL_T;
     const unsigned long long ntp = (unsigned long long)nt * (nt + 1) / 2;
     const int rep = ub.rep[u];
@@ -551,7 +586,7 @@ __global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
   for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
     const int u = (int)a.spill[sb * 3 + 0];
     const uint32_t s0 = a.spill[sb * 3 + 1], s = a.spill[sb * 3 + 2];
-    if ((int64_t)s * 4 <= a.n) continue;
+    if ((int64_t)s * 4 <= a.n || s <= (uint32_t)a.gcnt_min) continue;
     const uint32_t *gc = a.gcnt + (int64_t)u * a.n + s0;
     uint32_t mx = 0;
     for (uint32_t i = threadIdx.x; i < s; i += blockDim.x) mx = max(mx, gc[i]);

@@ -1,0 +1,40 @@
+"""Run a few builds of one config on cuda:0 (profiling driver for ncu).
+
+    python tools/run_build.py --config cfg3 --reps 2
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_0904_3151_b200 as eg  # noqa: E402
+from paper_0904_3151_b200 import distributed  # noqa: E402
+from paper_0904_3151_b200.workloads import CONFIGS  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg3")
+ap.add_argument("--reps", type=int, default=2)
+args = ap.parse_args()
+cfg = CONFIGS[args.config]
+params = bench.params_for(cfg, eg)
+data = bench.make_inputs(args.config)
+dev = torch.device("cuda", 0)
+if cfg.metric == "hamming":
+    import numpy as np
+    x = torch.from_numpy(data.view(np.int64)).to(dev).reshape(1, -1, 1)
+else:
+    x = torch.from_numpy(data).to(dev)
+for i in range(args.reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    if cfg.metric == "hamming":
+        res = distributed.hamming_step(x, params, 1, 0)
+    else:
+        res = distributed.build_step(x, params, cfg.metric, 1, 0)
+    torch.cuda.synchronize()
+    print(i, f"{(time.perf_counter() - t0) * 1e3:.1f} ms", distributed.last_counts(res), flush=True)
