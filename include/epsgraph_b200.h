@@ -63,11 +63,13 @@ int eg_profile_read(double *ms_out, long long *count_out, int max_classes);
 /* (lsh.py:48-57), _check_norms (lsh.py:121-125) and the norm pass of     */
 /* filter_exact (pipeline.py:203).                                        */
 /* d_x: n x dim row-major, float32 (x_is_f64 = 0) or float64 (= 1).       */
-/* d_norms[n] = sqrt(sum_q x_q^2) in fp64.  h_bad[0] = first row with a   */
-/* non-finite entry or -1; h_bad[1] = first zero-norm row or -1.          */
+/* d_norms[n] = sqrt(sum_q x_q^2) in fp64.  d_bad (device uint64[2]):     */
+/* [0] = first row with a non-finite entry, [1] = first zero-norm row,    */
+/* UINT64_MAX when none.  Asynchronous (no host synchronisation), so the  */
+/* build can check the flags once at its end.                             */
 /* --------------------------------------------------------------------- */
 int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
-                 double *d_norms, int64_t *h_bad, void *stream);
+                 double *d_norms, uint64_t *d_bad, void *stream);
 
 /* --------------------------------------------------------------------- */
 /* Projection + sign packing.  Replaces _sign_bits (lsh.py:96-113),       */
@@ -80,14 +82,16 @@ int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
 /* row is word t/64, position t%64; padding bits are zero.                */
 /* Signs are bit-identical to the reference's sequential fp64 sum: a fast */
 /* pass decides every entry whose |dot| exceeds a certified error band;   */
-/* the rest are recomputed with separately rounded fp64 mul/add.          */
-/* h_fixups (optional) receives the number of recomputed entries.         */
+/* the rest are recomputed with separately rounded fp64 mul/add (if the   */
+/* band list overflows, every entry is recomputed exactly, on device).    */
+/* d_fixups (optional, device uint64) receives the number of band         */
+/* entries.  Asynchronous.                                                */
 /* --------------------------------------------------------------------- */
 size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t replicates);
 int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
                const double *d_norms, const double *d_r, const double *d_rnorm,
                int32_t length, int32_t replicates, uint64_t *d_codes,
-               void *d_workspace, size_t workspace_bytes, int64_t *h_fixups,
+               void *d_workspace, size_t workspace_bytes, uint64_t *d_fixups,
                void *stream);
 
 /* --------------------------------------------------------------------- */

@@ -103,7 +103,7 @@ static double projection_tau(int dim) {
 }
 
 static unsigned long long fixup_cap(int64_t n, int cols) {
-  unsigned long long c = (unsigned long long)n * cols / 256;
+  unsigned long long c = (unsigned long long)n * cols / 32;
   return c < (1ull << 20) ? (1ull << 20) : c;
 }
 
@@ -178,15 +178,27 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
   const size_t smem_medium =
       sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>);
   a.gcnt_min = MediumCfg<W>::CAP;
-  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_hist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_hist));
-  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_scatter<W>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_scatter));
-  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_group<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_group));
-  EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_medium<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_medium));
+  static size_t set_hist = 0, set_scatter = 0;
+  static bool set_fixed = false;
+  if (smem_hist > set_hist) {
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_hist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_hist));
+    set_hist = smem_hist;
+  }
+  if (smem_scatter > set_scatter) {
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_scatter<W>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_scatter));
+    set_scatter = smem_scatter;
+  }
+  if (!set_fixed) {
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_group<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_group));
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_medium<W>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_medium));
+    set_fixed = true;
+  }
   const unsigned tiles = (unsigned)((a.n + MSM_TILE - 1) / MSM_TILE);
   const unsigned spill_grid = (unsigned)num_sms() * 8;
   for (const UnitBatch &ub : batches) {
@@ -267,26 +279,20 @@ int eg_device_sm_count(void) { return num_sms(); }
 
 // ------------------------------------------------------------ row stats
 int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *d_norms,
-                 int64_t *h_bad, void *stream) {
+                 uint64_t *d_bad, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (n < 0 || dim < 1 || !h_bad) return arg_error("eg_row_stats: bad shape");
-  h_bad[0] = h_bad[1] = -1;
+  if (n < 0 || dim < 1 || !d_bad) return arg_error("eg_row_stats: bad shape");
+  EG_CUDA_TRY(cudaMemsetAsync(d_bad, 0xff, 16, st));
   if (n == 0) return EG_OK;
-  unsigned long long *bad;
-  EG_CUDA_TRY(cudaMallocAsync(&bad, 16, st));
-  EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 16, st));
   unsigned grid = (unsigned)((n + 7) / 8);
   EG_PROF(PC_ROW_STATS, st);
   if (x_is_f64)
-    k_row_stats<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, bad);
+    k_row_stats<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms,
+                                              (unsigned long long *)d_bad);
   else
-    k_row_stats<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, bad);
+    k_row_stats<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms,
+                                             (unsigned long long *)d_bad);
   EG_LAUNCH_CHECK();
-  unsigned long long hb[2];
-  EG_CUDA_TRY(cudaMemcpyAsync(hb, bad, 16, cudaMemcpyDeviceToHost, st));
-  EG_CUDA_TRY(cudaFreeAsync(bad, st));
-  EG_CUDA_TRY(cudaStreamSynchronize(st));
-  for (int i = 0; i < 2; ++i) h_bad[i] = hb[i] == ~0ull ? -1 : (int64_t)hb[i];
   return EG_OK;
 }
 
@@ -300,7 +306,7 @@ size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t repl
 
 int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const double *d_norms,
                const double *d_r, const double *d_rnorm, int32_t length, int32_t replicates,
-               uint64_t *d_codes, void *d_workspace, size_t workspace_bytes, int64_t *h_fixups,
+               uint64_t *d_codes, void *d_workspace, size_t workspace_bytes, uint64_t *d_fixups,
                void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0 || dim < 1 || length < 1 || replicates < 1)
@@ -311,7 +317,7 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   const int cols = length * replicates;
   const int cols_pad = (cols + 31) / 32 * 32;
   EG_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)replicates * n * W * 8, st));
-  if (h_fixups) *h_fixups = 0;
+  if (d_fixups) EG_CUDA_TRY(cudaMemsetAsync(d_fixups, 0, 8, st));
   if (n == 0) return EG_OK;
   Arena ar(d_workspace, workspace_bytes);
   float *rt = ar.take<float>((size_t)dim * cols_pad);
@@ -341,31 +347,22 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   EG_LAUNCH_CHECK();
   const unsigned fgrid = (unsigned)num_sms() * 8;
   {
-  EG_PROF(PC_FIXUP, st);
-  if (x_is_f64)
-    k_fixup<double><<<fgrid, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W, d_codes,
-                                           items, cnt, cap, cols, 0);
-  else
-    k_fixup<float><<<fgrid, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W, d_codes,
-                                          items, cnt, cap, cols, 0);
+    EG_PROF(PC_FIXUP, st);
+    if (x_is_f64) {
+      k_fixup<double><<<fgrid, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W, d_codes,
+                                             items, cnt, cap, cols);
+      k_fixup_overflow<double><<<fgrid, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length,
+                                                      W, d_codes, cnt, cap, cols);
+    } else {
+      k_fixup<float><<<fgrid, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W, d_codes,
+                                            items, cnt, cap, cols);
+      k_fixup_overflow<float><<<fgrid, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W,
+                                                     d_codes, cnt, cap, cols);
+    }
   }
   EG_LAUNCH_CHECK();
-  unsigned long long hcnt = 0;
-  EG_CUDA_TRY(cudaMemcpyAsync(&hcnt, cnt, 8, cudaMemcpyDeviceToHost, st));
-  EG_CUDA_TRY(cudaStreamSynchronize(st));
-  if (hcnt > cap) {
-    // Band list overflowed (adversarial data): recompute every sign exactly.
-    EG_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)replicates * n * W * 8, st));
-    EG_PROF(PC_FIXUP, st);
-    if (x_is_f64)
-      k_fixup<double><<<fgrid * 4, 128, 0, st>>>((const double *)d_x, n, dim, d_r, length, W,
-                                                 d_codes, items, cnt, cap, cols, 1);
-    else
-      k_fixup<float><<<fgrid * 4, 128, 0, st>>>((const float *)d_x, n, dim, d_r, length, W,
-                                                d_codes, items, cnt, cap, cols, 1);
-    EG_LAUNCH_CHECK();
-  }
-  if (h_fixups) *h_fixups = (int64_t)hcnt;
+  if (d_fixups)
+    EG_CUDA_TRY(cudaMemcpyAsync(d_fixups, cnt, 8, cudaMemcpyDeviceToDevice, st));
   return EG_OK;
 }
 

@@ -163,36 +163,58 @@ __global__ void __launch_bounds__(PJ_NT) k_project(const TX *__restrict__ x, int
   }
 }
 
-// Exact recompute of listed entries: the reference's sequential fp64 sum.
+__device__ __forceinline__ void set_code_bit(uint64_t *codes, int64_t n, int L, int W,
+                                             int64_t row, int c, bool one) {
+  const int h = c / L, t = c - h * L;
+  unsigned long long *w =
+      (unsigned long long *)&codes[((int64_t)h * n + row) * W + (t >> 6)];
+  if (one) atomicOr(w, 1ull << (t & 63));
+  else atomicAnd(w, ~(1ull << (t & 63)));
+}
+
+// The reference's sign: sequential fp64 sum, separately rounded mul/add
+// (lsh.py:107-112).  __dmul_rn/__dadd_rn are never contracted into DFMA.
+template <typename TX>
+__device__ __forceinline__ bool exact_sign(const TX *__restrict__ xr, const double *__restrict__ rr,
+                                           int dim) {
+  double acc = 0.0;
+  for (int q = 0; q < dim; ++q) acc = __dadd_rn(acc, __dmul_rn((double)xr[q], rr[q]));
+  return acc > 0.0;
+}
+
+// Exact recompute of listed (in-band) entries.
 template <typename TX>
 __global__ void k_fixup(const TX *__restrict__ x, int64_t n, int dim, const double *__restrict__ r,
                         int L, int W, uint64_t *__restrict__ codes,
                         const unsigned long long *__restrict__ items,
                         const unsigned long long *__restrict__ count, unsigned long long cap,
-                        int cols, int exact_all) {
-  unsigned long long total = exact_all ? (unsigned long long)n * cols
-                                       : min(*count, cap);
+                        int cols) {
+  const unsigned long long total = min(*count, cap);
   for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (unsigned long long)gridDim.x * blockDim.x) {
-    int64_t row;
-    int c;
-    if (exact_all) {
-      row = (int64_t)(i / cols);
-      c = (int)(i % cols);
-    } else {
-      unsigned long long it = items[i];
-      row = (int64_t)(it >> 32);
-      c = (int)(it & 0xffffffffu);
-    }
-    const TX *xr = x + row * dim;
-    const double *rr = r + (int64_t)c * dim;
-    double acc = 0.0;
-    for (int q = 0; q < dim; ++q) acc = __dadd_rn(acc, __dmul_rn((double)xr[q], rr[q]));
-    if (acc > 0.0) {
-      int h = c / L, t = c - h * L;
-      atomicOr((unsigned long long *)&codes[((int64_t)h * n + row) * W + (t >> 6)],
-               1ull << (t & 63));
-    }
+    const unsigned long long it = items[i];
+    const int64_t row = (int64_t)(it >> 32);
+    const int c = (int)(it & 0xffffffffu);
+    if (exact_sign<TX>(x + row * dim, r + (int64_t)c * dim, dim))
+      set_code_bit(codes, n, L, W, row, c, true);
+  }
+}
+
+// Band list overflowed (adversarial data): recompute every sign exactly.
+// Exits immediately in the normal case.
+template <typename TX>
+__global__ void k_fixup_overflow(const TX *__restrict__ x, int64_t n, int dim,
+                                 const double *__restrict__ r, int L, int W,
+                                 uint64_t *__restrict__ codes,
+                                 const unsigned long long *__restrict__ count,
+                                 unsigned long long cap, int cols) {
+  if (*count <= cap) return;
+  const unsigned long long total = (unsigned long long)n * cols;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const int64_t row = (int64_t)(i / cols);
+    const int c = (int)(i % cols);
+    set_code_bit(codes, n, L, W, row, c, exact_sign<TX>(x + row * dim, r + (int64_t)c * dim, dim));
   }
 }
 

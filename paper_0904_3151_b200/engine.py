@@ -63,23 +63,35 @@ def as_device_rows(data, dev):
     return t
 
 
-def row_stats(x: torch.Tensor):
-    """fp64 row norms plus the first non-finite / zero-norm row (or -1)."""
+def row_stats_async(x: torch.Tensor):
+    """fp64 row norms + device flags (first non-finite row, first zero-norm
+    row; 2^64-1 when none), without synchronising."""
     n, dim = x.shape
     norms = torch.empty(n, dtype=torch.float64, device=x.device)
-    bad = (ctypes_i64 * 2)()
+    bad = torch.empty(2, dtype=torch.int64, device=x.device)
     check(_native.lib().eg_row_stats(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms),
-                                     ctypes_addr(bad), _stream(x.device)), "row_stats")
-    return norms, int(bad[0]), int(bad[1])
+                                     _p(bad), _stream(x.device)), "row_stats")
+    return norms, bad
+
+
+def raise_bad_rows(bad):
+    """Reference error shapes: lsh.py:55-56, then lsh.py:121-125."""
+    nonfinite, zero = (int(v) for v in bad.cpu().tolist())
+    if nonfinite != -1:
+        raise DataError(f"row {nonfinite} has a non-finite entry")
+    if zero != -1:
+        raise DataError(f"row {zero} has zero norm and cannot be projected")
+
+
+def row_stats(x: torch.Tensor):
+    norms, bad = row_stats_async(x)
+    nonfinite, zero = (int(v) for v in bad.cpu().tolist())
+    return norms, nonfinite, zero
 
 
 def validate_rows(x: torch.Tensor):
-    """Reference error shapes: lsh.py:55-56 then lsh.py:121-125."""
-    norms, nonfinite, zero = row_stats(x)
-    if nonfinite >= 0:
-        raise DataError(f"row {nonfinite} has a non-finite entry")
-    if zero >= 0:
-        raise DataError(f"row {zero} has zero norm and cannot be projected")
+    norms, bad = row_stats_async(x)
+    raise_bad_rows(bad)
     return norms
 
 
@@ -93,8 +105,9 @@ def directions(length: int, dim: int, seed: int, replicate_id: int) -> np.ndarra
 
 
 def project_codes(x: torch.Tensor, norms: torch.Tensor, length: int, seed: int,
-                  replicate_ids) -> tuple[torch.Tensor, int]:
-    """Packed codes ``(r, n, W)`` uint64 for the given replicate ids."""
+                  replicate_ids) -> tuple[torch.Tensor, torch.Tensor]:
+    """Packed codes ``(r, n, W)`` uint64 for the given replicate ids, plus a
+    device counter of band entries recomputed exactly (no host sync)."""
     dev = x.device
     n, dim = x.shape
     reps = len(replicate_ids)
@@ -106,11 +119,11 @@ def project_codes(x: torch.Tensor, norms: torch.Tensor, length: int, seed: int,
     codes = torch.empty((reps, n, W), dtype=torch.int64, device=dev)
     lib = _native.lib()
     ws = _ws(lib.eg_project_workspace(n, dim, length, reps), dev)
-    fix = ctypes_i64(0)
+    fix = torch.zeros(1, dtype=torch.int64, device=dev)
     check(lib.eg_project(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms), _p(r_d),
                          _p(rn_d), length, reps, _p(codes), _p(ws), ws.numel(),
-                         ctypes_addr(fix), _stream(dev)), "project")
-    return codes, int(fix.value)
+                         _p(fix), _stream(dev)), "project")
+    return codes, fix
 
 
 def masks_for(k: int, d: int):

@@ -114,9 +114,10 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
     mid = _metric_id(metric)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record()
+    bad = None
     if norms is None:
-        norms = engine.validate_rows(x)
-    fix = 0
+        norms, bad = engine.row_stats_async(x)     # checked once msm_pairs syncs
+    fix = None
     if codes is None:
         codes, fix = engine.project_codes(x, norms, params.length, params.seed,
                                           list(range(1, params.replicates + 1)))
@@ -127,6 +128,8 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
     else:
         ureps, umasks = units
     keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, ureps, umasks)
+    if bad is not None:
+        engine.raise_bad_rows(bad)
     ev[2].record()
     engine.sort_pair_keys(keys, n)
     ev[3].record()

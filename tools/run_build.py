@@ -38,3 +38,26 @@ for i in range(args.reps):
         res = distributed.build_step(x, params, cfg.metric, 1, 0)
     torch.cuda.synchronize()
     print(i, f"{(time.perf_counter() - t0) * 1e3:.1f} ms", distributed.last_counts(res), flush=True)
+
+if os.environ.get("EG_PROFILE"):
+    from paper_0904_3151_b200 import _native, engine
+    prof = _native.Profile()
+    for i in range(2):
+        prof.start()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if cfg.metric == "hamming":
+            res = distributed.hamming_step(x, params, 1, 0)
+        else:
+            res = distributed.build_step(x, params, cfg.metric, 1, 0)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        p = prof.stop()
+        print("profiled", f"{wall:.1f} ms", {k: round(v["ms"], 3) for k, v in p.items()}, flush=True)
+    if cfg.metric != "hamming":
+        for i in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            engine.validate_rows(x)
+            torch.cuda.synchronize()
+            print("row_stats", f"{(time.perf_counter() - t0) * 1e3:.2f} ms")
