@@ -109,18 +109,30 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
 /* blocks where they differ (== the reference's first-witness mask rule), */
 /* and popcount > d in every replicate g < h.                             */
 /* d_out_keys[capacity]: emitted pair keys, in no particular order.       */
+/* d_out_rep (optional, replicates > 1): when given, the cross-replicate  */
+/* rule is NOT applied here; every raw pair is emitted with its replicate */
+/* index in d_out_rep[slot] and eg_xrep_filter applies the rule later.    */
 /* h_counts (2*replicates + 2 int64): [0] total emitted (may exceed       */
 /* capacity -> EG_ERR_CAPACITY), [1] largest equal-key group seen,        */
 /* [2+h] raw pairs of replicate h (before the cross-replicate rule),      */
-/* [2+replicates+h] new pairs of replicate h.                             */
+/* [2+replicates+h] new pairs of replicate h (0 when deferred).           */
 /* --------------------------------------------------------------------- */
 size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates);
 int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
                  int32_t replicates, const int32_t *h_block_bounds, int32_t k,
                  int32_t d, const int32_t *h_unit_rep, const uint64_t *h_unit_mask,
-                 int64_t n_units, uint64_t *d_out_keys, int64_t capacity,
-                 int64_t *h_counts, void *d_workspace, size_t workspace_bytes,
-                 void *stream);
+                 int64_t n_units, uint64_t *d_out_keys, uint8_t *d_out_rep,
+                 int64_t capacity, int64_t *h_counts, void *d_workspace,
+                 size_t workspace_bytes, void *stream);
+
+/* Deferred cross-replicate first-witness rule (pipeline.py:286-314) over  */
+/* pairs emitted by eg_msm_pairs with d_out_rep: d_keep[p] = 1 iff the     */
+/* pair's Hamming distance exceeds d in every replicate before its own.   */
+/* h_new_counts[replicates] receives the survivors per replicate.         */
+int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+                   const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
+                   int32_t replicates, uint8_t *d_keep, int64_t *h_new_counts,
+                   void *stream);
 
 /* --------------------------------------------------------------------- */
 /* Grouped sort of one mask.  Replaces grouped_radix_sort                 */

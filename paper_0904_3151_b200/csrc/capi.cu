@@ -3,6 +3,7 @@
 // kernels.  Single translation unit: nvcc -gencode arch=compute_100a,
 // code=sm_100a -O3 -lineinfo -shared.
 #include <stdarg.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -133,8 +134,14 @@ static void dispatch_project(int tn, const TX *x, int64_t n, int dim, const floa
 }
 
 // ------------------------------------------------------------------ MSM
+static int env_int(const char *name, int dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
 static int msm_lgb(int64_t n) {
-  int64_t target = (n + MSM_TARGET - 1) / MSM_TARGET;
+  const int64_t tgt = env_int("EG_MSM_TARGET", MSM_TARGET);
+  int64_t target = (n + tgt - 1) / tgt;
   int l = ilog2_ceil((uint64_t)(target < 1 ? 1 : target));
   return l > MSM_MAX_LGB ? MSM_MAX_LGB : l;
 }
@@ -144,7 +151,8 @@ static int msm_batch_units(int64_t n) {
   int64_t per = n * 12;
   int64_t u = per > 0 ? (int64_t)(2ll << 30) / per : MSM_MAXU;
   if (u < 1) u = 1;
-  return (int)(u > MSM_MAXU ? MSM_MAXU : u);
+  const int cap = std::max(1, std::min(MSM_MAXU, env_int("EG_MSM_UNITS", MSM_MAXU)));
+  return (int)(u > cap ? cap : u);
 }
 
 struct MsmLayout {
@@ -174,7 +182,7 @@ template <int W>
 static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch> &batches,
                    cudaStream_t st) {
   const size_t smem_hist = (size_t)lay.B * 4, smem_scatter = (size_t)lay.B * 8;
-  const size_t smem_group = sizeof(HGroupSmem<W, MSM_SCAP, MSM_SNT>);
+  const size_t smem_group = sizeof(HGroupSmem<W, SmallCfg<W>::CAP, SmallCfg<W>::NT>);
   const size_t smem_medium =
       sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>);
   a.gcnt_min = MediumCfg<W>::CAP;
@@ -219,7 +227,7 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
     dim3 g4(lay.B, ub.count);
     {
       EG_PROF(PC_MSM_GROUP, st);
-      k_msm_group<W><<<g4, MSM_SNT, smem_group, st>>>(a, ub);
+      k_msm_group<W><<<g4, SmallCfg<W>::NT, smem_group, st>>>(a, ub);
     }
     {
       EG_PROF(PC_MSM_SPILL, st);
@@ -375,8 +383,8 @@ size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates) {
 int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t replicates,
                  const int32_t *h_block_bounds, int32_t k, int32_t d, const int32_t *h_unit_rep,
                  const uint64_t *h_unit_mask, int64_t n_units, uint64_t *d_out_keys,
-                 int64_t capacity, int64_t *h_counts, void *d_workspace, size_t workspace_bytes,
-                 void *stream) {
+                 uint8_t *d_out_rep, int64_t capacity, int64_t *h_counts, void *d_workspace,
+                 size_t workspace_bytes, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 1 || n >= (1ll << 32)) return arg_error("eg_msm_pairs: need 1 <= n < 2^32");
   if (length < 1 || length > EG_MAX_LENGTH)
@@ -420,6 +428,7 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   a.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 3);
   a.spill_cap = (int64_t)lay.U * (lay.B + 1);
   a.out_keys = (unsigned long long *)d_out_keys;
+  a.out_rep = replicates > 1 ? d_out_rep : nullptr;
   a.out_cap = capacity > 0 ? (unsigned long long)capacity : 0ull;
   if (!a.counts || !a.starts || !a.cursor || !a.elems || !a.gcnt || !b2b_d || !a.ctr || !a.spill) {
     set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
@@ -469,6 +478,29 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
     set_error("eg_msm_pairs: %llu pairs exceed capacity %llu", hc[0], a.out_cap);
     return EG_ERR_CAPACITY;
   }
+  return EG_OK;
+}
+
+int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+                   const uint64_t *d_codes, int64_t n, int32_t W, int32_t d, int32_t replicates,
+                   uint8_t *d_keep, int64_t *h_new_counts, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (replicates < 1 || replicates > 255) return arg_error("eg_xrep_filter: replicates outside [1, 255]");
+  unsigned long long *nc;
+  EG_CUDA_TRY(cudaMallocAsync(&nc, 8 * (size_t)replicates, st));
+  EG_CUDA_TRY(cudaMemsetAsync(nc, 0, 8 * (size_t)replicates, st));
+  if (m > 0) {
+    unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
+    EG_PROF(PC_MISC, st);
+    k_xrep_filter<<<grid, 256, 0, st>>>(d_keys, d_reps, m, d_codes, n, W, d, replicates, d_keep,
+                                        nc);
+    EG_LAUNCH_CHECK();
+  }
+  std::vector<unsigned long long> h(replicates);
+  EG_CUDA_TRY(cudaMemcpyAsync(h.data(), nc, 8 * (size_t)replicates, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaFreeAsync(nc, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < replicates; ++i) h_new_counts[i] = (int64_t)h[i];
   return EG_OK;
 }
 

@@ -32,9 +32,9 @@ namespace eg {
 
 constexpr int MSM_MAXU = 16;            // units per launch batch
 constexpr int MSM_IPT = 8;              // items per thread, hist/scatter
-constexpr int MSM_NT = 512;             // threads, hist/scatter
+constexpr int MSM_NT = 1024;            // threads, hist/scatter
 constexpr int MSM_TILE = MSM_IPT * MSM_NT;
-constexpr int MSM_TARGET = 384;         // target mean bucket size
+constexpr int MSM_TARGET = 768;         // default target mean bucket size
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 13;         // at most 8192 buckets per unit
 
@@ -63,6 +63,10 @@ struct MsmArgs {
   uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
   int64_t spill_cap;
   int gcnt_min;                  // spilled buckets above this size count groups
+  uint8_t *out_rep;              // non-null: emit raw pairs tagged with their
+                                 // replicate; the cross-replicate rule runs
+                                 // later in k_xrep_filter (off the group
+                                 // kernels' critical path)
 };
 
 template <int W>
@@ -229,6 +233,7 @@ __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint6
   }
   if (keydiff || pc > a.d) return 0;
   if (canonical_mask<W>(x, b2b, a.k, a.d) != maskbits) return 0;
+  if (a.out_rep) return 2;
   for (int g = 0; g < rep; ++g) {
     const uint64_t *cg = a.codes + (int64_t)g * a.n * W;
     int pg = 0;
@@ -407,8 +412,10 @@ __device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const 
     my_new += v == 2;
     const bool emit = v == 2;
     const unsigned long long slot = warp_append(emit, &a.ctr[0]);
-    if (emit && slot < a.out_cap)
+    if (emit && slot < a.out_cap) {
       a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+      if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+    }
   }
   if (my_raw) atomicAdd(&S.raw, my_raw);
   if (my_new) atomicAdd(&S.neu, my_new);
@@ -421,21 +428,25 @@ __device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const 
   __syncthreads();
 }
 
-constexpr int MSM_SCAP = 1024;   // small buckets: one CTA each, many CTAs per SM
-constexpr int MSM_SNT = 128;
+template <int W>
+struct SmallCfg {               // one CTA per bucket, several CTAs per SM
+  static constexpr int CAP = W <= 2 ? 2048 : 1024;
+  static constexpr int NT = 256;
+};
 template <int W>
 struct MediumCfg {
   static constexpr int CAP = W <= 2 ? 4096 : 2048;
   static constexpr int NT = 512;
 };
 
-// Small buckets (s <= MSM_SCAP): grid (B, units).  Larger buckets are queued
+// Small buckets (s <= SmallCfg::CAP): grid (B, units).  Larger buckets are queued
 // on the spill list for k_msm_medium / k_msm_spill.
 template <int W>
-__global__ void __launch_bounds__(MSM_SNT) k_msm_group(const __grid_constant__ MsmArgs a,
+__global__ void __launch_bounds__(SmallCfg<W>::NT) k_msm_group(const __grid_constant__ MsmArgs a,
                                                        const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  using Smem = HGroupSmem<W, MSM_SCAP, MSM_SNT>;
+  constexpr int CAP = SmallCfg<W>::CAP, NT = SmallCfg<W>::NT;
+  using Smem = HGroupSmem<W, CAP, NT>;
   Smem &S = *reinterpret_cast<Smem *>(smraw);
   const int u = blockIdx.y;
   const int b = blockIdx.x;
@@ -443,7 +454,7 @@ __global__ void __launch_bounds__(MSM_SNT) k_msm_group(const __grid_constant__ M
   const uint32_t *st = a.starts + (int64_t)u * (B + 1);
   const uint32_t s0 = st[b], s = st[b + 1] - s0;
   if (s < 2) return;
-  if (s > MSM_SCAP) {
+  if (s > CAP) {
     if (threadIdx.x == 0) {
       const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
       if ((int64_t)slot < a.spill_cap) {
@@ -454,15 +465,15 @@ __global__ void __launch_bounds__(MSM_SNT) k_msm_group(const __grid_constant__ M
     }
     if (s > (uint32_t)MediumCfg<W>::CAP && (int64_t)s * 4 > a.n) {
       uint32_t *g = a.gcnt + (int64_t)u * a.n + s0;   // group counts for the warning
-      for (uint32_t i = threadIdx.x; i < s; i += MSM_SNT) g[i] = 0;
+      for (uint32_t i = threadIdx.x; i < s; i += NT) g[i] = 0;
     }
     return;
   }
-  for (int i = threadIdx.x; i < a.L; i += MSM_SNT) S.b2b[i] = a.bit2blk[i];
-  process_bucket<W, MSM_SCAP, MSM_SNT>(S, a, ub, u, s0, s);
+  for (int i = threadIdx.x; i < a.L; i += NT) S.b2b[i] = a.bit2blk[i];
+  process_bucket<W, CAP, NT>(S, a, ub, u, s0, s);
 }
 
-// Medium buckets (MSM_SCAP < s <= MediumCfg::CAP) from the spill list,
+// Medium buckets (SmallCfg::CAP < s <= MediumCfg::CAP) from the spill list,
 // persistent CTAs.
 template <int W>
 __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
@@ -474,7 +485,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
   for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
     const uint32_t s = a.spill[sb * 3 + 2];
-    if (s > (uint32_t)MediumCfg<W>::CAP) continue;
+    if (s <= (uint32_t)SmallCfg<W>::CAP || s > (uint32_t)MediumCfg<W>::CAP) continue;
     process_bucket<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>(S, a, ub, (int)a.spill[sb * 3],
                                                            a.spill[sb * 3 + 1], s);
   }
@@ -560,8 +571,10 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
               emit = v == 2;
               if (emit) {
                 unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
-                if (slot < a.out_cap)
+                if (slot < a.out_cap) {
                   a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+                  if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+                }
               }
             }
           }
@@ -593,6 +606,37 @@ __global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) atomicMax(&a.ctr[1], (unsigned long long)mx + 1);
   }
+}
+
+// ------------------------------------------- cross-replicate first witness
+// Deferred form of the fold in pipeline.py:286-314: a raw pair of replicate
+// h survives iff its Hamming distance exceeds d in every replicate g < h.
+// Counts survivors per replicate (per_replicate_new).
+__global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ reps,
+                              int64_t m, const uint64_t *__restrict__ codes, int64_t n, int W,
+                              int d, int nreps, uint8_t *__restrict__ keep,
+                              unsigned long long *__restrict__ new_counts) {
+  __shared__ unsigned int cnt[256];
+  for (int i = threadIdx.x; i < nreps && i < 256; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[p];
+    const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+    const int h = reps[p];
+    bool ok = true;
+    for (int g = 0; g < h && ok; ++g) {
+      const uint64_t *cg = codes + (int64_t)g * n * W;
+      int pc = 0;
+      for (int w = 0; w < W; ++w) pc += __popcll(__ldg(cg + i * W + w) ^ __ldg(cg + j * W + w));
+      ok = pc > d;
+    }
+    keep[p] = ok;
+    if (ok) atomicAdd(&cnt[h], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nreps && i < 256; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&new_counts[i], (unsigned long long)cnt[i]);
 }
 
 // ------------------------------------------------------ first witness

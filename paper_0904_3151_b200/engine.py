@@ -163,26 +163,39 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
         capacity = _capacity_hint.get(hint_key, max(1 << 16, 2 * n))
     ws = _ws(lib.eg_msm_workspace(n, length, reps), dev)
     counts = (ctypes_i64 * (2 * reps + 2))()
+    defer = reps > 1       # cross-replicate rule in a separate streaming pass
     while True:
         out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
+        rtag = torch.empty(max(capacity, 1), dtype=torch.uint8, device=dev) if defer else None
         rc = lib.eg_msm_pairs(_p(codes), n, length, reps, bb.ctypes.data, k, d, ur.ctypes.data,
-                              um.ctypes.data, len(ur), _p(out), capacity, ctypes_addr(counts),
-                              _p(ws), ws.numel(), _stream(dev))
+                              um.ctypes.data, len(ur), _p(out), _p(rtag), capacity,
+                              ctypes_addr(counts), _p(ws), ws.numel(), _stream(dev))
         if rc == _native.EG_ERR_CAPACITY:
             capacity = int(counts[0])
-            del out
+            del out, rtag
             continue
         check(rc, "msm_pairs")
         break
     total = int(counts[0])
     _capacity_hint[hint_key] = max(1 << 16, int(total * 1.25) + 1024)
+    raw = tuple(int(counts[2 + h]) for h in range(reps))
+    keys = out[:total]
+    if defer:
+        keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+        newc = (ctypes_i64 * reps)()
+        check(lib.eg_xrep_filter(_p(keys), _p(rtag), total, _p(codes), n, W, d, reps, _p(keep),
+                                 ctypes_addr(newc), _stream(dev)), "xrep_filter")
+        keys = compact_keys(keys, keep[:total])
+        new = tuple(int(newc[h]) for h in range(reps))
+    else:
+        new = tuple(int(counts[2 + reps + h]) for h in range(reps))
     info = {
-        "emitted": total,
+        "emitted": int(keys.numel()),
         "max_group": int(counts[1]),
-        "raw": tuple(int(counts[2 + h]) for h in range(reps)),
-        "new": tuple(int(counts[2 + reps + h]) for h in range(reps)),
+        "raw": raw,
+        "new": new,
     }
-    return out[:total], info
+    return keys, info
 
 
 def sort_pair_keys(keys: torch.Tensor, n: int) -> torch.Tensor:
