@@ -173,7 +173,7 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   b += ws_bytes((size_t)l.U * n, 4);              // gcnt
   b += ws_bytes(EG_MAX_LENGTH, 1);                // bit2blk
   b += ws_bytes(3 + 2 * (size_t)reps, 8);         // counters
-  b += ws_bytes((size_t)l.U * (l.B + 1) * 3, 4);  // spill list
+  b += ws_bytes((size_t)l.U * (l.B + 1) * 9, 4);  // spill list (<= 3 entries/bucket)
   l.bytes = b + 4096;
   return l;
 }
@@ -425,8 +425,8 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   uint8_t *b2b_d = ar.take<uint8_t>(EG_MAX_LENGTH);
   a.bit2blk = b2b_d;
   a.ctr = ar.take<unsigned long long>(3 + 2 * (size_t)replicates);
-  a.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 3);
-  a.spill_cap = (int64_t)lay.U * (lay.B + 1);
+  a.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 9);
+  a.spill_cap = (int64_t)lay.U * (lay.B + 1) * 3;   // a bucket is queued at most 3 times
   a.out_keys = (unsigned long long *)d_out_keys;
   a.out_rep = replicates > 1 ? d_out_rep : nullptr;
   a.out_cap = capacity > 0 ? (unsigned long long)capacity : 0ull;

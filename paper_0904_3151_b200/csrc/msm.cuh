@@ -270,37 +270,47 @@ template <int W, int CAP, int NT>
 struct HGroupSmem {
   uint32_t key[2 * CAP];     // h2 per slot (EMPTY = ~0), then member offsets
   uint32_t cnt[2 * CAP];     // rows per slot
-  uint32_t members[CAP];     // rows of multi-row groups, grouped
-  uint64_t codes[CAP * W];   // their codes
-  uint32_t runs[CAP / 2];    // (start << 16) | len
-  uint32_t pp[CAP / 2 + 1];  // pair prefix per run
+  uint32_t mslot[CAP / 2];   // slots holding >= 2 rows (one entry per group)
+  uint32_t members[CAP / 2]; // rows of multi-row groups, grouped
+  uint64_t codes[CAP / 2 * W];
+  uint32_t runs[CAP / 2];    // (start << 16) | len, one per group
+  uint32_t pp[CAP / 2 + 1];  // pair prefix per group
   uint8_t b2b[EG_MAX_LENGTH];
-  uint32_t sw[NT / 32];
+  unsigned long long sw[NT / 32];
   uint32_t nruns, maxrun, raw, neu;
 };
 
 constexpr uint32_t HG_EMPTY = 0xffffffffu;
 
+__device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
+  return v <= 1 ? 1u : 1u << (32 - __clz(v - 1));
+}
+
+// Returns false (without touching the bucket) if its multi-row groups hold
+// more rows than the member capacity (CAP/2); the caller then re-queues it.
 template <int W, int CAP, int NT>
-__device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const MsmArgs &a,
+__device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const MsmArgs &a,
                                                const UnitBatch &ub, int u, uint32_t s0,
                                                uint32_t s) {
   constexpr int PT = CAP / NT;
+  constexpr uint32_t MCAP = CAP / 2;
   const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
   const int rep = ub.rep[u];
-  const uint32_t T = 1u << max(1, ilog2_ceil(2ull * s));
-  for (uint32_t i = threadIdx.x; i < T; i += NT) {
-    S.key[i] = HG_EMPTY;
-    S.cnt[i] = 0;
-  }
-  if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; }
+  const uint32_t T = pow2_at_least(2 * s);
+  // 1. load the bucket (coalesced) while the table is cleared
   uint64_t e[PT];
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const uint32_t i = threadIdx.x + j * NT;
     e[j] = i < s ? el[i] : 0ull;
   }
+  for (uint32_t i = threadIdx.x * 4; i < T; i += NT * 4) {
+    *reinterpret_cast<uint4 *>(&S.key[i]) = make_uint4(HG_EMPTY, HG_EMPTY, HG_EMPTY, HG_EMPTY);
+    *reinterpret_cast<uint4 *>(&S.cnt[i]) = make_uint4(0, 0, 0, 0);
+  }
+  if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; }
   __syncthreads();
+  // 2. insert: open addressing on h2; the second row of a slot registers it
   uint32_t sl[PT], rk[PT];
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
@@ -310,38 +320,19 @@ __device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const 
       if (h2 == HG_EMPTY) h2 = HG_EMPTY - 1;
       uint32_t slot = h2 & (T - 1);
       while (true) {
-        const uint32_t old = atomicCAS(&S.key[slot], HG_EMPTY, h2);
-        if (old == HG_EMPTY || old == h2) break;
+        uint32_t cur = S.key[slot];
+        if (cur == HG_EMPTY) {
+          cur = atomicCAS(&S.key[slot], HG_EMPTY, h2);
+          if (cur == HG_EMPTY) cur = h2;
+        }
+        if (cur == h2) break;
         slot = (slot + 1) & (T - 1);
       }
       sl[j] = slot;
       rk[j] = atomicAdd(&S.cnt[slot], 1u);
-    }
-  }
-  __syncthreads();
-  {  // member offsets of multi-row slots (blocked scan), run list
-    const uint32_t per = (T + NT - 1) / NT;
-    uint32_t loc = 0;
-    for (uint32_t q = 0; q < per; ++q) {
-      const uint32_t t = threadIdx.x * per + q;
-      if (t < T) {
-        const uint32_t c = S.cnt[t];
-        loc += c >= 2 ? c : 0;
-      }
-    }
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan<NT>(loc, tot, S.sw);
-    for (uint32_t q = 0; q < per; ++q) {
-      const uint32_t t = threadIdx.x * per + q;
-      if (t < T) {
-        const uint32_t c = S.cnt[t];
-        if (c >= 2) {
-          S.key[t] = run;
-          const uint32_t r = atomicAdd(&S.nruns, 1u);
-          S.runs[r] = (run << 16) | c;
-          atomicMax(&S.maxrun, c);
-          run += c;
-        }
+      if (rk[j] == 1) {
+        const uint32_t r = atomicAdd(&S.nruns, 1u);
+        if (r < MCAP) S.mslot[r] = slot;
       }
     }
   }
@@ -349,44 +340,66 @@ __device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const 
   const uint32_t R = S.nruns;
   if (R == 0) {
     __syncthreads();
-    return;
+    return true;
   }
+  // 3. start the code gathers for rows of multi-row groups (latency overlaps
+  //    the offset scan below)
   const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
+  uint64_t cg[PT][W];
+  bool mine[PT];
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const uint32_t i = threadIdx.x + j * NT;
-    if (i < s && S.cnt[sl[j]] >= 2) {
-      const uint32_t pos = S.key[sl[j]] + rk[j];
+    mine[j] = i < s && S.cnt[sl[j]] >= 2;
+    if (mine[j]) {
       const uint32_t row = (uint32_t)e[j];
-      S.members[pos] = row;
 #pragma unroll
-      for (int w = 0; w < W; ++w) S.codes[pos * W + w] = __ldg(codes + (int64_t)row * W + w);
+      for (int w = 0; w < W; ++w) cg[j][w] = __ldg(codes + (int64_t)row * W + w);
     }
   }
-  {  // pair prefix over runs
-    const uint32_t per = (R + NT - 1) / NT;
-    uint32_t loc = 0;
-    for (uint32_t q = 0; q < per; ++q) {
-      const uint32_t r = threadIdx.x * per + q;
-      if (r < R) {
-        const uint32_t len = S.runs[r] & 0xffffu;
-        loc += len * (len - 1) / 2;
-      }
+  // 4. one scan over the groups gives member offsets and pair prefix
+  uint32_t c_my[(MCAP + NT - 1) / NT];
+  unsigned long long loc = 0;
+  constexpr int RP = (MCAP + NT - 1) / NT;
+  const bool fits = R <= MCAP;
+#pragma unroll
+  for (int q = 0; q < RP; ++q) {
+    const uint32_t r = threadIdx.x * RP + q;
+    c_my[q] = (fits && r < R) ? S.cnt[S.mslot[r]] : 0u;
+    loc += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
+  }
+  unsigned long long tot;
+  unsigned long long run = block_exclusive_scan64<NT>(loc, tot, S.sw);
+  const uint32_t members = (uint32_t)(tot >> 32);
+  if (!fits || members > MCAP) {     // uniform: too many grouped rows
+    __syncthreads();
+    return false;
+  }
+#pragma unroll
+  for (int q = 0; q < RP; ++q) {
+    const uint32_t r = threadIdx.x * RP + q;
+    if (r < R) {
+      const uint32_t off = (uint32_t)(run >> 32);
+      S.key[S.mslot[r]] = off;
+      S.runs[r] = (off << 16) | c_my[q];
+      S.pp[r] = (uint32_t)run;
+      atomicMax(&S.maxrun, c_my[q]);
+      run += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
     }
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan<NT>(loc, tot, S.sw);
-    for (uint32_t q = 0; q < per; ++q) {
-      const uint32_t r = threadIdx.x * per + q;
-      if (r < R) {
-        S.pp[r] = run;
-        const uint32_t len = S.runs[r] & 0xffffu;
-        run += len * (len - 1) / 2;
-      }
+  }
+  if (threadIdx.x == 0) S.pp[R] = (uint32_t)tot;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    if (mine[j]) {
+      const uint32_t pos = S.key[sl[j]] + rk[j];
+      S.members[pos] = (uint32_t)e[j];
+#pragma unroll
+      for (int w = 0; w < W; ++w) S.codes[pos * W + w] = cg[j][w];
     }
-    if (threadIdx.x == 0) S.pp[R] = tot;
-    // S.b2b was filled by the caller before the first bucket
   }
   __syncthreads();
+  // 5. every in-group pair once (load-balanced over the CTA)
   const uint32_t P = S.pp[R];
   const unsigned long long *kept = ub.kept[u];
   const uint64_t maskbits = ub.maskbits[u];
@@ -426,6 +439,15 @@ __device__ __forceinline__ void process_bucket(HGroupSmem<W, CAP, NT> &S, const 
     atomicMax(&a.ctr[1], (unsigned long long)S.maxrun);
   }
   __syncthreads();
+  return true;
+}
+
+// Spill-list routing.  Tag bit 31: re-queued by the small tier (member room
+// exhausted) -> medium tier.  Tag bit 30: re-queued by the medium tier ->
+// tile kernel.  Untagged: routed by size.
+constexpr uint32_t SPILL_FROM_SMALL = 0x80000000u, SPILL_FROM_MEDIUM = 0x40000000u;
+__device__ __forceinline__ bool spill_for_tiles(uint32_t tag, uint32_t s, uint32_t med_cap) {
+  return (tag & SPILL_FROM_MEDIUM) || (!(tag & SPILL_FROM_SMALL) && s > med_cap);
 }
 
 template <int W>
@@ -470,7 +492,16 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT) k_msm_group(const __grid_cons
     return;
   }
   for (int i = threadIdx.x; i < a.L; i += NT) S.b2b[i] = a.bit2blk[i];
-  process_bucket<W, CAP, NT>(S, a, ub, u, s0, s);
+  if (!process_bucket<W, CAP, NT>(S, a, ub, u, s0, s) && threadIdx.x == 0) {
+    // grouped rows exceed the member capacity: hand the bucket to the
+    // medium tier (it accepts any size up to its own capacity)
+    const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+    if ((int64_t)slot < a.spill_cap) {
+      a.spill[slot * 3 + 0] = (uint32_t)u | SPILL_FROM_SMALL;
+      a.spill[slot * 3 + 1] = s0;
+      a.spill[slot * 3 + 2] = s;
+    }
+  }
 }
 
 // Medium buckets (SmallCfg::CAP < s <= MediumCfg::CAP) from the spill list,
@@ -485,9 +516,29 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
   for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
     const uint32_t s = a.spill[sb * 3 + 2];
-    if (s <= (uint32_t)SmallCfg<W>::CAP || s > (uint32_t)MediumCfg<W>::CAP) continue;
-    process_bucket<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>(S, a, ub, (int)a.spill[sb * 3],
-                                                           a.spill[sb * 3 + 1], s);
+    const uint32_t tag = a.spill[sb * 3];
+    const bool requeued = tag & SPILL_FROM_SMALL;     // small tier ran out of member room
+    if ((tag & SPILL_FROM_MEDIUM) || (!requeued && s <= (uint32_t)SmallCfg<W>::CAP) ||
+        s > (uint32_t)MediumCfg<W>::CAP)
+      continue;
+    const int u = (int)(tag & 0x3fffffffu);
+    const uint32_t s0 = a.spill[sb * 3 + 1];
+    if (!process_bucket<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>(S, a, ub, u, s0, s)) {
+      // still too many grouped rows: the tile kernel takes it
+      if ((int64_t)s * 4 > a.n) {
+        uint32_t *g = a.gcnt + (int64_t)u * a.n + s0;
+        for (uint32_t i = threadIdx.x; i < s; i += MediumCfg<W>::NT) g[i] = 0;
+      }
+      if (threadIdx.x == 0) {
+        const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+        if ((int64_t)slot < a.spill_cap) {
+          a.spill[slot * 3 + 0] = (uint32_t)u | SPILL_FROM_MEDIUM;
+          a.spill[slot * 3 + 1] = s0;
+          a.spill[slot * 3 + 2] = s;
+        }
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -505,9 +556,10 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
   for (int i = threadIdx.x; i < a.L; i += MSM_SPILL_T) b2b[i] = a.bit2blk[i];
   const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
   for (unsigned long long sb = 0; sb < nspill; ++sb) {
-    const int u = (int)a.spill[sb * 3 + 0];
+    const uint32_t tag = a.spill[sb * 3 + 0];
+    const int u = (int)(tag & 0x3fffffffu);
     const uint32_t s0 = a.spill[sb * 3 + 1], s = a.spill[sb * 3 + 2];
-    if (s <= (uint32_t)MediumCfg<W>::CAP) continue;
+    if (!spill_for_tiles(tag, s, MediumCfg<W>::CAP)) continue;
     const uint32_t nt = (s + MSM_SPILL_T - 1) / MSM_SPILL_T;
     const unsigned long long ntp = (unsigned long long)nt * (nt + 1) / 2;
     const int rep = ub.rep[u];
@@ -597,9 +649,10 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
 __global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
   const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
   for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
-    const int u = (int)a.spill[sb * 3 + 0];
+    const uint32_t tag = a.spill[sb * 3 + 0];
+    const int u = (int)(tag & 0x3fffffffu);
     const uint32_t s0 = a.spill[sb * 3 + 1], s = a.spill[sb * 3 + 2];
-    if ((int64_t)s * 4 <= a.n || s <= (uint32_t)a.gcnt_min) continue;
+    if ((int64_t)s * 4 <= a.n || !spill_for_tiles(tag, s, (uint32_t)a.gcnt_min)) continue;
     const uint32_t *gc = a.gcnt + (int64_t)u * a.n + s0;
     uint32_t mx = 0;
     for (uint32_t i = threadIdx.x; i < s; i += blockDim.x) mx = max(mx, gc[i]);
