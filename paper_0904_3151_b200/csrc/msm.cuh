@@ -268,32 +268,32 @@ __device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia,
 // hamming_join.py:116-122) and applies pair_verdict.
 template <int W, int CAP, int NT>
 struct HGroupSmem {
-  uint32_t key[2 * CAP];     // h2 per slot (EMPTY = ~0), then member offsets
-  uint32_t cnt[2 * CAP];     // rows per slot
-  uint32_t mslot[CAP / 2];   // slots holding >= 2 rows (one entry per group)
+  unsigned long long tab[2 * CAP];  // (h2 << 32 | rows) per slot; later (offset << 32 | rows)
+  uint32_t mslot[CAP / 4];   // slots holding >= 2 rows (one entry per group)
   uint32_t members[CAP / 2]; // rows of multi-row groups, grouped
   uint64_t codes[CAP / 2 * W];
-  uint32_t runs[CAP / 2];    // (start << 16) | len, one per group
-  uint32_t pp[CAP / 2 + 1];  // pair prefix per group
+  uint32_t runs[CAP / 4];    // (start << 16) | len, one per group
+  uint32_t pp[CAP / 4 + 1];  // pair prefix per group
   uint8_t b2b[EG_MAX_LENGTH];
   unsigned long long sw[NT / 32];
   uint32_t nruns, maxrun, raw, neu;
 };
 
-constexpr uint32_t HG_EMPTY = 0xffffffffu;
+constexpr unsigned long long HG_EMPTY = ~0ull;
 
 __device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
   return v <= 1 ? 1u : 1u << (32 - __clz(v - 1));
 }
 
-// Returns false (without touching the bucket) if its multi-row groups hold
-// more rows than the member capacity (CAP/2); the caller then re-queues it.
+// Returns false (without emitting anything) if the bucket's multi-row groups
+// hold more rows than the member capacity (CAP/2) or more groups than CAP/4;
+// the caller then re-queues it for the next tier.
 template <int W, int CAP, int NT>
 __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const MsmArgs &a,
                                                const UnitBatch &ub, int u, uint32_t s0,
                                                uint32_t s) {
   constexpr int PT = CAP / NT;
-  constexpr uint32_t MCAP = CAP / 2;
+  constexpr uint32_t MCAP = CAP / 2, GCAP = CAP / 4;
   const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
   const int rep = ub.rep[u];
   const uint32_t T = pow2_at_least(2 * s);
@@ -304,35 +304,34 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const 
     const uint32_t i = threadIdx.x + j * NT;
     e[j] = i < s ? el[i] : 0ull;
   }
-  for (uint32_t i = threadIdx.x * 4; i < T; i += NT * 4) {
-    *reinterpret_cast<uint4 *>(&S.key[i]) = make_uint4(HG_EMPTY, HG_EMPTY, HG_EMPTY, HG_EMPTY);
-    *reinterpret_cast<uint4 *>(&S.cnt[i]) = make_uint4(0, 0, 0, 0);
-  }
+  for (uint32_t i = threadIdx.x * 2; i < T; i += NT * 2)
+    *reinterpret_cast<ulonglong2 *>(&S.tab[i]) = make_ulonglong2(HG_EMPTY, HG_EMPTY);
   if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; }
   __syncthreads();
-  // 2. insert: open addressing on h2; the second row of a slot registers it
-  uint32_t sl[PT], rk[PT];
+  // 2. insert: one CAS claims an empty slot (singletons: one atomic); a
+  //    repeated h2 bumps the slot's count and the second row registers it
+  uint32_t slr[PT];   // (slot << 16) | rank within the group
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const uint32_t i = threadIdx.x + j * NT;
     if (i < s) {
       uint32_t h2 = (uint32_t)(e[j] >> 32);
-      if (h2 == HG_EMPTY) h2 = HG_EMPTY - 1;
-      uint32_t slot = h2 & (T - 1);
+      if (h2 == 0xffffffffu) h2 = 0xfffffffeu;
+      const unsigned long long mine = ((unsigned long long)h2 << 32) | 1ull;
+      uint32_t slot = h2 & (T - 1), rank = 0;
       while (true) {
-        uint32_t cur = S.key[slot];
-        if (cur == HG_EMPTY) {
-          cur = atomicCAS(&S.key[slot], HG_EMPTY, h2);
-          if (cur == HG_EMPTY) cur = h2;
+        const unsigned long long old = atomicCAS(&S.tab[slot], HG_EMPTY, mine);
+        if (old == HG_EMPTY) break;
+        if ((uint32_t)(old >> 32) == h2) {
+          rank = (uint32_t)atomicAdd(&S.tab[slot], 1ull);
+          break;
         }
-        if (cur == h2) break;
         slot = (slot + 1) & (T - 1);
       }
-      sl[j] = slot;
-      rk[j] = atomicAdd(&S.cnt[slot], 1u);
-      if (rk[j] == 1) {
+      slr[j] = (slot << 16) | rank;
+      if (rank == 1) {
         const uint32_t r = atomicAdd(&S.nruns, 1u);
-        if (r < MCAP) S.mslot[r] = slot;
+        if (r < GCAP) S.mslot[r] = slot;
       }
     }
   }
@@ -342,36 +341,38 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const 
     __syncthreads();
     return true;
   }
+  if (R > GCAP) {
+    __syncthreads();
+    return false;
+  }
   // 3. start the code gathers for rows of multi-row groups (latency overlaps
   //    the offset scan below)
   const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
   uint64_t cg[PT][W];
-  bool mine[PT];
+  uint32_t grouped = 0;   // bit j: element j sits in a multi-row group
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const uint32_t i = threadIdx.x + j * NT;
-    mine[j] = i < s && S.cnt[sl[j]] >= 2;
-    if (mine[j]) {
+    if (i < s && (uint32_t)S.tab[slr[j] >> 16] >= 2) {
+      grouped |= 1u << j;
       const uint32_t row = (uint32_t)e[j];
 #pragma unroll
       for (int w = 0; w < W; ++w) cg[j][w] = __ldg(codes + (int64_t)row * W + w);
     }
   }
-  // 4. one scan over the groups gives member offsets and pair prefix
-  uint32_t c_my[(MCAP + NT - 1) / NT];
+  // 4. one scan over the groups gives member offsets and the pair prefix
+  constexpr int RP = (GCAP + NT - 1) / NT;
+  uint32_t c_my[RP];
   unsigned long long loc = 0;
-  constexpr int RP = (MCAP + NT - 1) / NT;
-  const bool fits = R <= MCAP;
 #pragma unroll
   for (int q = 0; q < RP; ++q) {
     const uint32_t r = threadIdx.x * RP + q;
-    c_my[q] = (fits && r < R) ? S.cnt[S.mslot[r]] : 0u;
+    c_my[q] = r < R ? (uint32_t)S.tab[S.mslot[r]] : 0u;
     loc += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
   }
   unsigned long long tot;
   unsigned long long run = block_exclusive_scan64<NT>(loc, tot, S.sw);
-  const uint32_t members = (uint32_t)(tot >> 32);
-  if (!fits || members > MCAP) {     // uniform: too many grouped rows
+  if ((uint32_t)(tot >> 32) > MCAP) {     // uniform: too many grouped rows
     __syncthreads();
     return false;
   }
@@ -380,7 +381,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const 
     const uint32_t r = threadIdx.x * RP + q;
     if (r < R) {
       const uint32_t off = (uint32_t)(run >> 32);
-      S.key[S.mslot[r]] = off;
+      S.tab[S.mslot[r]] = ((unsigned long long)off << 32) | c_my[q];
       S.runs[r] = (off << 16) | c_my[q];
       S.pp[r] = (uint32_t)run;
       atomicMax(&S.maxrun, c_my[q]);
@@ -391,8 +392,8 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const 
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
-    if (mine[j]) {
-      const uint32_t pos = S.key[sl[j]] + rk[j];
+    if (grouped >> j & 1) {
+      const uint32_t pos = (uint32_t)(S.tab[slr[j] >> 16] >> 32) + (slr[j] & 0xffffu);
       S.members[pos] = (uint32_t)e[j];
 #pragma unroll
       for (int w = 0; w < W; ++w) S.codes[pos * W + w] = cg[j][w];
@@ -454,6 +455,7 @@ template <int W>
 struct SmallCfg {               // one CTA per bucket, several CTAs per SM
   static constexpr int CAP = W <= 2 ? 2048 : 1024;
   static constexpr int NT = 256;
+  static constexpr int MIN_CTAS = 4;
 };
 template <int W>
 struct MediumCfg {
@@ -464,7 +466,7 @@ struct MediumCfg {
 // Small buckets (s <= SmallCfg::CAP): grid (B, units).  Larger buckets are queued
 // on the spill list for k_msm_medium / k_msm_spill.
 template <int W>
-__global__ void __launch_bounds__(SmallCfg<W>::NT) k_msm_group(const __grid_constant__ MsmArgs a,
+__global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_group(const __grid_constant__ MsmArgs a,
                                                        const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int CAP = SmallCfg<W>::CAP, NT = SmallCfg<W>::NT;
