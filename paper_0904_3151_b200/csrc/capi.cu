@@ -181,7 +181,12 @@ static MsmLayout msm_layout(int64_t n, int reps) {
 template <int W>
 static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch> &batches,
                    cudaStream_t st) {
-  const size_t smem_hist = (size_t)lay.B * 4, smem_scatter = (size_t)lay.B * 8;
+  // histograms of several units side by side (<= 96 KB), staging for scatter
+  const size_t smem_hist =
+      std::min<size_t>((size_t)96 << 10, (size_t)lay.B * 4 * lay.U) / ((size_t)lay.B * 4) *
+      ((size_t)lay.B * 4);
+  a.hist_smem = (int)smem_hist;
+  const size_t smem_scatter = (size_t)MSM_TILE * 10 + (size_t)lay.B * 12;
   const size_t smem_group = sizeof(HGroupSmem<W, SmallCfg<W>::CAP, SmallCfg<W>::NT>);
   const size_t smem_medium =
       sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>);
@@ -214,7 +219,7 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
     dim3 g1(tiles, ub.count);
     {
       EG_PROF(PC_MSM_HIST, st);
-      k_msm_hist<W><<<g1, MSM_NT, smem_hist, st>>>(a, ub);
+      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(a, ub);
     }
     {
       EG_PROF(PC_MSM_SCAN, st);
@@ -222,7 +227,7 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
     }
     {
       EG_PROF(PC_MSM_SCATTER, st);
-      k_msm_scatter<W><<<g1, MSM_NT, smem_scatter, st>>>(a, ub);
+      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(a, ub);
     }
     dim3 g4(lay.B, ub.count);
     {

@@ -34,7 +34,8 @@ constexpr int MSM_MAXU = 16;            // units per launch batch
 constexpr int MSM_IPT = 8;              // items per thread, hist/scatter
 constexpr int MSM_NT = 1024;            // threads, hist/scatter
 constexpr int MSM_TILE = MSM_IPT * MSM_NT;
-constexpr int MSM_TARGET = 768;         // default target mean bucket size
+constexpr int MSM_SC_NT = 512;          // threads, scatter (16 items each)
+constexpr int MSM_TARGET = 3072;        // default target mean bucket size (tuned on cfg3)
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 13;         // at most 8192 buckets per unit
 
@@ -63,6 +64,7 @@ struct MsmArgs {
   uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
   int64_t spill_cap;
   int gcnt_min;                  // spilled buckets above this size count groups
+  int hist_smem;                  // dynamic shared memory of k_msm_hist (bytes)
   uint8_t *out_rep;              // non-null: emit raw pairs tagged with their
                                  // replicate; the cross-replicate rule runs
                                  // later in k_xrep_filter (off the group
@@ -81,34 +83,56 @@ __device__ __forceinline__ void load_code(const uint64_t *__restrict__ codes, in
 }
 
 // ------------------------------------------------------------------ 1
+// Bucket histogram for every unit of the batch: each CTA reads its code tile
+// once (registers) and hashes it under each unit's mask, so the codes cross
+// L2 once per batch instead of once per unit.  Shared-memory histograms
+// (units_per_pass x B counters), one global atomic per non-empty (CTA, unit,
+// bucket).
 template <int W>
 __global__ void __launch_bounds__(MSM_NT) k_msm_hist(const __grid_constant__ MsmArgs a,
-                                                         const __grid_constant__ UnitBatch ub) {
+                                                     const __grid_constant__ UnitBatch ub) {
   extern __shared__ uint32_t hist[];
-  const int u = blockIdx.y;
   const int B = 1 << a.lgB;
-  for (int i = threadIdx.x; i < B; i += MSM_NT) hist[i] = 0;
-  __syncthreads();
-  const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
-  const unsigned long long *kept = ub.kept[u];
-  const uint64_t salt = ub.salt[u];
+  const int upp = max(1, min(ub.count, (int)(a.hist_smem / (B * 4))));
   const int sh = 64 - a.lgB;
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
+  // all units of one batch share a replicate except at replicate boundaries
+  for (int u0 = 0; u0 < ub.count; u0 += upp) {
+    const int nu = min(upp, ub.count - u0);
+    for (int i = threadIdx.x; i < nu * B; i += MSM_NT) hist[i] = 0;
+    __syncthreads();
+    int cur_rep = -1;
+    uint64_t c[MSM_IPT][W];
+    for (int uu = 0; uu < nu; ++uu) {
+      const int u = u0 + uu;
+      if (ub.rep[u] != cur_rep) {
+        cur_rep = ub.rep[u];
+        const uint64_t *codes = a.codes + (int64_t)cur_rep * a.n * W;
 #pragma unroll
-  for (int i = 0; i < MSM_IPT; ++i) {
-    int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
-    if (row < a.n) {
-      uint64_t c[W];
-      load_code<W>(codes, row, c);
-      uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
-      uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
-      atomicAdd(&hist[b], 1u);
+        for (int i = 0; i < MSM_IPT; ++i) {
+          const int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
+          if (row < a.n) load_code<W>(codes, row, c[i]);
+        }
+      }
+      const unsigned long long *kept = ub.kept[u];
+      const uint64_t salt = ub.salt[u];
+      uint32_t *hu = hist + uu * B;
+#pragma unroll
+      for (int i = 0; i < MSM_IPT; ++i) {
+        const int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
+        if (row < a.n) {
+          const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
+          atomicAdd(&hu[a.lgB ? (uint32_t)(h >> sh) : 0u], 1u);
+        }
+      }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nu * B; i += MSM_NT) {
+      const uint32_t v = hist[i];
+      if (v) atomicAdd(&a.counts[(int64_t)(u0 + i / B) * B + (i % B)], v);
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  uint32_t *cnt = a.counts + (int64_t)u * B;
-  for (int i = threadIdx.x; i < B; i += MSM_NT)
-    if (hist[i]) atomicAdd(&cnt[i], hist[i]);
 }
 
 // ------------------------------------------------------------------ 2
@@ -142,47 +166,81 @@ __global__ void __launch_bounds__(1024) k_msm_scan(const __grid_constant__ MsmAr
 }
 
 // ------------------------------------------------------------------ 3
+// MSD scatter of (h2 << 32 | row) into the unit's buckets.  Elements are
+// first reordered by bucket in shared memory, so each (CTA, bucket) run is
+// written by consecutive threads (coalesced) after one global atomic per
+// non-empty bucket reserves its range.
 template <int W>
-__global__ void __launch_bounds__(MSM_NT) k_msm_scatter(const __grid_constant__ MsmArgs a,
-                                                            const __grid_constant__ UnitBatch ub) {
-  extern __shared__ uint32_t sm[];
+__global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_constant__ MsmArgs a,
+                                                              const __grid_constant__ UnitBatch ub) {
+  extern __shared__ __align__(16) unsigned char smsc[];
   const int u = blockIdx.y;
   const int B = 1 << a.lgB;
-  uint32_t *hist = sm;
-  uint32_t *bbase = sm + B;
-  for (int i = threadIdx.x; i < B; i += MSM_NT) hist[i] = 0;
+  uint64_t *stage = reinterpret_cast<uint64_t *>(smsc);                    // [MSM_TILE]
+  uint16_t *sbk = reinterpret_cast<uint16_t *>(stage + MSM_TILE);        // [MSM_TILE]
+  uint32_t *hist = reinterpret_cast<uint32_t *>(sbk + MSM_TILE);         // [B]
+  uint32_t *tstart = hist + B;                                            // [B]
+  uint32_t *gbase = tstart + B;                                           // [B]
+  __shared__ uint32_t sw[MSM_SC_NT / 32];
+  for (int i = threadIdx.x; i < B; i += MSM_SC_NT) hist[i] = 0;
   __syncthreads();
   const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
   const unsigned long long *kept = ub.kept[u];
   const uint64_t salt = ub.salt[u];
   const int sh = 64 - a.lgB;
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
-  uint32_t bk[MSM_IPT], rk[MSM_IPT], h2[MSM_IPT];
+  constexpr int IPT = MSM_TILE / MSM_SC_NT;
+  uint32_t br[IPT], h2[IPT];   // (bucket << 16 | rank) -- B <= 8192, rank < 8192
 #pragma unroll
-  for (int i = 0; i < MSM_IPT; ++i) {
-    int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
-    bk[i] = 0xffffffffu;
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
     if (row < a.n) {
       uint64_t c[W];
       load_code<W>(codes, row, c);
-      uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
-      bk[i] = a.lgB ? (uint32_t)(h >> sh) : 0u;
+      const uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
+      const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
       h2[i] = (uint32_t)h;
-      rk[i] = atomicAdd(&hist[bk[i]], 1u);
+      br[i] = (b << 16) | atomicAdd(&hist[b], 1u);
     }
   }
   __syncthreads();
-  uint32_t *cur = a.cursor + (int64_t)u * B;
-  for (int i = threadIdx.x; i < B; i += MSM_NT) {
-    uint32_t c = hist[i];
-    bbase[i] = c ? atomicAdd(&cur[i], c) : 0u;
+  {  // tile-local bucket starts (blocked scan) and global reservations
+    const int per = (B + MSM_SC_NT - 1) / MSM_SC_NT;
+    uint32_t loc = 0;
+    for (int q = 0; q < per; ++q) {
+      const int b = threadIdx.x * per + q;
+      if (b < B) loc += hist[b];
+    }
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<MSM_SC_NT>(loc, tot, sw);
+    uint32_t *cur = a.cursor + (int64_t)u * B;
+    for (int q = 0; q < per; ++q) {
+      const int b = threadIdx.x * per + q;
+      if (b < B) {
+        const uint32_t c = hist[b];
+        tstart[b] = run;
+        gbase[b] = c ? atomicAdd(&cur[b], c) : 0u;
+        run += c;
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+    if (row < a.n) {
+      const uint32_t b = br[i] >> 16;
+      const uint32_t pos = tstart[b] + (br[i] & 0xffffu);
+      stage[pos] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
+      sbk[pos] = (uint16_t)b;
+    }
   }
   __syncthreads();
   uint64_t *el = a.elems + (int64_t)u * a.n;
-#pragma unroll
-  for (int i = 0; i < MSM_IPT; ++i) {
-    int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
-    if (row < a.n) el[bbase[bk[i]] + rk[i]] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
+  const int valid = (int)min((int64_t)MSM_TILE, a.n - base);
+  for (int j = threadIdx.x; j < valid; j += MSM_SC_NT) {
+    const uint32_t b = sbk[j];
+    el[gbase[b] + (j - tstart[b])] = stage[j];
   }
 }
 
