@@ -94,6 +94,11 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
                void *d_workspace, size_t workspace_bytes, uint64_t *d_fixups,
                void *stream);
 
+/* Test hook: when d_buf is non-null, the tensor-core projection path also */
+/* writes its raw fp32 accumulator (n x replicates*length) to d_buf, so the */
+/* tests can measure the worst error against the exact fp64 product.       */
+void eg_debug_set_tc_dump(float *d_buf);
+
 /* --------------------------------------------------------------------- */
 /* Multiple-sorting-method enumeration over (replicate, mask) units.      */
 /* Replaces, per unit, masked_key_table (bitpool.py:224-253),             */

@@ -62,6 +62,7 @@ def _declare(lib):
         "eg_profile_class_name": ([I], ctypes.c_char_p),
         "eg_profile_read": ([P, P, I], I),
         "eg_row_stats": ([P, I, i64, i32, P, P, P], I),
+        "eg_debug_set_tc_dump": ([P], None),
         "eg_project_workspace": ([i64, i32, i32, i32], sz),
         "eg_project": ([P, I, i64, i32, P, P, P, i32, i32, P, P, sz, P, P], I),
         "eg_msm_workspace": ([i64, i32, i32], sz),

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "msm.cuh"
 #include "project.cuh"
+#include "project_tc.cuh"
 #include "scan_sort.cuh"
 #include "verify.cuh"
 
@@ -89,6 +90,8 @@ static int num_sms() {
   }
   return cached;
 }
+
+static int env_int(const char *name, int dflt);
 
 // ------------------------------------------------------------ projection
 static int project_tn(int cols) {
@@ -313,9 +316,16 @@ int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *
 size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t replicates) {
   int cols = length * replicates;
   int cols_pad = (cols + 31) / 32 * 32;
+  int npad = (cols + 15) / 16 * 16;
   return ws_bytes((size_t)dim * cols_pad, 4) + ws_bytes(1, 8) +
-         ws_bytes(fixup_cap(n, cols), 8) + 1024;
+         ws_bytes(fixup_cap(n, cols), 8) +
+         ws_bytes((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK, 4) + 2048;
 }
+
+// Test hook: when set, the tensor-core projection also writes its raw fp32
+// accumulator (n x cols) here (used to validate the error band).
+static float *g_tc_debug = nullptr;
+extern "C" void eg_debug_set_tc_dump(float *d_buf) { g_tc_debug = d_buf; }
 
 int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const double *d_norms,
                const double *d_r, const double *d_rnorm, int32_t length, int32_t replicates,
@@ -342,22 +352,55 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
     return EG_ERR_WORKSPACE;
   }
   EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
-  {
-    int64_t tot = (int64_t)dim * cols_pad;
-    EG_PROF(PC_MISC, st);
-    k_prep_directions<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_r, cols, dim, cols_pad, rt);
+  FixupList fl{cnt, items, cap};
+  const int npad = (cols + 15) / 16 * 16;
+  const bool use_tc = !x_is_f64 && dim % 4 == 0 && npad <= TC_MAXN &&
+                      !env_int("EG_PROJECT_SIMT", 0);
+  if (use_tc) {
+    float *img = ar.take<float>((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK);
+    if (!img) {
+      set_error("eg_project: workspace too small");
+      return EG_ERR_WORKSPACE;
+    }
+    {
+      EG_PROF(PC_MISC, st);
+      k_tc_prep_directions<<<256, 256, 0, st>>>(d_r, cols, dim, npad, img);
+    }
+    EG_LAUNCH_CHECK();
+    const size_t smem = 2 * tc_stage_bytes(npad) + sizeof(TcSmem) + 1024;
+    static size_t tc_smem_set = 0;
+    if (smem > tc_smem_set) {
+      EG_CUDA_TRY(cudaFuncSetAttribute(k_project_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+      tc_smem_set = smem;
+    }
+    const int64_t ntiles = (n + TC_M - 1) / TC_M;
+    const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
+    {
+      EG_PROF(PC_PROJECT, st);
+      k_project_tc<<<grid, TC_NT, smem, st>>>((const float *)d_x, n, dim, img, cols, npad, d_norms,
+                                              d_rnorm, tc_tau(dim), length, W, d_codes, fl,
+                                              g_tc_debug);
+    }
+    EG_LAUNCH_CHECK();
+  } else {
+    {
+      int64_t tot = (int64_t)dim * cols_pad;
+      EG_PROF(PC_MISC, st);
+      k_prep_directions<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(d_r, cols, dim, cols_pad,
+                                                                      rt);
+      EG_LAUNCH_CHECK();
+    }
+    const double tau = projection_tau(dim);
+    const int tn = project_tn(cols);
+    if (x_is_f64)
+      dispatch_project<double>(tn, (const double *)d_x, n, dim, rt, cols, cols_pad, d_norms,
+                               d_rnorm, tau, length, W, d_codes, fl, st);
+    else
+      dispatch_project<float>(tn, (const float *)d_x, n, dim, rt, cols, cols_pad, d_norms,
+                              d_rnorm, tau, length, W, d_codes, fl, st);
     EG_LAUNCH_CHECK();
   }
-  FixupList fl{cnt, items, cap};
-  const double tau = projection_tau(dim);
-  const int tn = project_tn(cols);
-  if (x_is_f64)
-    dispatch_project<double>(tn, (const double *)d_x, n, dim, rt, cols, cols_pad, d_norms, d_rnorm,
-                             tau, length, W, d_codes, fl, st);
-  else
-    dispatch_project<float>(tn, (const float *)d_x, n, dim, rt, cols, cols_pad, d_norms, d_rnorm,
-                            tau, length, W, d_codes, fl, st);
-  EG_LAUNCH_CHECK();
   const unsigned fgrid = (unsigned)num_sms() * 8;
   {
     EG_PROF(PC_FIXUP, st);

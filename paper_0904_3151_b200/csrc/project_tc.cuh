@@ -1,0 +1,309 @@
+// project_tc.cuh -- LSH projection on the 5th-generation tensor cores
+// (tcgen05.mma kind::tf32, accumulator in TMEM), 3xTF32 split precision,
+// with the certified sign band + exact fp64 fix-up of project.cuh.
+//
+// Reference: lsh.py:96-113 (_sign_bits), lsh.py:128-147 (_project_words),
+// bitpool.py:125-141 (packing).  D = X . R^T with X n x dim fp32 rows and
+// R (replicates*length) x dim fp64 directions.
+//
+// Split: x = xh + xl with xh = x with the low 13 mantissa bits cleared
+// (exactly representable in TF32) and xl = x - xh (exact in fp32); the
+// directions likewise r ~ rh + rl.  D ~= xh.rh + xh.rl + xl.rh, accumulated
+// in fp32 in TMEM.  The epilogue decides every sign with |D| > tau * |x| |r|
+// (tau bounds the split + accumulation error, see tc_tau()); the rest are
+// listed for the exact fp64 recompute (k_fixup), so the packed codes equal
+// the reference's sequential-fp64 signs bit for bit.
+//
+// Per CTA (128 threads, persistent over 128-row tiles): for each 32-wide K
+// chunk the threads load the X chunk (one row per thread), split it and
+// store xh/xl into a 128B-swizzled K-major tile; the pre-swizzled rh/rl
+// chunk images are copied in; thread 0 issues 12 MMAs (M=128, N=cols,
+// K=8 x 4 steps x 3 terms) and commits them to the stage's mbarrier.  Two
+// stages overlap the next chunk's loads with the current MMAs.  After the
+// last chunk of a tile, tcgen05.ld brings row t of the accumulator to
+// thread t, which packs its signs into the row's code words.
+#pragma once
+
+#include "common.cuh"
+#include "project.cuh"
+
+namespace eg {
+
+constexpr int TC_M = 128;       // rows per tile (UMMA M)
+constexpr int TC_BK = 32;       // fp32 elements per K chunk = one 128B swizzle row
+constexpr int TC_NT = 128;      // threads per CTA
+constexpr int TC_MAXN = 256;    // UMMA N limit (cols per pass)
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, K-major, SWIZZLE_128B: 8-row groups of
+// 128-byte rows at SBO = 1024 B; LBO unused (1); version 1 (sm100).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3fff);
+  d |= (uint64_t)1 << 16;                 // LBO (16 B units)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+  d |= (uint64_t)1 << 46;                 // version
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: D f32, A/B tf32, K-major both, N, M=128.
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(TC_M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+      smem_u32(bar)));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Byte offset of (row, 16-byte chunk c) in a 128B-swizzled K-major tile.
+__host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t c) {
+  return row * 128u + ((c ^ (row & 7u)) << 4);
+}
+
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+
+// Pre-swizzled direction images: img[(kc * 2 + part) * npad * 32 + swizzled]
+// with part 0 = rh (tf32-exact), 1 = rl = tf32-rounded residual.
+__global__ void k_tc_prep_directions(const double *__restrict__ r, int cols, int dim, int npad,
+                                     float *__restrict__ img) {
+  const int nkc = (dim + TC_BK - 1) / TC_BK;
+  const int64_t total = (int64_t)nkc * npad * TC_BK;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int kc = (int)(i / ((int64_t)npad * TC_BK));
+    const int rem = (int)(i % ((int64_t)npad * TC_BK));
+    const int n = rem / TC_BK, kk = rem % TC_BK;
+    const int q = kc * TC_BK + kk;
+    double v = (n < cols && q < dim) ? r[(int64_t)n * dim + q] : 0.0;
+    float hi = tf32_hi((float)v);
+    float lo = (float)(v - (double)hi);
+    const uint32_t off = sw128_off((uint32_t)n, (uint32_t)(kk >> 2)) / 4 + (kk & 3);
+    float *base = img + (int64_t)kc * 2 * npad * TC_BK;
+    base[off] = hi;
+    base[(int64_t)npad * TC_BK + off] = lo;
+  }
+}
+
+struct TcSmem {
+  // two stages; each: xh [128][32], xl [128][32], rh [npad][32], rl [npad][32]
+  // (sizes depend on npad, carved from the dynamic buffer)
+  uint64_t bar[2];
+  uint64_t done;
+  uint32_t tmem_base;
+};
+
+__host__ __device__ inline size_t tc_stage_bytes(int npad) {
+  return (size_t)(2 * TC_M + 2 * npad) * TC_BK * 4;
+}
+
+// 1024-byte aligned dynamic smem: [stage0][stage1][TcSmem]
+__global__ void __launch_bounds__(TC_NT, 1) k_project_tc(
+    const float *__restrict__ x, int64_t n, int dim, const float *__restrict__ img, int cols,
+    int npad, const double *__restrict__ xnorm, const double *__restrict__ rnorm, double tau,
+    int L, int W, uint64_t *__restrict__ codes, FixupList fix, float *__restrict__ dbg) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  // align the stage buffers to 1024 B in the shared window (SW128 atoms)
+  unsigned char *smem = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
+  const size_t sb = tc_stage_bytes(npad);
+  TcSmem &S = *reinterpret_cast<TcSmem *>(smem + 2 * sb);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int nkc = (dim + TC_BK - 1) / TC_BK;
+  const uint32_t ncols_alloc = npad <= 32 ? 32 : npad <= 64 ? 64 : npad <= 128 ? 128 : 256;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&S.tmem_base)),
+                 "r"(ncols_alloc));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&S.bar[0], 1);
+    mbar_init(&S.bar[1], 1);
+    mbar_init(&S.done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = S.tmem_base;
+  const uint32_t idesc = umma_idesc_tf32(npad);
+  uint32_t phase[2] = {0, 0}, done_phase = 0;
+  uint32_t issued[2] = {0, 0};   // outstanding commit on stage s
+
+  const int64_t ntiles = (n + TC_M - 1) / TC_M;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * TC_M;
+    const int64_t grow = row0 + tid;
+    const bool row_ok = grow < n;
+    const float *xr = x + (row_ok ? grow : 0) * dim;
+    for (int kc = 0; kc < nkc; ++kc) {
+      const int s = kc & 1;
+      unsigned char *st = smem + s * sb;
+      // this thread's row chunk (issue loads before waiting on the stage)
+      float4 v[8];
+      const int q0 = kc * TC_BK;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int q = q0 + c * 4;
+        v[c] = (row_ok && q < dim) ? __ldg(reinterpret_cast<const float4 *>(xr + q))
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (issued[s]) {   // MMAs that read this stage two chunks ago
+        mbar_wait(&S.bar[s], phase[s]);
+        phase[s] ^= 1;
+        issued[s] = 0;
+      }
+      float *xh = reinterpret_cast<float *>(st);
+      float *xl = xh + TC_M * TC_BK;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float4 h = make_float4(tf32_hi(v[c].x), tf32_hi(v[c].y), tf32_hi(v[c].z), tf32_hi(v[c].w));
+        float4 l = make_float4(v[c].x - h.x, v[c].y - h.y, v[c].z - h.z, v[c].w - h.w);
+        const uint32_t off = sw128_off((uint32_t)tid, (uint32_t)c) / 4;
+        *reinterpret_cast<float4 *>(xh + off) = h;
+        *reinterpret_cast<float4 *>(xl + off) = l;
+      }
+      {  // direction images (L2-resident, pre-swizzled): straight 16B copies
+        const float4 *src = reinterpret_cast<const float4 *>(img + (int64_t)kc * 2 * npad * TC_BK);
+        float4 *dst = reinterpret_cast<float4 *>(xl + TC_M * TC_BK);
+        const int nv = 2 * npad * TC_BK / 4;
+        for (int i = tid; i < nv; i += TC_NT) dst[i] = __ldg(src + i);
+      }
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        const uint32_t a_h = smem_u32(xh), a_l = smem_u32(xl);
+        const uint32_t b_h = a_l + TC_M * TC_BK * 4, b_l = b_h + npad * TC_BK * 4;
+#pragma unroll
+        for (int j = 0; j < TC_BK / 8; ++j) {   // K = 8 per MMA (32 bytes)
+          const uint32_t o = j * 32;
+          umma_tf32(tmem, umma_desc_sw128(a_h + o), umma_desc_sw128(b_h + o), idesc,
+                    (kc | j) ? 1u : 0u);
+          umma_tf32(tmem, umma_desc_sw128(a_h + o), umma_desc_sw128(b_l + o), idesc, 1u);
+          umma_tf32(tmem, umma_desc_sw128(a_l + o), umma_desc_sw128(b_h + o), idesc, 1u);
+        }
+        umma_commit(&S.bar[s]);
+        if (kc == nkc - 1) umma_commit(&S.done);
+      }
+      issued[s] = 1;
+    }
+    // epilogue: row tid of the accumulator -> this thread
+    mbar_wait(&S.done, done_phase);
+    done_phase ^= 1;
+    tc_fence_after();
+    const double xn = row_ok ? xnorm[grow] : 0.0;
+    uint64_t word = 0;
+    int cur_word = -1;   // flattened (h * W + w) of `word`
+    for (int c0 = 0; c0 < npad; c0 += 16) {
+      uint32_t acc[16];
+      tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, acc);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = c0 + j;
+        bool unc = false;
+        if (row_ok && c < cols) {
+          const double sv = (double)__uint_as_float(acc[j]);
+          if (dbg) dbg[grow * cols + c] = __uint_as_float(acc[j]);
+          const double band = tau * xn * __ldg(rnorm + c) + 1e-30;
+          const int h = c / L, t = c - h * L;
+          const int wi = h * W + (t >> 6);
+          if (wi != cur_word) {
+            if (cur_word >= 0 && word)
+              atomicOr((unsigned long long *)&codes[((int64_t)(cur_word / W) * n + grow) * W +
+                                                    (cur_word % W)],
+                       (unsigned long long)word);
+            cur_word = wi;
+            word = 0;
+          }
+          if (sv > band) word |= 1ull << (t & 63);
+          unc = !(sv > band) && !(sv < -band);
+        }
+        const unsigned long long slot = warp_append(unc, fix.count);
+        if (unc && slot < fix.cap) fix.items[slot] = ((unsigned long long)grow << 32) | (unsigned)c;
+      }
+    }
+    if (cur_word >= 0 && word)
+      atomicOr((unsigned long long *)&codes[((int64_t)(cur_word / W) * n + grow) * W +
+                                            (cur_word % W)],
+               (unsigned long long)word);
+    tc_fence_before();
+    __syncthreads();   // TMEM reads done before the next tile's MMAs overwrite it
+  }
+  // drain outstanding stage commits before freeing TMEM
+  for (int s = 0; s < 2; ++s)
+    if (issued[s]) mbar_wait(&S.bar[s], phase[s]);
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(ncols_alloc));
+}
+
+// Error band of the 3xTF32 product relative to ||x|| ||r|| (see header):
+// dropped xl.rl and the TF32 truncation of both residuals (<= 3 * 2^-20 per
+// product) plus one fp32 rounding of the TMEM accumulator per MMA
+// (3 * ceil(dim/8) MMAs, each <= 2^-22 of the running |sum| allowing
+// round-toward-zero with a guard bit), doubled; plus the reference's own
+// fp64 error.  Validated by tests/test_gpu_parity.py::
+// test_tc_projection_error_band, which measures the worst observed error.
+__host__ inline double tc_tau(int dim) {
+  const double mmas = 3.0 * (double)((dim + 7) / 8);
+  return 2.0 * (mmas * ldexp(1.0, -22) + 3.0 * ldexp(1.0, -20)) + (double)dim * ldexp(1.0, -52);
+}
+
+}  // namespace eg

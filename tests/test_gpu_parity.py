@@ -317,3 +317,43 @@ def test_cfg5_small_euclidean(eg, oracle, manifest):
     from paper_0904_3151_b200 import workloads
     _config_build(eg, oracle, manifest, "cfg5_small",
                   workloads.cfg5_points(40_000, clusters=2_000), metric="euclidean")
+
+
+def _tc_tau(dim):
+    import math
+    mmas = 3.0 * ((dim + 7) // 8)
+    return 2.0 * (mmas * 2.0 ** -22 + 3.0 * 2.0 ** -20) + dim * 2.0 ** -52
+
+
+@pytest.mark.parametrize("n,dim,length,reps", [(20000, 384, 48, 3), (7000, 100, 64, 2),
+                                               (5000, 128, 64, 1), (3000, 64, 32, 1)])
+def test_tc_projection_error_band(eg, oracle, n, dim, length, reps):
+    """The tensor-core (3xTF32) projection's raw accumulator stays well inside
+    the certified band it uses to decide signs; signs equal the oracle."""
+    import torch
+    from paper_0904_3151_b200 import _native, engine
+    rng = np.random.default_rng(n + dim)
+    x = rng.standard_normal((n, dim)).astype(np.float32)
+    x[: n // 4] = np.abs(x[: n // 4])          # skewed rows like config 3
+    dev = torch.device("cuda", 0)
+    xd = torch.from_numpy(x).to(dev)
+    cols = length * reps
+    dump = torch.zeros((n, cols), dtype=torch.float32, device=dev)
+    lib = _native.lib()
+    lib.eg_debug_set_tc_dump(dump.data_ptr())
+    try:
+        norms = engine.validate_rows(xd)
+        codes, _ = engine.project_codes(xd, norms, length, 0, list(range(1, reps + 1)))
+        torch.cuda.synchronize()
+    finally:
+        lib.eg_debug_set_tc_dump(None)
+    acc = dump.cpu().numpy().astype(np.float64)
+    r = np.concatenate([engine.directions(length, dim, 0, h) for h in range(1, reps + 1)])
+    exact = x.astype(np.float64) @ r.T
+    scale = np.linalg.norm(x.astype(np.float64), axis=1)[:, None] * np.linalg.norm(r, axis=1)[None, :]
+    ratio = np.abs(acc - exact) / scale
+    tau = _tc_tau(dim)
+    assert ratio.max() < tau / 2, (ratio.max(), tau)
+    for h in range(reps):
+        want = oracle.project_words(x, length, 0, h + 1)
+        np.testing.assert_array_equal(codes[h].cpu().numpy().view(np.uint64), want)
