@@ -15,6 +15,7 @@
 #include "msm.cuh"
 #include "project.cuh"
 #include "project_tc.cuh"
+#include <cudaTypedefs.h>
 #include "scan_sort.cuh"
 #include "verify.cuh"
 
@@ -322,6 +323,31 @@ size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t repl
          ws_bytes((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK, 4) + 2048;
 }
 
+// TMA descriptor of the row-major fp32 rows: box = 32 columns (128 B, one
+// swizzle row) x 128 rows, SWIZZLE_128B, out-of-bounds rows zero-filled.
+static bool make_x_tensor_map(CUtensorMap *map, const void *d_x, int64_t n, int dim) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = (PFN_cuTensorMapEncodeTiled)fn;
+  }
+  if (((uintptr_t)d_x & 15) || (dim * 4) % 16) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)dim, (cuuint64_t)n};
+  cuuint64_t gstride[1] = {(cuuint64_t)dim * 4};
+  cuuint32_t box[2] = {TC_BK, TC_M};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(d_x), gdim,
+                      gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // Test hook: when set, the tensor-core projection also writes its raw fp32
 // accumulator (n x cols) here (used to validate the error band).
 static float *g_tc_debug = nullptr;
@@ -367,20 +393,36 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
       k_tc_prep_directions<<<256, 256, 0, st>>>(d_r, cols, dim, npad, img);
     }
     EG_LAUNCH_CHECK();
-    const size_t smem = 2 * tc_stage_bytes(npad) + sizeof(TcSmem) + 1024;
-    static size_t tc_smem_set = 0;
-    if (smem > tc_smem_set) {
-      EG_CUDA_TRY(cudaFuncSetAttribute(k_project_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-      tc_smem_set = smem;
-    }
     const int64_t ntiles = (n + TC_M - 1) / TC_M;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
-    {
+    CUtensorMap xmap;
+    const bool tma_ok = !env_int("EG_PROJECT_TC1", 0) && make_x_tensor_map(&xmap, d_x, n, dim);
+    if (tma_ok) {
+      const size_t sbytes = tc2_stage_bytes(npad);
+      const int nstages = (int)std::min<size_t>(4, ((size_t)200 << 10) / sbytes);
+      const size_t smem = nstages * sbytes + sizeof(Tc2Bars) + 1024;
+      static size_t tc2_smem_set = 0;
+      if (smem > tc2_smem_set) {
+        EG_CUDA_TRY(cudaFuncSetAttribute(k_project_tc2,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        tc2_smem_set = smem;
+      }
       EG_PROF(PC_PROJECT, st);
-      k_project_tc<<<grid, TC_NT, smem, st>>>((const float *)d_x, n, dim, img, cols, npad, d_norms,
-                                              d_rnorm, tc_tau(dim), length, W, d_codes, fl,
-                                              g_tc_debug);
+      k_project_tc2<<<grid, TC2_THREADS, smem, st>>>(xmap, n, dim, img, cols, npad, nstages,
+                                                     d_norms, d_rnorm, tc_tau(dim), length, W,
+                                                     d_codes, fl, g_tc_debug);
+    } else {
+      const size_t smem = 2 * tc_stage_bytes(npad) + sizeof(TcSmem) + 1024;
+      static size_t tc_smem_set = 0;
+      if (smem > tc_smem_set) {
+        EG_CUDA_TRY(cudaFuncSetAttribute(k_project_tc,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        tc_smem_set = smem;
+      }
+      EG_PROF(PC_PROJECT, st);
+      k_project_tc<<<grid, TC_NT, smem, st>>>((const float *)d_x, n, dim, img, cols, npad,
+                                              d_norms, d_rnorm, tc_tau(dim), length, W, d_codes,
+                                              fl, g_tc_debug);
     }
     EG_LAUNCH_CHECK();
   } else {

@@ -24,6 +24,8 @@
 // thread t, which packs its signs into the row's code words.
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "project.cuh"
 
@@ -292,6 +294,224 @@ __global__ void __launch_bounds__(TC_NT, 1) k_project_tc(
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(ncols_alloc));
+}
+
+
+// ====================================================================
+// Warp-specialised, TMA-fed version (the production path).
+//   warp 0      : producer -- TMA 2D load of the X chunk (128 rows x 128 B,
+//                 SWIZZLE_128B, OOB rows zero-filled) + one bulk copy of the
+//                 pre-swizzled rh/rl chunk image, both completing on full[s]
+//   warp 1      : TMEM allocation; lane 0 issues the 12 MMAs per chunk into
+//                 one of two TMEM accumulators, commits empty[s] / accfull[b]
+//   warps 4-7   : converters -- split the landed X chunk into xh (in place)
+//                 and xl, fence.proxy.async, arrive conv[s]
+//   warps 8-11  : epilogue -- tcgen05.ld their lane quarter of the finished
+//                 accumulator, certified signs -> packed code words, fix-up
+//                 list; arrive accempty[b]
+// Stages are ring-buffered with mbarrier phase parity; the accumulator is
+// double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
+constexpr int TC2_THREADS = 384;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes,
+                                          uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct Tc2Bars {
+  uint64_t full[4], conv[4], empty[4], accfull[2], accempty[2];
+  uint32_t tmem_base;
+};
+
+__host__ __device__ inline size_t tc2_stage_bytes(int npad) {
+  return (size_t)(2 * TC_M + 2 * npad) * TC_BK * 4;   // x/xh, xl, rh, rl
+}
+
+__global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
+    const __grid_constant__ CUtensorMap xmap, int64_t n, int dim, const float *__restrict__ img,
+    int cols, int npad, int nstages, const double *__restrict__ xnorm,
+    const double *__restrict__ rnorm, double tau, int L, int W, uint64_t *__restrict__ codes,
+    FixupList fix, float *__restrict__ dbg) {
+  extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
+  unsigned char *smem = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
+  const size_t sb = tc2_stage_bytes(npad);
+  Tc2Bars &B = *reinterpret_cast<Tc2Bars *>(smem + nstages * sb);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nkc = (dim + TC_BK - 1) / TC_BK;
+  const int64_t ntiles = (n + TC_M - 1) / TC_M;
+  const uint32_t xbytes = TC_M * TC_BK * 4, rbytes = 2u * npad * TC_BK * 4;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&B.tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int s = 0; s < nstages; ++s) {
+      mbar_init(&B.full[s], 1);
+      mbar_init(&B.conv[s], 128);
+      mbar_init(&B.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&B.accfull[b], 1);
+      mbar_init(&B.accempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&xmap) : "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = B.tmem_base;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % nstages;
+          const uint32_t use = it / nstages;
+          mbar_wait(&B.empty[s], (use & 1) ^ 1);
+          unsigned char *st = smem + s * sb;
+          mbar_expect_tx(&B.full[s], xbytes + rbytes);
+          tma_load_2d(st, &xmap, kc * TC_BK, (int)(tile * TC_M), &B.full[s]);
+          bulk_load(st + 2 * xbytes, img + (int64_t)kc * 2 * npad * TC_BK, rbytes, &B.full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ----------------------------------------------------------------- MMA
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc_tf32(npad);
+      uint32_t it = 0, t = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+        const uint32_t b = t & 1, buse = t >> 1;
+        mbar_wait(&B.accempty[b], (buse & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dcol = tmem + b * 256;
+        for (int kc = 0; kc < nkc; ++kc, ++it) {
+          const int s = it % nstages;
+          const uint32_t use = it / nstages;
+          mbar_wait(&B.conv[s], use & 1);
+          tc_fence_after();
+          const uint32_t a_h = smem_u32(smem + s * sb), a_l = a_h + xbytes;
+          const uint32_t b_h = a_l + xbytes, b_l = b_h + npad * TC_BK * 4;
+#pragma unroll
+          for (int j = 0; j < TC_BK / 8; ++j) {
+            const uint32_t o = j * 32;
+            umma_tf32(dcol, umma_desc_sw128(a_h + o), umma_desc_sw128(b_h + o), idesc,
+                      (kc | j) ? 1u : 0u);
+            umma_tf32(dcol, umma_desc_sw128(a_h + o), umma_desc_sw128(b_l + o), idesc, 1u);
+            umma_tf32(dcol, umma_desc_sw128(a_l + o), umma_desc_sw128(b_h + o), idesc, 1u);
+          }
+          umma_commit(&B.empty[s]);
+          if (kc == nkc - 1) umma_commit(&B.accfull[b]);
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------------------------------------------------- converters
+    const uint32_t row = (uint32_t)(tid - 128);
+    uint32_t it = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int kc = 0; kc < nkc; ++kc, ++it) {
+        const int s = it % nstages;
+        const uint32_t use = it / nstages;
+        mbar_wait(&B.full[s], use & 1);
+        float *xh = reinterpret_cast<float *>(smem + s * sb);
+        float *xl = xh + TC_M * TC_BK;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const uint32_t off = sw128_off(row, (uint32_t)c) / 4;
+          const float4 v = *reinterpret_cast<const float4 *>(xh + off);
+          const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+          *reinterpret_cast<float4 *>(xh + off) = h;
+          *reinterpret_cast<float4 *>(xl + off) =
+              make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        }
+        fence_async_smem();
+        mbar_arrive(&B.conv[s]);
+      }
+    }
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp - 8;                       // == warp % 4: TMEM lane quarter
+    uint32_t t = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      const uint32_t b = t & 1, buse = t >> 1;
+      mbar_wait(&B.accfull[b], buse & 1);
+      tc_fence_after();
+      const int64_t grow = tile * TC_M + q * 32 + lane;
+      const bool row_ok = grow < n;
+      const double xn = row_ok ? __ldg(xnorm + grow) : 0.0;
+      uint64_t word = 0;
+      int cur_word = -1;
+      for (int c0 = 0; c0 < npad; c0 += 16) {
+        uint32_t acc[16];
+        tmem_ld16(tmem + b * 256 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, acc);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int c = c0 + j;
+          bool unc = false;
+          if (row_ok && c < cols) {
+            const float fv = __uint_as_float(acc[j]);
+            if (dbg) dbg[grow * cols + c] = fv;
+            const double sv = (double)fv;
+            const double band = tau * xn * __ldg(rnorm + c) + 1e-30;
+            const int h = c / L, tt = c - h * L;
+            const int wi = h * W + (tt >> 6);
+            if (wi != cur_word) {
+              if (cur_word >= 0 && word)
+                atomicOr((unsigned long long *)&codes[((int64_t)(cur_word / W) * n + grow) * W +
+                                                      (cur_word % W)],
+                         (unsigned long long)word);
+              cur_word = wi;
+              word = 0;
+            }
+            if (sv > band) word |= 1ull << (tt & 63);
+            unc = !(sv > band) && !(sv < -band);
+          }
+          const unsigned long long slot = warp_append(unc, fix.count);
+          if (unc && slot < fix.cap)
+            fix.items[slot] = ((unsigned long long)grow << 32) | (unsigned)c;
+        }
+      }
+      if (cur_word >= 0 && word)
+        atomicOr((unsigned long long *)&codes[((int64_t)(cur_word / W) * n + grow) * W +
+                                              (cur_word % W)],
+                 (unsigned long long)word);
+      tc_fence_before();
+      mbar_arrive(&B.accempty[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // Error band of the 3xTF32 product relative to ||x|| ||r|| (see header):
