@@ -320,7 +320,8 @@ size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t repl
   int npad = (cols + 15) / 16 * 16;
   return ws_bytes((size_t)dim * cols_pad, 4) + ws_bytes(1, 8) +
          ws_bytes(fixup_cap(n, cols), 8) +
-         ws_bytes((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK, 4) + 2048;
+         ws_bytes((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK, 4) +
+         ws_bytes((size_t)replicates * n * ((length + 63) / 64), 8) + 2048;
 }
 
 // TMA descriptor of the row-major fp32 rows: box = 32 columns (128 B, one
@@ -399,7 +400,7 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
     const bool tma_ok = !env_int("EG_PROJECT_TC1", 0) && make_x_tensor_map(&xmap, d_x, n, dim);
     if (tma_ok) {
       const size_t sbytes = tc2_stage_bytes(npad);
-      const int nstages = (int)std::min<size_t>(4, ((size_t)200 << 10) / sbytes);
+      const int nstages = (int)std::min<size_t>(4, ((size_t)212 << 10) / sbytes);
       const size_t smem = nstages * sbytes + sizeof(Tc2Bars) + 1024;
       static size_t tc2_smem_set = 0;
       if (smem > tc2_smem_set) {
@@ -407,10 +408,34 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         tc2_smem_set = smem;
       }
-      EG_PROF(PC_PROJECT, st);
-      k_project_tc2<<<grid, TC2_THREADS, smem, st>>>(xmap, n, dim, img, cols, npad, nstages,
-                                                     d_norms, d_rnorm, tc_tau(dim), length, W,
-                                                     d_codes, fl, g_tc_debug);
+      uint64_t *unc = ar.take<uint64_t>((size_t)replicates * n * W);
+      if (!unc) {
+        set_error("eg_project: workspace too small");
+        return EG_ERR_WORKSPACE;
+      }
+      {
+        EG_PROF(PC_PROJECT, st);
+        k_project_tc2<<<grid, TC2_THREADS, smem, st>>>(xmap, n, dim, img, cols, npad, nstages,
+                                                       d_norms, d_rnorm, tc_tau(dim), length, W,
+                                                       d_codes, unc, g_tc_debug,
+                                                       env_int("EG_TC_EXP", 0));
+      }
+      EG_LAUNCH_CHECK();
+      {
+        EG_PROF(PC_FIXUP, st);
+        const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
+        if (fsm > 48 * 1024)
+          EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_bits,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)fsm));
+        const unsigned fg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+        k_fixup_bits<<<fg, 256, fsm, st>>>((const float *)d_x, n, dim, d_r, length, W,
+                                           replicates, d_codes, unc, cnt);
+      }
+      EG_LAUNCH_CHECK();
+      if (d_fixups)
+        EG_CUDA_TRY(cudaMemcpyAsync(d_fixups, cnt, 8, cudaMemcpyDeviceToDevice, st));
+      return EG_OK;
     } else {
       const size_t smem = 2 * tc_stage_bytes(npad) + sizeof(TcSmem) + 1024;
       static size_t tc_smem_set = 0;

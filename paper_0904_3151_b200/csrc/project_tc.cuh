@@ -344,6 +344,11 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 struct Tc2Bars {
   uint64_t full[4], conv[4], empty[4], accfull[2], accempty[2];
   uint32_t tmem_base;
+  // epilogue column tables: word index (h * W + t / 64), bit (t % 64),
+  // tau * ||r_c|| (fp32, rounded up)
+  uint16_t colw[TC_MAXN];
+  uint8_t colb[TC_MAXN];
+  float colband[TC_MAXN];
 };
 
 __host__ __device__ inline size_t tc2_stage_bytes(int npad) {
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
     const __grid_constant__ CUtensorMap xmap, int64_t n, int dim, const float *__restrict__ img,
     int cols, int npad, int nstages, const double *__restrict__ xnorm,
     const double *__restrict__ rnorm, double tau, int L, int W, uint64_t *__restrict__ codes,
-    FixupList fix, float *__restrict__ dbg) {
+    uint64_t *__restrict__ unc_bits, float *__restrict__ dbg, int exp_flags) {
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   unsigned char *smem = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
   const size_t sb = tc2_stage_bytes(npad);
@@ -368,6 +373,12 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
         smem_u32(&B.tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int c = tid; c < npad; c += TC2_THREADS) {
+    const int h = c / L, t = c - h * L;
+    B.colw[c] = (uint16_t)(c < cols ? h * W + (t >> 6) : 0xffff);
+    B.colb[c] = (uint8_t)(t & 63);
+    B.colband[c] = c < cols ? (float)(tau * rnorm[c] * (1.0 + 1e-6)) : 0.f;
   }
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) {
@@ -397,9 +408,11 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
           const uint32_t use = it / nstages;
           mbar_wait(&B.empty[s], (use & 1) ^ 1);
           unsigned char *st = smem + s * sb;
-          mbar_expect_tx(&B.full[s], xbytes + rbytes);
+          const bool load_r = !(exp_flags & 4) || use == 0;
+          mbar_expect_tx(&B.full[s], xbytes + (load_r ? rbytes : 0));
           tma_load_2d(st, &xmap, kc * TC_BK, (int)(tile * TC_M), &B.full[s]);
-          bulk_load(st + 2 * xbytes, img + (int64_t)kc * 2 * npad * TC_BK, rbytes, &B.full[s]);
+          if (load_r)
+            bulk_load(st + 2 * xbytes, img + (int64_t)kc * 2 * npad * TC_BK, rbytes, &B.full[s]);
         }
       }
     }
@@ -445,7 +458,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         float *xh = reinterpret_cast<float *>(smem + s * sb);
         float *xl = xh + TC_M * TC_BK;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < ((exp_flags & 2) ? 0 : 8); ++c) {
           const uint32_t off = sw128_off(row, (uint32_t)c) / 4;
           const float4 v = *reinterpret_cast<const float4 *>(xh + off);
           const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
@@ -467,43 +480,41 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       tc_fence_after();
       const int64_t grow = tile * TC_M + q * 32 + lane;
       const bool row_ok = grow < n;
-      const double xn = row_ok ? __ldg(xnorm + grow) : 0.0;
-      uint64_t word = 0;
-      int cur_word = -1;
-      for (int c0 = 0; c0 < npad; c0 += 16) {
+      const float xn = row_ok ? (float)(__ldg(xnorm + grow) * (1.0 + 1e-6)) : 0.f;
+      uint64_t word = 0, uword = 0;
+      uint32_t cur_word = 0xffffffffu;
+      // Each row's words are produced entirely by this thread, in column
+      // order, so they are stored (not OR-ed) when the word index changes.
+      auto flush = [&](void) {
+        if (cur_word != 0xffffffffu && row_ok) {
+          const int64_t idx = ((int64_t)(cur_word / W) * n + grow) * W + (cur_word % W);
+          codes[idx] = word;
+          unc_bits[idx] = uword;
+        }
+      };
+      for (int c0 = 0; c0 < ((exp_flags & 1) ? 0 : npad); c0 += 16) {
         uint32_t acc[16];
         tmem_ld16(tmem + b * 256 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, acc);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int c = c0 + j;
-          bool unc = false;
-          if (row_ok && c < cols) {
-            const float fv = __uint_as_float(acc[j]);
-            if (dbg) dbg[grow * cols + c] = fv;
-            const double sv = (double)fv;
-            const double band = tau * xn * __ldg(rnorm + c) + 1e-30;
-            const int h = c / L, tt = c - h * L;
-            const int wi = h * W + (tt >> 6);
-            if (wi != cur_word) {
-              if (cur_word >= 0 && word)
-                atomicOr((unsigned long long *)&codes[((int64_t)(cur_word / W) * n + grow) * W +
-                                                      (cur_word % W)],
-                         (unsigned long long)word);
-              cur_word = wi;
-              word = 0;
-            }
-            if (sv > band) word |= 1ull << (tt & 63);
-            unc = !(sv > band) && !(sv < -band);
+          const uint32_t wi = B.colw[c];
+          if (wi == 0xffffu) continue;
+          const float sv = __uint_as_float(acc[j]);
+          if (dbg && row_ok) dbg[grow * cols + c] = sv;
+          const float band = B.colband[c] * xn + 1e-30f;
+          if (wi != cur_word) {
+            flush();
+            cur_word = wi;
+            word = 0;
+            uword = 0;
           }
-          const unsigned long long slot = warp_append(unc, fix.count);
-          if (unc && slot < fix.cap)
-            fix.items[slot] = ((unsigned long long)grow << 32) | (unsigned)c;
+          const uint64_t bit = 1ull << B.colb[c];
+          if (sv > band) word |= bit;
+          else if (!(sv < -band)) uword |= bit;
         }
       }
-      if (cur_word >= 0 && word)
-        atomicOr((unsigned long long *)&codes[((int64_t)(cur_word / W) * n + grow) * W +
-                                              (cur_word % W)],
-                 (unsigned long long)word);
+      flush();
       tc_fence_before();
       mbar_arrive(&B.accempty[b]);
     }
@@ -512,6 +523,57 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
   __syncthreads();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// Exact recompute of the band entries flagged in the bitmap (same layout as
+// the codes).  One warp per 32 rows: lanes compute the separately rounded
+// products of one entry in parallel (coalesced row reads), lane 0 adds them
+// in ascending q -- the reference's sequential fp64 sum (lsh.py:107-112).
+__global__ void __launch_bounds__(256) k_fixup_bits(const float *__restrict__ x, int64_t n,
+                                                    int dim, const double *__restrict__ r, int L,
+                                                    int W, int reps,
+                                                    uint64_t *__restrict__ codes,
+                                                    const uint64_t *__restrict__ unc_bits,
+                                                    unsigned long long *__restrict__ count) {
+  extern __shared__ double prod_all[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double *prod = prod_all + (int64_t)wib * dim;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned long long mine = 0;
+  for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * 32; base < n;
+       base += nwarps * 32) {
+    const int64_t row = base + lane;
+    for (int h = 0; h < reps; ++h) {
+      for (int w = 0; w < W; ++w) {
+        uint64_t u = row < n ? unc_bits[((int64_t)h * n + row) * W + w] : 0ull;
+        unsigned pend = __ballot_sync(0xffffffffu, u != 0);
+        while (pend) {
+          const int src = __ffs(pend) - 1;
+          uint64_t uu = __shfl_sync(0xffffffffu, u, src);
+          const int64_t rr = base + src;
+          while (uu) {
+            const int bit = __ffsll((long long)uu) - 1;
+            uu &= uu - 1;
+            const int t = w * 64 + bit;
+            const int c = h * L + t;
+            const float *xr = x + rr * dim;
+            const double *rc = r + (int64_t)c * dim;
+            for (int qq = lane; qq < dim; qq += 32) prod[qq] = __dmul_rn((double)xr[qq], rc[qq]);
+            __syncwarp();
+            if (lane == 0) {
+              double acc = 0.0;
+              for (int qq = 0; qq < dim; ++qq) acc = __dadd_rn(acc, prod[qq]);
+              if (acc > 0.0) codes[((int64_t)h * n + rr) * W + w] |= 1ull << bit;
+              ++mine;
+            }
+            __syncwarp();
+          }
+          pend &= pend - 1;
+        }
+      }
+    }
+  }
+  if (lane == 0 && mine) atomicAdd(count, mine);
 }
 
 // Error band of the 3xTF32 product relative to ||x|| ||r|| (see header):

@@ -353,6 +353,8 @@ def test_tc_projection_error_band(eg, oracle, n, dim, length, reps):
     scale = np.linalg.norm(x.astype(np.float64), axis=1)[:, None] * np.linalg.norm(r, axis=1)[None, :]
     ratio = np.abs(acc - exact) / scale
     tau = _tc_tau(dim)
+    print(f"tc band: max err/(|x||r|) = {ratio.max():.3e}, tau = {tau:.3e}, "
+          f"in-band share = {np.mean(np.abs(exact) <= tau * scale):.2e}")
     assert ratio.max() < tau / 2, (ratio.max(), tau)
     for h in range(reps):
         want = oracle.project_words(x, length, 0, h + 1)
