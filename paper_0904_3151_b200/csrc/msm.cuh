@@ -334,7 +334,7 @@ struct HGroupSmem {
   uint32_t pp[CAP / 4 + 1];  // pair prefix per group
   uint8_t b2b[EG_MAX_LENGTH];
   unsigned long long sw[NT / 32];
-  uint32_t nruns, maxrun, raw, neu;
+  uint32_t nruns, maxrun, raw, neu, ncand;
 };
 
 constexpr unsigned long long HG_EMPTY = ~0ull;
@@ -354,25 +354,67 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const 
   constexpr uint32_t MCAP = CAP / 2, GCAP = CAP / 4;
   const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
   const int rep = ub.rep[u];
-  const uint32_t T = pow2_at_least(2 * s);
-  // 1. load the bucket (coalesced) while the table is cleared
+  // 1. load the bucket (coalesced)
   uint64_t e[PT];
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const uint32_t i = threadIdx.x + j * NT;
     e[j] = i < s ? el[i] : 0ull;
   }
-  for (uint32_t i = threadIdx.x * 2; i < T; i += NT * 2)
-    *reinterpret_cast<ulonglong2 *>(&S.tab[i]) = make_ulonglong2(HG_EMPTY, HG_EMPTY);
-  if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; }
+  // 2. atomic-free singleton filter: every row writes its local index into
+  //    a slot chosen by the high bits of h2 (plain stores, last writer
+  //    wins); a row that reads back someone else's index, or finds its slot
+  //    marked contested, may share its key and becomes a candidate.  Only
+  //    candidates (true group members + ~s/FS false ones) enter the exact
+  //    hash table below, so the expensive shared-memory atomics touch a
+  //    small fraction of the bucket.
+  constexpr uint32_t FS = 2 * CAP * 4;            // u16 slots overlaying tab
+  constexpr int FSB = 31 - __builtin_clz(FS);
+  uint16_t *F = reinterpret_cast<uint16_t *>(S.tab);
+  for (uint32_t i = threadIdx.x * 8; i < FS; i += NT * 8)
+    *reinterpret_cast<uint4 *>(&F[i]) = make_uint4(~0u, ~0u, ~0u, ~0u);
+  if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; }
   __syncthreads();
-  // 2. insert: one CAS claims an empty slot (singletons: one atomic); a
-  //    repeated h2 bumps the slot's count and the second row registers it
-  uint32_t slr[PT];   // (slot << 16) | rank within the group
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     const uint32_t i = threadIdx.x + j * NT;
-    if (i < s) {
+    if (i < s) F[(uint32_t)(e[j] >> 32) >> (32 - FSB)] = (uint16_t)i;
+  }
+  __syncthreads();
+  uint32_t cand = 0;
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    const uint32_t i = threadIdx.x + j * NT;
+    if (i < s && F[(uint32_t)(e[j] >> 32) >> (32 - FSB)] != (uint16_t)i) cand |= 1u << j;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PT; ++j)
+    if (cand >> j & 1) F[(uint32_t)(e[j] >> 32) >> (32 - FSB)] = 0xfffe;
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    const uint32_t i = threadIdx.x + j * NT;
+    if (i < s && !(cand >> j & 1) && F[(uint32_t)(e[j] >> 32) >> (32 - FSB)] == 0xfffe)
+      cand |= 1u << j;
+  }
+  if (cand) atomicAdd(&S.ncand, (uint32_t)__popc(cand));
+  __syncthreads();
+  const uint32_t ncand = S.ncand;
+  if (ncand == 0) {
+    __syncthreads();
+    return true;
+  }
+  const uint32_t T = pow2_at_least(2 * ncand);
+  for (uint32_t i = threadIdx.x * 2; i < T; i += NT * 2)
+    *reinterpret_cast<ulonglong2 *>(&S.tab[i]) = make_ulonglong2(HG_EMPTY, HG_EMPTY);
+  __syncthreads();
+  // 3. insert candidates: one CAS claims an empty slot; a repeated h2 bumps
+  //    the slot's count and the second row registers it as a group
+  uint32_t slr[PT];   // (slot << 16) | rank within the group
+#pragma unroll
+  for (int j = 0; j < PT; ++j) {
+    if (cand >> j & 1) {
       uint32_t h2 = (uint32_t)(e[j] >> 32);
       if (h2 == 0xffffffffu) h2 = 0xfffffffeu;
       const unsigned long long mine = ((unsigned long long)h2 << 32) | 1ull;
@@ -410,8 +452,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const 
   uint32_t grouped = 0;   // bit j: element j sits in a multi-row group
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
-    const uint32_t i = threadIdx.x + j * NT;
-    if (i < s && (uint32_t)S.tab[slr[j] >> 16] >= 2) {
+    if ((cand >> j & 1) && (uint32_t)S.tab[slr[j] >> 16] >= 2) {
       grouped |= 1u << j;
       const uint32_t row = (uint32_t)e[j];
 #pragma unroll

@@ -562,7 +562,15 @@ __global__ void __launch_bounds__(256) k_fixup_bits(const float *__restrict__ x,
             __syncwarp();
             if (lane == 0) {
               double acc = 0.0;
-              for (int qq = 0; qq < dim; ++qq) acc = __dadd_rn(acc, prod[qq]);
+              int qq = 0;
+              for (; qq + 8 <= dim; qq += 8) {     // loads issued ahead of the add chain
+                double p8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) p8[e] = prod[qq + e];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc = __dadd_rn(acc, p8[e]);
+              }
+              for (; qq < dim; ++qq) acc = __dadd_rn(acc, prod[qq]);
               if (acc > 0.0) codes[((int64_t)h * n + rr) * W + w] |= 1ull << bit;
               ++mine;
             }
