@@ -1,0 +1,131 @@
+"""Multi-rank host logic over gloo (world_size 2, CPU).
+
+The per-rank compute is stubbed with the CPU oracle (test infrastructure);
+what is under test is paper_0904_3151_b200.distributed: row sharding of the
+projection, the all-gather of codes and norms, cyclic (replicate, mask) unit
+ownership with disjoint outputs, and the gather + merge of per-rank sorted
+edge runs on rank 0.  The result must equal the single-process oracle build.
+"""
+
+import itertools
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as tdist
+import torch.multiprocessing as mp
+
+from conftest import ROOT
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class OracleOps:
+    """CPU stand-ins for DeviceOps, built on the oracle."""
+
+    def __init__(self, orc, x_full):
+        self.orc = orc
+        self.x = np.asarray(x_full)
+
+    def norms(self, xs):
+        return torch.from_numpy(np.sqrt((xs.numpy().astype(np.float64) ** 2).sum(axis=1)))
+
+    def project(self, xs, norms, params):
+        codes = [self.orc.project_words(xs.numpy(), params.length, params.seed, h + 1)
+                 for h in range(params.replicates)]
+        return torch.from_numpy(np.stack(codes).view(np.int64))
+
+    def candidates(self, codes, params, units):
+        """Pairs owned by `units`: owner = (replicate, canonical mask of the
+        differing blocks) -- the rule the CUDA kernels implement."""
+        orc = self.orc
+        words = [c.numpy().view(np.uint64) for c in codes]
+        bounds = orc.block_partition(params.length, params.blocks)
+        masks = list(itertools.combinations(range(params.blocks), params.mismatch))
+        blk = np.zeros(params.length, dtype=np.int64)
+        for b in range(params.blocks):
+            blk[bounds[b]:bounds[b + 1]] = b
+        mine = set(units)
+        keys = []
+        for h in range(params.replicates):
+            pairs, _ = orc.enumerate_pairs(words[h], params.length, bounds, params.mismatch)
+            keep = orc.first_witness(pairs, words[:h], params.mismatch)
+            for (i, j) in pairs[keep]:
+                x = int(words[h][i, 0] ^ words[h][j, 0])
+                delta = sorted({int(blk[t]) for t in range(params.length) if x >> t & 1})
+                fill = [b for b in range(params.blocks) if b not in delta]
+                canon = tuple(sorted(delta + fill[:params.mismatch - len(delta)]))
+                unit = h * len(masks) + masks.index(canon)
+                if unit in mine:
+                    keys.append((int(i) << 32) | int(j))
+        return torch.tensor(keys, dtype=torch.int64), {}
+
+    def sort(self, keys, n):
+        return torch.sort(keys).values
+
+    def verify(self, x, norms, keys, metric, eps):
+        k = keys.numpy().view(np.uint64)
+        pairs = np.stack([(k >> np.uint64(32)).astype(np.int64),
+                          (k & np.uint64(0xffffffff)).astype(np.int64)], axis=1)
+        d = self.orc.cosine_dist(self.x, pairs)
+        keep = d <= eps
+        return keys[torch.from_numpy(keep)], torch.from_numpy(d[keep])
+
+    def merge(self, keys, dists, n):
+        order = torch.argsort(keys)
+        return keys[order], dists[order]
+
+
+def _worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    import paper_0904_3151_b200 as eg
+    from paper_0904_3151_b200 import distributed, workloads
+    x = workloads.planted_clusters(400, 8, 8, 20, 0.03, 5)
+    params = eg.MsmParams(epsilon=0.05, gamma=1e-3, length=24, mismatch=2, blocks=4,
+                          replicates=3, seed=7)
+    res = distributed.build_step(torch.from_numpy(x), params, "cosine", world, rank,
+                                 ops=OracleOps(orc, x))
+    if rank == 0:
+        np.savez(out_path, keys=res["keys"].numpy(), dist=res["dist"].numpy())
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_two_rank_build_equals_single_process(oracle, tmp_path):
+    out = str(tmp_path / "merged.npz")
+    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    got = np.load(out)
+    from paper_0904_3151_b200 import workloads
+    x = workloads.planted_clusters(400, 8, 8, 20, 0.03, 5)
+    ref = oracle.build_graph(x, 0.05, 24, 2, 4, 3, 7)
+    k = got["keys"].view(np.uint64)
+    pairs = np.stack([(k >> np.uint64(32)).astype(np.int64),
+                      (k & np.uint64(0xffffffff)).astype(np.int64)], axis=1)
+    np.testing.assert_array_equal(pairs, ref.pairs)
+    np.testing.assert_allclose(got["dist"], ref.distances, rtol=0, atol=1e-12)
+
+
+def test_unit_and_row_sharding_cover_exactly_once():
+    from paper_0904_3151_b200 import distributed
+    for total, world in [(660, 8), (28, 3), (5, 8)]:
+        seen = sorted(u for r in range(world) for u in distributed.my_units(total, world, r))
+        assert seen == list(range(total))
+    for n, world in [(1_600_000, 8), (10, 3), (7, 8)]:
+        rows = []
+        for r in range(world):
+            lo, hi, per = distributed.row_shard(n, world, r)
+            assert hi - lo <= per
+            rows.extend(range(lo, hi))
+        assert rows == list(range(n))
