@@ -15,7 +15,7 @@ import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-LIB_PATH = os.path.join(_HERE, "_native", "libepsgraph_b200.so")
+LIB_PATH = os.environ.get("EG_LIB_PATH") or os.path.join(_HERE, "_native", "libepsgraph_b200.so")
 _SRC_DIR = os.path.join(_HERE, "csrc")
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo",
               "-std=c++17", "-Xcompiler", "-fPIC", "-shared"]

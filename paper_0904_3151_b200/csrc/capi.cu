@@ -144,7 +144,10 @@ static int env_int(const char *name, int dflt) {
 }
 
 static int msm_lgb(int64_t n) {
-  const int64_t tgt = env_int("EG_MSM_TARGET", MSM_TARGET);
+  // mean bucket size: the tuned target, but never above 80% of the small
+  // tier's capacity (so Poisson tails and fully clustered buckets still fit)
+  const int64_t cap_mean = (int64_t)(0.8 * SmallCfg<1>::CAP);
+  const int64_t tgt = std::min<int64_t>(env_int("EG_MSM_TARGET", MSM_TARGET), cap_mean);
   int64_t target = (n + tgt - 1) / tgt;
   int l = ilog2_ceil((uint64_t)(target < 1 ? 1 : target));
   return l > MSM_MAX_LGB ? MSM_MAX_LGB : l;
@@ -187,13 +190,18 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
                    cudaStream_t st) {
   // histograms of several units side by side (<= 96 KB), staging for scatter
   const size_t smem_hist =
-      std::min<size_t>((size_t)96 << 10, (size_t)lay.B * 4 * lay.U) / ((size_t)lay.B * 4) *
+      std::min<size_t>((size_t)128 << 10, (size_t)lay.B * 4 * lay.U) / ((size_t)lay.B * 4) *
       ((size_t)lay.B * 4);
   a.hist_smem = (int)smem_hist;
-  const size_t smem_scatter = (size_t)MSM_TILE * 10 + (size_t)lay.B * 12;
-  const size_t smem_group = sizeof(HGroupSmem<W, SmallCfg<W>::CAP, SmallCfg<W>::NT>);
-  const size_t smem_medium =
-      sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>);
+  // smem-staged coalesced runs only pay when a tile holds several rows per
+  // bucket; for large B the scatter writes directly
+  const bool staged = lay.B <= MSM_STAGE_MAX_B;
+  a.scatter_staged = staged ? 1 : 0;
+  const size_t smem_scatter =
+      staged ? (size_t)MSM_TILE * 10 + (size_t)lay.B * 12 : (size_t)lay.B * 8;
+  const size_t smem_group =
+      sizeof(HGroupSmem<W, SmallCfg<W>::CAP, SmallCfg<W>::NT, SmallCfg<W>::MDIV>);
+  const size_t smem_medium = sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>);
   a.gcnt_min = MediumCfg<W>::CAP;
   static size_t set_hist = 0, set_scatter = 0;
   static bool set_fixed = false;

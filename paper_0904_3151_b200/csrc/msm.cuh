@@ -37,7 +37,8 @@ constexpr int MSM_TILE = MSM_IPT * MSM_NT;
 constexpr int MSM_SC_NT = 512;          // threads, scatter (16 items each)
 constexpr int MSM_TARGET = 3072;        // default target mean bucket size (tuned on cfg3)
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
-constexpr int MSM_MAX_LGB = 13;         // at most 8192 buckets per unit
+constexpr int MSM_MAX_LGB = 14;         // at most 16384 buckets per unit
+constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to this B
 
 struct UnitBatch {
   int count;
@@ -65,6 +66,7 @@ struct MsmArgs {
   int64_t spill_cap;
   int gcnt_min;                  // spilled buckets above this size count groups
   int hist_smem;                  // dynamic shared memory of k_msm_hist (bytes)
+  int scatter_staged;             // 1: k_msm_scatter reorders runs in smem
   uint8_t *out_rep;              // non-null: emit raw pairs tagged with their
                                  // replicate; the cross-replicate rule runs
                                  // later in k_xrep_filter (off the group
@@ -176,11 +178,13 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
   extern __shared__ __align__(16) unsigned char smsc[];
   const int u = blockIdx.y;
   const int B = 1 << a.lgB;
+  const bool staged = a.scatter_staged;
   uint64_t *stage = reinterpret_cast<uint64_t *>(smsc);                    // [MSM_TILE]
   uint16_t *sbk = reinterpret_cast<uint16_t *>(stage + MSM_TILE);        // [MSM_TILE]
-  uint32_t *hist = reinterpret_cast<uint32_t *>(sbk + MSM_TILE);         // [B]
-  uint32_t *tstart = hist + B;                                            // [B]
-  uint32_t *gbase = tstart + B;                                           // [B]
+  uint32_t *hist = staged ? reinterpret_cast<uint32_t *>(sbk + MSM_TILE)
+                          : reinterpret_cast<uint32_t *>(smsc);          // [B]
+  uint32_t *tstart = hist + B;                                            // [B] (staged)
+  uint32_t *gbase = staged ? tstart + B : hist + B;                       // [B]
   __shared__ uint32_t sw[MSM_SC_NT / 32];
   for (int i = threadIdx.x; i < B; i += MSM_SC_NT) hist[i] = 0;
   __syncthreads();
@@ -190,7 +194,9 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
   const int sh = 64 - a.lgB;
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
   constexpr int IPT = MSM_TILE / MSM_SC_NT;
-  uint32_t br[IPT], h2[IPT];   // (bucket << 16 | rank) -- B <= 8192, rank < 8192
+  // (bucket << 13) | rank: B <= 2^14, rank < MSM_TILE = 2^13
+  static_assert(MSM_TILE <= (1 << 13) && MSM_MAX_LGB <= 19, "br packing");
+  uint32_t br[IPT], h2[IPT];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
@@ -200,11 +206,12 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
       const uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
       const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
       h2[i] = (uint32_t)h;
-      br[i] = (b << 16) | atomicAdd(&hist[b], 1u);
+      br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
     }
   }
   __syncthreads();
-  {  // tile-local bucket starts (blocked scan) and global reservations
+  uint32_t *cur = a.cursor + (int64_t)u * B;
+  if (staged) {  // tile-local bucket starts (blocked scan) and global reservations
     const int per = (B + MSM_SC_NT - 1) / MSM_SC_NT;
     uint32_t loc = 0;
     for (int q = 0; q < per; ++q) {
@@ -213,7 +220,6 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
     }
     uint32_t tot;
     uint32_t run = block_exclusive_scan<MSM_SC_NT>(loc, tot, sw);
-    uint32_t *cur = a.cursor + (int64_t)u * B;
     for (int q = 0; q < per; ++q) {
       const int b = threadIdx.x * per + q;
       if (b < B) {
@@ -223,20 +229,33 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
         run += c;
       }
     }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
-    if (row < a.n) {
-      const uint32_t b = br[i] >> 16;
-      const uint32_t pos = tstart[b] + (br[i] & 0xffffu);
-      stage[pos] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
-      sbk[pos] = (uint16_t)b;
+  } else {
+    for (int b = threadIdx.x; b < B; b += MSM_SC_NT) {
+      const uint32_t c = hist[b];
+      gbase[b] = c ? atomicAdd(&cur[b], c) : 0u;
     }
   }
   __syncthreads();
   uint64_t *el = a.elems + (int64_t)u * a.n;
+  if (!staged) {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+      if (row < a.n)
+        el[gbase[br[i] >> 13] + (br[i] & 0x1fffu)] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+    if (row < a.n) {
+      const uint32_t pos = tstart[br[i] >> 13] + (br[i] & 0x1fffu);
+      stage[pos] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
+      sbk[pos] = (uint16_t)(br[i] >> 13);
+    }
+  }
+  __syncthreads();
   const int valid = (int)min((int64_t)MSM_TILE, a.n - base);
   for (int j = threadIdx.x; j < valid; j += MSM_SC_NT) {
     const uint32_t b = sbk[j];
@@ -324,14 +343,25 @@ __device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia,
 // majority -- cost one table insert.  A flattened, load-balanced pair loop
 // then visits every in-group pair once (the reference's group visits,
 // hamming_join.py:116-122) and applies pair_verdict.
-template <int W, int CAP, int NT>
+#ifndef EG_SMALL_MDIV
+#define EG_SMALL_MDIV 1
+#endif
+// Member capacity of a bucket tier: CAP / MDIV grouped rows, half as many
+// groups.
+template <int CAP, int MDIV>
+struct MemberCap {
+  static constexpr uint32_t M = CAP / MDIV, G = CAP / MDIV / 2;
+};
+
+template <int W, int CAP, int NT, int MDIV = 1>
 struct HGroupSmem {
+  static constexpr uint32_t MCAP = MemberCap<CAP, MDIV>::M, GCAP = MemberCap<CAP, MDIV>::G;
   unsigned long long tab[2 * CAP];  // (h2 << 32 | rows) per slot; later (offset << 32 | rows)
-  uint32_t mslot[CAP / 4];   // slots holding >= 2 rows (one entry per group)
-  uint32_t members[CAP / 2]; // rows of multi-row groups, grouped
-  uint64_t codes[CAP / 2 * W];
-  uint32_t runs[CAP / 4];    // (start << 16) | len, one per group
-  uint32_t pp[CAP / 4 + 1];  // pair prefix per group
+  uint32_t mslot[GCAP];      // slots holding >= 2 rows (one entry per group)
+  uint32_t members[MCAP];    // rows of multi-row groups, grouped
+  uint64_t codes[MCAP * W];
+  uint32_t runs[GCAP];       // (start << 16) | len, one per group
+  uint32_t pp[GCAP + 1];     // pair prefix per group
   uint8_t b2b[EG_MAX_LENGTH];
   unsigned long long sw[NT / 32];
   uint32_t nruns, maxrun, raw, neu, ncand;
@@ -346,12 +376,13 @@ __device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
 // Returns false (without emitting anything) if the bucket's multi-row groups
 // hold more rows than the member capacity (CAP/2) or more groups than CAP/4;
 // the caller then re-queues it for the next tier.
-template <int W, int CAP, int NT>
-__device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT> &S, const MsmArgs &a,
-                                               const UnitBatch &ub, int u, uint32_t s0,
-                                               uint32_t s) {
+template <int W, int CAP, int NT, int MDIV>
+__device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
+                                               const MsmArgs &a, const UnitBatch &ub, int u,
+                                               uint32_t s0, uint32_t s) {
   constexpr int PT = CAP / NT;
-  constexpr uint32_t MCAP = CAP / 2, GCAP = CAP / 4;
+  constexpr uint32_t MCAP = HGroupSmem<W, CAP, NT, MDIV>::MCAP;
+  constexpr uint32_t GCAP = HGroupSmem<W, CAP, NT, MDIV>::GCAP;
   const uint64_t *el = a.elems + (int64_t)u * a.n + s0;
   const int rep = ub.rep[u];
   // 1. load the bucket (coalesced)
@@ -554,7 +585,8 @@ template <int W>
 struct SmallCfg {               // one CTA per bucket, several CTAs per SM
   static constexpr int CAP = W <= 2 ? 2048 : 1024;
   static constexpr int NT = 256;
-  static constexpr int MIN_CTAS = 4;
+  static constexpr int MIN_CTAS = EG_SMALL_MDIV == 1 ? 3 : 4;
+  static constexpr int MDIV = EG_SMALL_MDIV;
 };
 template <int W>
 struct MediumCfg {
@@ -569,7 +601,7 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
                                                        const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smraw[];
   constexpr int CAP = SmallCfg<W>::CAP, NT = SmallCfg<W>::NT;
-  using Smem = HGroupSmem<W, CAP, NT>;
+  using Smem = HGroupSmem<W, CAP, NT, SmallCfg<W>::MDIV>;
   Smem &S = *reinterpret_cast<Smem *>(smraw);
   const int u = blockIdx.y;
   const int b = blockIdx.x;
@@ -593,7 +625,7 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
     return;
   }
   for (int i = threadIdx.x; i < a.L; i += NT) S.b2b[i] = a.bit2blk[i];
-  if (!process_bucket<W, CAP, NT>(S, a, ub, u, s0, s) && threadIdx.x == 0) {
+  if (!process_bucket(S, a, ub, u, s0, s) && threadIdx.x == 0) {
     // grouped rows exceed the member capacity: hand the bucket to the
     // medium tier (it accepts any size up to its own capacity)
     const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
@@ -611,7 +643,7 @@ template <int W>
 __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
     const __grid_constant__ MsmArgs a, const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  using Smem = HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>;
+  using Smem = HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>;
   Smem &S = *reinterpret_cast<Smem *>(smraw);
   const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
@@ -624,7 +656,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
       continue;
     const int u = (int)(tag & 0x3fffffffu);
     const uint32_t s0 = a.spill[sb * 3 + 1];
-    if (!process_bucket<W, MediumCfg<W>::CAP, MediumCfg<W>::NT>(S, a, ub, u, s0, s)) {
+    if (!process_bucket(S, a, ub, u, s0, s)) {
       // still too many grouped rows: the tile kernel takes it
       if ((int64_t)s * 4 > a.n) {
         uint32_t *g = a.gcnt + (int64_t)u * a.n + s0;
