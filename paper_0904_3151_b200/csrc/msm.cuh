@@ -368,11 +368,6 @@ struct HGroupSmem {
 };
 
 constexpr unsigned long long HG_EMPTY = ~0ull;
-constexpr uint32_t HG_SMALL_GROUP = 64;   // groups up to this size: per-member pair loops
-
-__device__ __forceinline__ uint32_t big_pairs(uint32_t c) {
-  return c > HG_SMALL_GROUP ? c * (c - 1) / 2 : 0u;
-}
 
 __device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
   return v <= 1 ? 1u : 1u << (32 - __clz(v - 1));
@@ -456,13 +451,8 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
       const unsigned long long mine = ((unsigned long long)h2 << 32) | 1ull;
       uint32_t slot = h2 & (T - 1), rank = 0;
       while (true) {
-        // candidates are mostly group members: look before claiming, so a
-        // repeated key costs one atomic
-        unsigned long long old = S.tab[slot];
-        if (old == HG_EMPTY) {
-          old = atomicCAS(&S.tab[slot], HG_EMPTY, mine);
-          if (old == HG_EMPTY) break;
-        }
+        const unsigned long long old = atomicCAS(&S.tab[slot], HG_EMPTY, mine);
+        if (old == HG_EMPTY) break;
         if ((uint32_t)(old >> 32) == h2) {
           rank = (uint32_t)atomicAdd(&S.tab[slot], 1ull);
           break;
@@ -508,7 +498,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   for (int q = 0; q < RP; ++q) {
     const uint32_t r = threadIdx.x * RP + q;
     c_my[q] = r < R ? (uint32_t)S.tab[S.mslot[r]] : 0u;
-    loc += ((unsigned long long)c_my[q] << 32) | big_pairs(c_my[q]);
+    loc += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
   }
   unsigned long long tot;
   unsigned long long run = block_exclusive_scan64<NT>(loc, tot, S.sw);
@@ -525,7 +515,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
       S.runs[r] = (off << 16) | c_my[q];
       S.pp[r] = (uint32_t)run;
       atomicMax(&S.maxrun, c_my[q]);
-      run += ((unsigned long long)c_my[q] << 32) | big_pairs(c_my[q]);
+      run += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
     }
   }
   if (threadIdx.x == 0) S.pp[R] = (uint32_t)tot;
@@ -540,39 +530,11 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     }
   }
   __syncthreads();
-  // 5. every in-group pair once.  Groups of <= HG_SMALL_GROUP rows: each
-  //    member row (already in this thread's registers, code included)
-  //    walks its later partners.  Bigger groups: flattened pair index,
-  //    load-balanced over the CTA.
+  // 5. every in-group pair once (load-balanced over the CTA)
+  const uint32_t P = S.pp[R];
   const unsigned long long *kept = ub.kept[u];
   const uint64_t maskbits = ub.maskbits[u];
   uint32_t my_raw = 0, my_new = 0;
-#pragma unroll
-  for (int j = 0; j < PT; ++j) {
-    if (!(grouped >> j & 1)) continue;
-    const unsigned long long tv = S.tab[slr[j] >> 16];
-    const uint32_t cnt = (uint32_t)tv;
-    if (cnt > HG_SMALL_GROUP) continue;
-    const uint32_t off = (uint32_t)(tv >> 32), rank = slr[j] & 0xffffu;
-    const uint32_t ra = (uint32_t)e[j];
-    for (uint32_t bb = rank + 1; bb < cnt; ++bb) {
-      const uint32_t ib = off + bb;
-      uint64_t cb[W];
-#pragma unroll
-      for (int w = 0; w < W; ++w) cb[w] = S.codes[ib * W + w];
-      const uint32_t rb = S.members[ib];
-      const int v = pair_verdict<W>(cg[j], cb, ra, rb, a, kept, maskbits, rep, S.b2b);
-      my_raw += v > 0;
-      my_new += v == 2;
-      const bool emit = v == 2;
-      const unsigned long long slot = warp_append(emit, &a.ctr[0]);
-      if (emit && slot < a.out_cap) {
-        a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-        if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
-      }
-    }
-  }
-  const uint32_t P = S.pp[R];
   for (uint32_t p = threadIdx.x; p < P; p += NT) {
     uint32_t lo = 0, hi = R;  // r with pp[r] <= p < pp[r+1]
     while (hi - lo > 1) {
