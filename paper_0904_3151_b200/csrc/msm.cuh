@@ -535,30 +535,57 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   const unsigned long long *kept = ub.kept[u];
   const uint64_t maskbits = ub.maskbits[u];
   uint32_t my_raw = 0, my_new = 0;
-  for (uint32_t p = threadIdx.x; p < P; p += NT) {
+  // Each thread takes a contiguous range of the flattened pair index and
+  // walks it incrementally (one group lookup + triangular decode per thread).
+  const uint32_t chunk = (P + NT - 1) / NT;
+  uint32_t p = threadIdx.x * chunk;
+  const uint32_t pend = min(P, p + chunk);
+  if (p < pend) {
     uint32_t lo = 0, hi = R;  // r with pp[r] <= p < pp[r+1]
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
       if (S.pp[mid] <= p) lo = mid; else hi = mid;
     }
-    const uint32_t rr = S.runs[lo];
-    const uint32_t start = rr >> 16, len = rr & 0xffffu;
+    uint32_t r = lo;
+    uint32_t rr = S.runs[r];
+    uint32_t start = rr >> 16, len = rr & 0xffffu;
     uint32_t ia, ib;
-    tri_decode(p - S.pp[lo], len, ia, ib);
-    ia += start;
-    ib += start;
-    uint64_t ca[W], cb[W];
+    tri_decode(p - S.pp[r], len, ia, ib);
+    uint64_t ca[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) { ca[w] = S.codes[ia * W + w]; cb[w] = S.codes[ib * W + w]; }
-    const uint32_t ra = S.members[ia], rb = S.members[ib];
-    const int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
-    my_raw += v > 0;
-    my_new += v == 2;
-    const bool emit = v == 2;
-    const unsigned long long slot = warp_append(emit, &a.ctr[0]);
-    if (emit && slot < a.out_cap) {
-      a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-      if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+    for (int w = 0; w < W; ++w) ca[w] = S.codes[(start + ia) * W + w];
+    uint32_t ra = S.members[start + ia];
+    for (; p < pend; ++p) {
+      uint64_t cb[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) cb[w] = S.codes[(start + ib) * W + w];
+      const uint32_t rb = S.members[start + ib];
+      const int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
+      my_raw += v > 0;
+      my_new += v == 2;
+      const bool emit = v == 2;
+      const unsigned long long slot = warp_append(emit, &a.ctr[0]);
+      if (emit && slot < a.out_cap) {
+        a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+        if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+      }
+      // advance (ia, ib) in (0,1),(0,2),..,(1,2),.. order, crossing groups
+      if (++ib == len) {
+        if (++ia == len - 1) {
+          do {
+            ++r;
+          } while (r < R && S.pp[r + 1] == S.pp[r]);
+          if (r >= R) break;
+          rr = S.runs[r];
+          start = rr >> 16;
+          len = rr & 0xffffu;
+          ia = 0;
+        }
+        ib = ia + 1;
+#pragma unroll
+        for (int w = 0; w < W; ++w) ca[w] = S.codes[(start + ia) * W + w];
+        ra = S.members[start + ia];
+      }
     }
   }
   if (my_raw) atomicAdd(&S.raw, my_raw);
