@@ -61,6 +61,11 @@ def make_inputs(name: str):
     raise ValueError(name)
 
 
+def make_inputs_rows(name: str) -> int:
+    return {"cfg1": 20_000, "cfg2": 10_500_000, "cfg3": 1_600_000, "cfg4": 4_000_000,
+            "cfg5": 20_000_000}[name]
+
+
 def sample_inputs(name: str, rows: int):
     """CPU-baseline sample: the same generator at a bounded row count."""
     if name == "cfg1":
@@ -181,12 +186,17 @@ def run_reference(args, rank, world):
         times.append(time.perf_counter() - t0)
     sec = sum(times) / len(times)
     value = n / sec
-    sample = f"{args.config} generator at n={n} rows (full params), C oracle port, {cores} threads"
+    sample = (f"{args.config} generator at n={n} rows (full params), C oracle port "
+              f"(reference algorithm, oracle/), {cores} threads; points/s of that sample")
+    full_n = make_inputs_rows(args.config)
+    cfgb = config_block(args, cfg, full_n, world)
+    cfgb["parallelism"] = f"CPU oracle, {cores} threads (rank 0 only)"
+    cfgb["cpu_sample_rows"] = n
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_block(args, cfg, n, world),
+        "data": "synthetic", "config": cfgb,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -210,7 +220,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-sample-rows", type=int, default=100_000)
+    ap.add_argument("--cpu-sample-rows", type=int, default=400_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
@@ -287,7 +297,7 @@ def main():
 
     # ---------------------------------------------------------------- e2e
     e2e = None
-    if rank == 0:
+    if rank == 0 and args.e2e_steps > 0:
         if hamming:
             host = torch.from_numpy(data.view(np.int64)).pin_memory()
         else:

@@ -149,6 +149,24 @@ def test_spill_path_giant_group(eg, oracle):
         np.testing.assert_array_equal(got.array, want)
 
 
+def test_medium_tier_bucket(eg, oracle):
+    # one key group of ~3000 rows: bucket above the small tier (2048), inside
+    # the medium tier (4096); plus background rows
+    rng = np.random.default_rng(9)
+    n = 5000
+    base = np.uint64(int(rng.integers(0, 2**63)))
+    words = np.full((n, 1), base, dtype=np.uint64)
+    flip = rng.integers(0, 64, size=n).astype(np.uint64)
+    sel = rng.random(n) < 0.7
+    words[sel, 0] ^= np.uint64(1) << flip[sel]
+    words[3000:, 0] = rng.integers(0, 2**63, size=n - 3000, dtype=np.int64).astype(np.uint64)
+    pool = eg.BitStringPool(words, 64).partitioned(8)
+    for d in (1, 2):
+        got = eg.enumerate_pairs(pool, d)
+        want, _ = oracle.enumerate_pairs(words, 64, pool.block_bounds, d)
+        np.testing.assert_array_equal(got.array, want)
+
+
 def test_hamming_builder_variants(eg, oracle):
     rng = np.random.default_rng(31)
     bits = (rng.random((200, 32)) < 0.5).astype(np.uint8)
