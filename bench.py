@@ -337,9 +337,17 @@ def main():
         avg_ms = batch["ms"] / batch["count"]
         alg = sort_bytes_per_unit(n, cfg) * units_per_launch
         achieved = alg / (avg_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+                tr = json.load(f).get(args.config)
+            if tr:   # measured DRAM bytes per 16-unit batch, scaled to this batch size
+                traffic = tr["msm_batch_dram_bytes"] * units_per_launch / tr["units_per_batch"]
+        except Exception:
+            traffic = None
         roof = {"kernel": "msm unit pipeline (hist+scan+scatter+group+spill), one launch batch",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg),
                 "units_per_launch": units_per_launch, "avg_launch_ms": avg_ms}
     stage_ms = {k: v["ms"] / args.steps for k, v in kprof.items()}
