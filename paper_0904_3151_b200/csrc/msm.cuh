@@ -356,15 +356,26 @@ struct MemberCap {
 template <int W, int CAP, int NT, int MDIV = 1>
 struct HGroupSmem {
   static constexpr uint32_t MCAP = MemberCap<CAP, MDIV>::M, GCAP = MemberCap<CAP, MDIV>::G;
-  unsigned long long tab[2 * CAP];  // (h2 << 32 | rows) per slot; later (offset << 32 | rows)
+  // The grouped rows and their codes overlay the hash table once every
+  // thread has read its member position out of it (see process_bucket).
+  static constexpr bool OVERLAY = (4 + 8 * W) * MCAP <= 16 * CAP;
+  static constexpr size_t TAB_BYTES = 16 * (size_t)CAP;
+  static constexpr size_t MEM_BYTES = (size_t)(4 + 8 * W) * MCAP;
+  alignas(16) unsigned char big[OVERLAY ? TAB_BYTES : TAB_BYTES + MEM_BYTES];
   uint32_t mslot[GCAP];      // slots holding >= 2 rows (one entry per group)
-  uint32_t members[MCAP];    // rows of multi-row groups, grouped
-  uint64_t codes[MCAP * W];
   uint32_t runs[GCAP];       // (start << 16) | len, one per group
   uint32_t pp[GCAP + 1];     // pair prefix per group
   uint8_t b2b[EG_MAX_LENGTH];
   unsigned long long sw[NT / 32];
   uint32_t nruns, maxrun, raw, neu, ncand;
+  // (h2 << 32 | rows) per slot; later (member offset << 32 | rows)
+  __device__ unsigned long long *tab() { return reinterpret_cast<unsigned long long *>(big); }
+  __device__ uint64_t *codes() {
+    return reinterpret_cast<uint64_t *>(big + (OVERLAY ? 0 : TAB_BYTES));
+  }
+  __device__ uint32_t *members() {
+    return reinterpret_cast<uint32_t *>(big + (OVERLAY ? 0 : TAB_BYTES) + 8 * W * MCAP);
+  }
 };
 
 constexpr unsigned long long HG_EMPTY = ~0ull;
@@ -401,7 +412,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   //    small fraction of the bucket.
   constexpr uint32_t FS = 2 * CAP * 4;            // u16 slots overlaying tab
   constexpr int FSB = 31 - __builtin_clz(FS);
-  uint16_t *F = reinterpret_cast<uint16_t *>(S.tab);
+  uint16_t *F = reinterpret_cast<uint16_t *>(S.tab());
   for (uint32_t i = threadIdx.x * 8; i < FS; i += NT * 8)
     *reinterpret_cast<uint4 *>(&F[i]) = make_uint4(~0u, ~0u, ~0u, ~0u);
   if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; }
@@ -438,7 +449,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   }
   const uint32_t T = pow2_at_least(2 * ncand);
   for (uint32_t i = threadIdx.x * 2; i < T; i += NT * 2)
-    *reinterpret_cast<ulonglong2 *>(&S.tab[i]) = make_ulonglong2(HG_EMPTY, HG_EMPTY);
+    *reinterpret_cast<ulonglong2 *>(&S.tab()[i]) = make_ulonglong2(HG_EMPTY, HG_EMPTY);
   __syncthreads();
   // 3. insert candidates: one CAS claims an empty slot; a repeated h2 bumps
   //    the slot's count and the second row registers it as a group
@@ -451,10 +462,10 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
       const unsigned long long mine = ((unsigned long long)h2 << 32) | 1ull;
       uint32_t slot = h2 & (T - 1), rank = 0;
       while (true) {
-        const unsigned long long old = atomicCAS(&S.tab[slot], HG_EMPTY, mine);
+        const unsigned long long old = atomicCAS(&S.tab()[slot], HG_EMPTY, mine);
         if (old == HG_EMPTY) break;
         if ((uint32_t)(old >> 32) == h2) {
-          rank = (uint32_t)atomicAdd(&S.tab[slot], 1ull);
+          rank = (uint32_t)atomicAdd(&S.tab()[slot], 1ull);
           break;
         }
         slot = (slot + 1) & (T - 1);
@@ -483,7 +494,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   uint32_t grouped = 0;   // bit j: element j sits in a multi-row group
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
-    if ((cand >> j & 1) && (uint32_t)S.tab[slr[j] >> 16] >= 2) {
+    if ((cand >> j & 1) && (uint32_t)S.tab()[slr[j] >> 16] >= 2) {
       grouped |= 1u << j;
       const uint32_t row = (uint32_t)e[j];
 #pragma unroll
@@ -497,7 +508,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
 #pragma unroll
   for (int q = 0; q < RP; ++q) {
     const uint32_t r = threadIdx.x * RP + q;
-    c_my[q] = r < R ? (uint32_t)S.tab[S.mslot[r]] : 0u;
+    c_my[q] = r < R ? (uint32_t)S.tab()[S.mslot[r]] : 0u;
     loc += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
   }
   unsigned long long tot;
@@ -511,7 +522,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     const uint32_t r = threadIdx.x * RP + q;
     if (r < R) {
       const uint32_t off = (uint32_t)(run >> 32);
-      S.tab[S.mslot[r]] = ((unsigned long long)off << 32) | c_my[q];
+      S.tab()[S.mslot[r]] = ((unsigned long long)off << 32) | c_my[q];
       S.runs[r] = (off << 16) | c_my[q];
       S.pp[r] = (uint32_t)run;
       atomicMax(&S.maxrun, c_my[q]);
@@ -520,13 +531,22 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   }
   if (threadIdx.x == 0) S.pp[R] = (uint32_t)tot;
   __syncthreads();
+  // member positions out of the table first; then the (possibly overlaid)
+  // member arrays are written
+#pragma unroll
+  for (int j = 0; j < PT; ++j)
+    if (grouped >> j & 1)
+      slr[j] = (uint32_t)(S.tab()[slr[j] >> 16] >> 32) + (slr[j] & 0xffffu);
+  uint64_t *mcodes = S.codes();
+  uint32_t *mrows = S.members();
+  if (HGroupSmem<W, CAP, NT, MDIV>::OVERLAY) __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     if (grouped >> j & 1) {
-      const uint32_t pos = (uint32_t)(S.tab[slr[j] >> 16] >> 32) + (slr[j] & 0xffffu);
-      S.members[pos] = (uint32_t)e[j];
+      const uint32_t pos = slr[j];
+      mrows[pos] = (uint32_t)e[j];
 #pragma unroll
-      for (int w = 0; w < W; ++w) S.codes[pos * W + w] = cg[j][w];
+      for (int w = 0; w < W; ++w) mcodes[pos * W + w] = cg[j][w];
     }
   }
   __syncthreads();
@@ -553,13 +573,13 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     tri_decode(p - S.pp[r], len, ia, ib);
     uint64_t ca[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) ca[w] = S.codes[(start + ia) * W + w];
-    uint32_t ra = S.members[start + ia];
+    for (int w = 0; w < W; ++w) ca[w] = mcodes[(start + ia) * W + w];
+    uint32_t ra = mrows[start + ia];
     for (; p < pend; ++p) {
       uint64_t cb[W];
 #pragma unroll
-      for (int w = 0; w < W; ++w) cb[w] = S.codes[(start + ib) * W + w];
-      const uint32_t rb = S.members[start + ib];
+      for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + ib) * W + w];
+      const uint32_t rb = mrows[start + ib];
       const int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
       my_raw += v > 0;
       my_new += v == 2;
@@ -583,8 +603,8 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
         }
         ib = ia + 1;
 #pragma unroll
-        for (int w = 0; w < W; ++w) ca[w] = S.codes[(start + ia) * W + w];
-        ra = S.members[start + ia];
+        for (int w = 0; w < W; ++w) ca[w] = mcodes[(start + ia) * W + w];
+        ra = mrows[start + ia];
       }
     }
   }
@@ -612,7 +632,7 @@ template <int W>
 struct SmallCfg {               // one CTA per bucket, several CTAs per SM
   static constexpr int CAP = W <= 2 ? 2048 : 1024;
   static constexpr int NT = 256;
-  static constexpr int MIN_CTAS = EG_SMALL_MDIV == 1 ? 3 : 4;
+  static constexpr int MIN_CTAS = 4;
   static constexpr int MDIV = EG_SMALL_MDIV;
 };
 template <int W>
