@@ -329,23 +329,25 @@ def main():
     peak, peak_kind = peaks()
     units_total = cfg.replicates * math.comb(cfg.blocks, cfg.mismatch)
     units_mine = len(distributed.my_units(units_total, world, rank))
-    batch = kprof.get("msm_batch", {"ms": 0.0, "count": 0})
+    stage = kprof.get("msm_stage", {"ms": 0.0, "count": 0})
     roof = None
-    if batch["count"]:
-        batches_per_step = batch["count"] / args.steps
-        units_per_launch = units_mine / batches_per_step
-        avg_ms = batch["ms"] / batch["count"]
+    if stage["count"]:
+        # one "launch" = one eg_msm_pairs call: every (replicate, mask) unit
+        # of the build through hist / scan / scatter / group / tiers
+        units_per_launch = units_mine
+        avg_ms = stage["ms"] / stage["count"]
         alg = sort_bytes_per_unit(n, cfg) * units_per_launch
         achieved = alg / (avg_ms / 1e3) / 1e9
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
                 tr = json.load(f).get(args.config)
-            if tr:   # measured DRAM bytes per 16-unit batch, scaled to this batch size
+            if tr:   # measured DRAM bytes per 16-unit batch, scaled to the launch
                 traffic = tr["msm_batch_dram_bytes"] * units_per_launch / tr["units_per_batch"]
         except Exception:
             traffic = None
-        roof = {"kernel": "msm unit pipeline (hist+scan+scatter+group+spill), one launch batch",
+        roof = {"kernel": "eg_msm_pairs: MSM unit pipeline (hist+scan+scatter+group+tiers) "
+                          "over all units of the build",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg),

@@ -44,7 +44,7 @@ static std::vector<cudaEvent_t> g_event_pool;
 static const char *g_prof_names[PC_COUNT] = {
     "row_stats", "project", "fixup", "msm_hist", "msm_scan", "msm_scatter", "msm_group",
     "msm_spill", "msm_batch", "sort_upsweep", "scan", "sort_downsweep", "verify", "compact",
-    "misc"};
+    "misc", "msm_stage"};
 
 static cudaEvent_t take_event() {
   if (!g_event_pool.empty()) {
@@ -163,7 +163,7 @@ static int msm_batch_units(int64_t n) {
 }
 
 struct MsmLayout {
-  int lgB, B, U;
+  int lgB, B, U, sets;
   size_t bytes;
 };
 
@@ -172,6 +172,8 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   l.lgB = msm_lgb(n);
   l.B = 1 << l.lgB;
   l.U = msm_batch_units(n);
+  // two scratch sets: batch i+1's hist/scatter overlap batch i's grouping
+  l.sets = env_int("EG_MSM_STREAMS", 2) >= 2 ? 2 : 1;
   size_t b = 0;
   b += ws_bytes((size_t)l.U * l.B, 4);            // counts
   b += ws_bytes((size_t)l.U * (l.B + 1), 4);      // starts
@@ -181,13 +183,15 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   b += ws_bytes(EG_MAX_LENGTH, 1);                // bit2blk
   b += ws_bytes(3 + 2 * (size_t)reps, 8);         // counters
   b += ws_bytes((size_t)l.U * (l.B + 1) * 9, 4);  // spill list (<= 3 entries/bucket)
-  l.bytes = b + 4096;
+  b += ws_bytes(1, 8);                            // spill counter
+  l.bytes = (b + 4096) * l.sets;
   return l;
 }
 
 template <int W>
-static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch> &batches,
+static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBatch> &batches,
                    cudaStream_t st) {
+  MsmArgs a = sets[0];
   // histograms of several units side by side (<= 96 KB), staging for scatter
   const size_t smem_hist =
       std::min<size_t>((size_t)128 << 10, (size_t)lay.B * 4 * lay.U) / ((size_t)lay.B * 4) *
@@ -226,39 +230,75 @@ static int msm_run(MsmArgs a, const MsmLayout &lay, const std::vector<UnitBatch>
   }
   const unsigned tiles = (unsigned)((a.n + MSM_TILE - 1) / MSM_TILE);
   const unsigned spill_grid = (unsigned)num_sms() * 8;
-  for (const UnitBatch &ub : batches) {
-    EG_PROF_GROUP(PC_MSM_BATCH, st);
+  // Two scratch sets on two streams: the caller's stream runs hist / scan /
+  // scatter of batch i+1 while a side stream groups batch i (the first is
+  // L2/atomic bound, the second issue bound).  Events order the reuse of a
+  // set and the final join.
+  static cudaStream_t side[64];
+  static cudaEvent_t ev_scat[64][2], ev_done[64][2];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const bool two = lay.sets == 2;
+  if (two && !side[dev]) {
+    EG_CUDA_TRY(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_scat[dev][i], cudaEventDisableTiming));
+      EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_done[dev][i], cudaEventDisableTiming));
+    }
+  }
+  cudaStream_t gs = two ? side[dev] : st;
+  if (two) {   // the side stream starts after everything already on st
+    EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][0], st));
+    EG_CUDA_TRY(cudaStreamWaitEvent(gs, ev_scat[dev][0], 0));
+  }
+  for (size_t bi = 0; bi < batches.size(); ++bi) {
+    const UnitBatch &ub = batches[bi];
+    const int si = two ? (int)(bi & 1) : 0;
+    MsmArgs &x = sets[si];
+    x.hist_smem = a.hist_smem;
+    x.scatter_staged = a.scatter_staged;
+    x.gcnt_min = a.gcnt_min;
+    if (two && bi >= 2) EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_done[dev][si], 0));
     dim3 g1(tiles, ub.count);
     {
       EG_PROF(PC_MSM_HIST, st);
-      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(a, ub);
+      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(x, ub);
     }
     {
       EG_PROF(PC_MSM_SCAN, st);
-      k_msm_scan<<<ub.count, 1024, 0, st>>>(a);
+      k_msm_scan<<<ub.count, 1024, 0, st>>>(x);
     }
     {
       EG_PROF(PC_MSM_SCATTER, st);
-      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(a, ub);
+      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(x, ub);
+    }
+    if (two) {
+      EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][si], st));
+      EG_CUDA_TRY(cudaStreamWaitEvent(gs, ev_scat[dev][si], 0));
     }
     dim3 g4(lay.B, ub.count);
     {
-      EG_PROF(PC_MSM_GROUP, st);
-      k_msm_group<W><<<g4, SmallCfg<W>::NT, smem_group, st>>>(a, ub);
+      EG_PROF(PC_MSM_GROUP, gs);
+      k_msm_group<W><<<g4, SmallCfg<W>::NT, smem_group, gs>>>(x, ub);
     }
     {
-      EG_PROF(PC_MSM_SPILL, st);
-      k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, st>>>(a, ub);
+      EG_PROF(PC_MSM_SPILL, gs);
+      k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, gs>>>(x, ub);
     }
     {
-      EG_PROF(PC_MSM_SPILL, st);
-      k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, st>>>(a, ub);
+      EG_PROF(PC_MSM_SPILL, gs);
+      k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, gs>>>(x, ub);
     }
     {
-      EG_PROF(PC_MSM_SPILL, st);
-      k_msm_spill_maxgroup<<<64, 256, 0, st>>>(a);
+      EG_PROF(PC_MSM_SPILL, gs);
+      k_msm_spill_maxgroup<<<64, 256, 0, gs>>>(x);
     }
+    if (two) EG_CUDA_TRY(cudaEventRecord(ev_done[dev][si], gs));
     EG_LAUNCH_CHECK();
+  }
+  if (two) {
+    EG_CUDA_TRY(cudaEventRecord(ev_done[dev][0], gs));
+    EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_done[dev][0], 0));
   }
   return EG_OK;
 }
@@ -540,24 +580,35 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   a.d = d;
   a.lgB = lay.lgB;
   a.reps = replicates;
-  a.counts = ar.take<uint32_t>((size_t)lay.U * lay.B);
-  a.starts = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1));
-  a.cursor = ar.take<uint32_t>((size_t)lay.U * lay.B);
-  a.elems = ar.take<uint64_t>((size_t)lay.U * n);
-  a.gcnt = ar.take<uint32_t>((size_t)lay.U * n);
   uint8_t *b2b_d = ar.take<uint8_t>(EG_MAX_LENGTH);
   a.bit2blk = b2b_d;
   a.ctr = ar.take<unsigned long long>(3 + 2 * (size_t)replicates);
-  a.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 9);
   a.spill_cap = (int64_t)lay.U * (lay.B + 1) * 3;   // a bucket is queued at most 3 times
   a.out_keys = (unsigned long long *)d_out_keys;
   a.out_rep = replicates > 1 ? d_out_rep : nullptr;
   a.out_cap = capacity > 0 ? (unsigned long long)capacity : 0ull;
-  if (!a.counts || !a.starts || !a.cursor || !a.elems || !a.gcnt || !b2b_d || !a.ctr || !a.spill) {
+  if (!b2b_d || !a.ctr) {
     set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
     return EG_ERR_WORKSPACE;
   }
-  EG_CUDA_TRY(cudaMemsetAsync(a.counts, 0, (size_t)lay.U * lay.B * 4, st));
+  MsmArgs sets[2];
+  for (int si = 0; si < lay.sets; ++si) {
+    MsmArgs &x = sets[si];
+    x = a;
+    x.counts = ar.take<uint32_t>((size_t)lay.U * lay.B);
+    x.starts = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1));
+    x.cursor = ar.take<uint32_t>((size_t)lay.U * lay.B);
+    x.elems = ar.take<uint64_t>((size_t)lay.U * n);
+    x.gcnt = ar.take<uint32_t>((size_t)lay.U * n);
+    x.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 9);
+    x.spill_ctr = ar.take<unsigned long long>(1);
+    if (!x.counts || !x.starts || !x.cursor || !x.elems || !x.gcnt || !x.spill || !x.spill_ctr) {
+      set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
+      return EG_ERR_WORKSPACE;
+    }
+    EG_CUDA_TRY(cudaMemsetAsync(x.counts, 0, (size_t)lay.U * lay.B * 4, st));
+  }
+  if (lay.sets == 1) sets[1] = sets[0];
   EG_CUDA_TRY(cudaMemsetAsync(a.ctr, 0, (3 + 2 * (size_t)replicates) * 8, st));
   EG_CUDA_TRY(cudaMemcpyAsync(b2b_d, b2b, EG_MAX_LENGTH, cudaMemcpyHostToDevice, st));
 
@@ -584,11 +635,14 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
     batches.push_back(ub);
   }
   int rc = EG_OK;
-  switch (W) {
-    case 1: rc = msm_run<1>(a, lay, batches, st); break;
-    case 2: rc = msm_run<2>(a, lay, batches, st); break;
-    case 3: rc = msm_run<3>(a, lay, batches, st); break;
-    default: rc = msm_run<4>(a, lay, batches, st); break;
+  {
+    EG_PROF(PC_MSM_STAGE, st);
+    switch (W) {
+      case 1: rc = msm_run<1>(sets, lay, batches, st); break;
+      case 2: rc = msm_run<2>(sets, lay, batches, st); break;
+      case 3: rc = msm_run<3>(sets, lay, batches, st); break;
+      default: rc = msm_run<4>(sets, lay, batches, st); break;
+    }
   }
   if (rc) return rc;
   std::vector<unsigned long long> hc(3 + 2 * (size_t)replicates);

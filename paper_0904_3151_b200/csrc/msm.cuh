@@ -60,8 +60,9 @@ struct MsmArgs {
   const uint8_t *bit2blk;        // [EG_MAX_LENGTH]
   unsigned long long *out_keys;
   unsigned long long out_cap;
-  unsigned long long *ctr;       // [0] emitted, [1] max group, [2] spill count,
+  unsigned long long *ctr;       // [0] emitted, [1] max group, [2] unused,
                                  // [3..3+reps) raw, [3+reps..) new
+  unsigned long long *spill_ctr; // [0] entries on this scratch set's spill list
   uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
   int64_t spill_cap;
   int gcnt_min;                  // spilled buckets above this size count groups
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(1024) k_msm_scan(const __grid_constant__ MsmAr
     }
   }
   if (threadIdx.x == 0) st[B] = tot;
-  if (u == 0 && threadIdx.x == 0) a.ctr[2] = 0;   // spill list reset for this batch
+  if (u == 0 && threadIdx.x == 0) a.spill_ctr[0] = 0;   // spill list reset for this batch
 }
 
 // ------------------------------------------------------------------ 3
@@ -658,7 +659,7 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
   if (s < 2) return;
   if (s > CAP) {
     if (threadIdx.x == 0) {
-      const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+      const unsigned long long slot = atomicAdd(&a.spill_ctr[0], 1ull);
       if ((int64_t)slot < a.spill_cap) {
         a.spill[slot * 3 + 0] = (uint32_t)u;
         a.spill[slot * 3 + 1] = s0;
@@ -675,7 +676,7 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
   if (!process_bucket(S, a, ub, u, s0, s) && threadIdx.x == 0) {
     // grouped rows exceed the member capacity: hand the bucket to the
     // medium tier (it accepts any size up to its own capacity)
-    const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+    const unsigned long long slot = atomicAdd(&a.spill_ctr[0], 1ull);
     if ((int64_t)slot < a.spill_cap) {
       a.spill[slot * 3 + 0] = (uint32_t)u | SPILL_FROM_SMALL;
       a.spill[slot * 3 + 1] = s0;
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
   extern __shared__ __align__(16) unsigned char smraw[];
   using Smem = HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>;
   Smem &S = *reinterpret_cast<Smem *>(smraw);
-  const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
+  const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
   for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
     const uint32_t s = a.spill[sb * 3 + 2];
@@ -710,7 +711,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
         for (uint32_t i = threadIdx.x; i < s; i += MediumCfg<W>::NT) g[i] = 0;
       }
       if (threadIdx.x == 0) {
-        const unsigned long long slot = atomicAdd(&a.ctr[2], 1ull);
+        const unsigned long long slot = atomicAdd(&a.spill_ctr[0], 1ull);
         if ((int64_t)slot < a.spill_cap) {
           a.spill[slot * 3 + 0] = (uint32_t)u | SPILL_FROM_MEDIUM;
           a.spill[slot * 3 + 1] = s0;
@@ -734,7 +735,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
   __shared__ uint8_t b2b[EG_MAX_LENGTH];
   __shared__ uint32_t sraw, sneu;
   for (int i = threadIdx.x; i < a.L; i += MSM_SPILL_T) b2b[i] = a.bit2blk[i];
-  const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
+  const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (unsigned long long sb = 0; sb < nspill; ++sb) {
     const uint32_t tag = a.spill[sb * 3 + 0];
     const int u = (int)(tag & 0x3fffffffu);
@@ -827,7 +828,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
 // Largest group inside spilled buckets that could trip the reference's
 // oversized warning (hamming_join.py:341-344): max(gcnt) + 1.
 __global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
-  const unsigned long long nspill = min(a.ctr[2], (unsigned long long)a.spill_cap);
+  const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
     const uint32_t tag = a.spill[sb * 3 + 0];
     const int u = (int)(tag & 0x3fffffffu);
