@@ -163,7 +163,7 @@ static int msm_batch_units(int64_t n) {
 }
 
 struct MsmLayout {
-  int lgB, B, U, sets;
+  int lgB, B, U, sets, tiled, ntiles;
   size_t bytes;
 };
 
@@ -174,6 +174,10 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   l.U = msm_batch_units(n);
   // two scratch sets: batch i+1's hist/scatter overlap batch i's grouping
   l.sets = env_int("EG_MSM_STREAMS", 2) >= 2 ? 2 : 1;
+  // tile-local partition when every tile holds >= 4 rows per bucket and the
+  // group kernel can stage the per-tile segment table
+  l.ntiles = (int)((n + MSM_TILE - 1) / MSM_TILE);
+  l.tiled = env_int("EG_MSM_TILED", 1) && l.B * 4 <= MSM_TILE && l.ntiles <= 2048;
   size_t b = 0;
   b += ws_bytes((size_t)l.U * l.B, 4);            // counts
   b += ws_bytes((size_t)l.U * (l.B + 1), 4);      // starts
@@ -184,6 +188,11 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   b += ws_bytes(3 + 2 * (size_t)reps, 8);         // counters
   b += ws_bytes((size_t)l.U * (l.B + 1) * 9, 4);  // spill list (<= 3 entries/bucket)
   b += ws_bytes(1, 8);                            // spill counter
+  if (l.tiled) {
+    b += ws_bytes((size_t)l.U * (l.B + 1) * l.ntiles, 2);   // tile bucket offsets
+    b += ws_bytes((size_t)l.U * n, 8);                      // spilled bucket copies
+    b += ws_bytes(1, 8);
+  }
   l.bytes = (b + 4096) * l.sets;
   return l;
 }
@@ -207,6 +216,13 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
       sizeof(HGroupSmem<W, SmallCfg<W>::CAP, SmallCfg<W>::NT, SmallCfg<W>::MDIV>);
   const size_t smem_medium = sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>);
   a.gcnt_min = MediumCfg<W>::CAP;
+  const size_t smem_tsort = (size_t)MSM_TILE * 8 + (size_t)lay.B * 4;
+  static size_t set_tsort = 0;
+  if (lay.tiled && smem_tsort > set_tsort) {
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_tsort<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_tsort));
+    set_tsort = smem_tsort;
+  }
   static size_t set_hist = 0, set_scatter = 0;
   static bool set_fixed = false;
   if (smem_hist > set_hist) {
@@ -260,17 +276,22 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     x.gcnt_min = a.gcnt_min;
     if (two && bi >= 2) EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_done[dev][si], 0));
     dim3 g1(tiles, ub.count);
-    {
-      EG_PROF(PC_MSM_HIST, st);
-      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(x, ub);
-    }
-    {
-      EG_PROF(PC_MSM_SCAN, st);
-      k_msm_scan<<<ub.count, 1024, 0, st>>>(x);
-    }
-    {
+    if (lay.tiled) {
       EG_PROF(PC_MSM_SCATTER, st);
-      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(x, ub);
+      k_msm_tsort<W><<<g1, MSM_SC_NT, smem_tsort, st>>>(x, ub);
+    } else {
+      {
+        EG_PROF(PC_MSM_HIST, st);
+        k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(x, ub);
+      }
+      {
+        EG_PROF(PC_MSM_SCAN, st);
+        k_msm_scan<<<ub.count, 1024, 0, st>>>(x);
+      }
+      {
+        EG_PROF(PC_MSM_SCATTER, st);
+        k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(x, ub);
+      }
     }
     if (two) {
       EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][si], st));
@@ -602,6 +623,18 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
     x.gcnt = ar.take<uint32_t>((size_t)lay.U * n);
     x.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 9);
     x.spill_ctr = ar.take<unsigned long long>(1);
+    x.tiled = lay.tiled;
+    x.ntiles = lay.ntiles;
+    if (lay.tiled) {
+      x.toff = ar.take<uint16_t>((size_t)lay.U * (lay.B + 1) * lay.ntiles);
+      x.toff_ro = x.toff;
+      x.sel = ar.take<uint64_t>((size_t)lay.U * n);
+      x.sel_ctr = ar.take<unsigned long long>(1);
+      if (!x.toff || !x.sel || !x.sel_ctr) {
+        set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
+        return EG_ERR_WORKSPACE;
+      }
+    }
     if (!x.counts || !x.starts || !x.cursor || !x.elems || !x.gcnt || !x.spill || !x.spill_ctr) {
       set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
       return EG_ERR_WORKSPACE;

@@ -377,3 +377,21 @@ def test_tc_projection_error_band(eg, oracle, n, dim, length, reps):
     for h in range(reps):
         want = oracle.project_words(x, length, 0, h + 1)
         np.testing.assert_array_equal(codes[h].cpu().numpy().view(np.uint64), want)
+
+
+@pytest.mark.parametrize("env", [{"EG_MSM_TILED": "0"}, {"EG_MSM_STREAMS": "1"},
+                                 {"EG_MSM_TILED": "0", "EG_MSM_STREAMS": "1"}])
+def test_msm_launch_variants(eg, oracle, manifest, monkeypatch, env):
+    """The classic (global histogram + scatter) partition and the single-stream
+    schedule give the same pair sets as the defaults."""
+    from paper_0904_3151_b200 import workloads
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    words = workloads.cfg2_words(200_000, 10_000)
+    got = eg.build_graph_hamming(eg.BitStringPool(words, 64).partitioned(8), 2)
+    assert oracle.pair_digest(got.array) == manifest["cfg2_small"]["pairs_sha256"]
+    g = golden("random_pools")
+    for case in manifest["random_pools"][:16]:
+        c = case["case"]
+        pool = eg.BitStringPool(g[f"words_{c}"], case["length"]).partitioned(case["k"])
+        np.testing.assert_array_equal(eg.enumerate_pairs(pool, case["d"]).array, g[f"pairs_{c}"])
