@@ -797,11 +797,17 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
       in_smem = true;
     }
     const uint64_t *elu = a.elems + (int64_t)u * a.n;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int t = wid; t < nt; t += NT / 32) {       // a warp per segment
-      const uint32_t o = segstart[t], len = (t + 1 < nt ? segstart[t + 1] : s) - o;
-      const uint64_t *sp = elu + (int64_t)t * MSM_TILE + seglo[t];
-      for (uint32_t i = lane; i < len; i += 32) dst[o + i] = sp[i];
+    if (threadIdx.x == 0) segstart[nt] = s;
+    __syncthreads();
+    // flattened gather: every row of the bucket is one independent load
+    // (segment found by binary search over the smem segment starts)
+    for (uint32_t i = threadIdx.x; i < s; i += NT) {
+      uint32_t lo = 0, hi = (uint32_t)nt;   // t with segstart[t] <= i < segstart[t+1]
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (segstart[mid] <= i) lo = mid; else hi = mid;
+      }
+      dst[i] = elu[(int64_t)lo * MSM_TILE + seglo[lo] + (i - segstart[lo])];
     }
     __syncthreads();
     src = dst;
