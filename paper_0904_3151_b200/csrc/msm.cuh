@@ -799,15 +799,20 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
     const uint64_t *elu = a.elems + (int64_t)u * a.n;
     if (threadIdx.x == 0) segstart[nt] = s;
     __syncthreads();
-    // flattened gather: every row of the bucket is one independent load
-    // (segment found by binary search over the smem segment starts)
-    for (uint32_t i = threadIdx.x; i < s; i += NT) {
-      uint32_t lo = 0, hi = (uint32_t)nt;   // t with segstart[t] <= i < segstart[t+1]
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (segstart[mid] <= i) lo = mid; else hi = mid;
+    // gather: thread per tile segment (~MSM_TILE/B contiguous rows each);
+    // the unrolled loads of a segment are independent and issued together
+    for (int t = threadIdx.x; t < nt; t += NT) {
+      const uint32_t o = segstart[t], len = segstart[t + 1] - o;
+      const uint64_t *sp = elu + (int64_t)t * MSM_TILE + seglo[t];
+      uint32_t k = 0;
+      for (; k + 8 <= len; k += 8) {
+        uint64_t v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = sp[k + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dst[o + k + q] = v[q];
       }
-      dst[i] = elu[(int64_t)lo * MSM_TILE + seglo[lo] + (i - segstart[lo])];
+      for (; k < len; ++k) dst[o + k] = sp[k];
     }
     __syncthreads();
     src = dst;
