@@ -177,7 +177,7 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   // tile-local partition when every tile holds >= 4 rows per bucket and the
   // group kernel can stage the per-tile segment table
   l.ntiles = (int)((n + MSM_TILE - 1) / MSM_TILE);
-  l.tiled = env_int("EG_MSM_TILED", 1) && l.B * 4 <= MSM_TILE && l.ntiles <= 2048;
+  l.tiled = env_int("EG_MSM_TILED", 0) && l.B * 4 <= MSM_TILE && l.ntiles <= 2048;
   size_t b = 0;
   b += ws_bytes((size_t)l.U * l.B, 4);            // counts
   b += ws_bytes((size_t)l.U * (l.B + 1), 4);      // starts

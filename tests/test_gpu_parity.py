@@ -379,11 +379,11 @@ def test_tc_projection_error_band(eg, oracle, n, dim, length, reps):
         np.testing.assert_array_equal(codes[h].cpu().numpy().view(np.uint64), want)
 
 
-@pytest.mark.parametrize("env", [{"EG_MSM_TILED": "0"}, {"EG_MSM_STREAMS": "1"},
-                                 {"EG_MSM_TILED": "0", "EG_MSM_STREAMS": "1"}])
+@pytest.mark.parametrize("env", [{"EG_MSM_TILED": "1"}, {"EG_MSM_STREAMS": "1"},
+                                 {"EG_MSM_TILED": "1", "EG_MSM_STREAMS": "1"}])
 def test_msm_launch_variants(eg, oracle, manifest, monkeypatch, env):
-    """The classic (global histogram + scatter) partition and the single-stream
-    schedule give the same pair sets as the defaults."""
+    """The tile-local partition (k_msm_tsort) and the single-stream schedule
+    give the same pair sets as the defaults."""
     from paper_0904_3151_b200 import workloads
     for k, v in env.items():
         monkeypatch.setenv(k, v)
