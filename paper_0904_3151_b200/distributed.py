@@ -123,14 +123,16 @@ def gather_edges(keys, dists, world, rank, ops, n):
     return ops.merge(ks, ds, n)
 
 
-def build_step(x, params, metric: str, world: int, rank: int, ops=None):
+def build_step(x, params, metric: str, world: int, rank: int, ops=None,
+               force_dist: bool = False):
     """One full build of ``x`` (resident rows) on ``world`` ranks.
 
     Returns a dict with rank 0's merged ``keys``/``dist`` (None on other
-    ranks) and this rank's counters."""
+    ranks) and this rank's counters.  ``force_dist`` runs the sharded code
+    path (collectives included) even for a single rank (tests)."""
     ops = ops or DeviceOps()
     n = x.shape[0]
-    if world == 1:
+    if world == 1 and not force_dist:
         from .pipeline import build_graph_device
         out = build_graph_device(x, params, metric=metric)
         return {"keys": out["keys"], "dist": out["dist"], "info": out["info"]}

@@ -395,3 +395,30 @@ def test_msm_launch_variants(eg, oracle, manifest, monkeypatch, env):
         c = case["case"]
         pool = eg.BitStringPool(g[f"words_{c}"], case["length"]).partitioned(case["k"])
         np.testing.assert_array_equal(eg.enumerate_pairs(pool, case["d"]).array, g[f"pairs_{c}"])
+
+
+def test_sharded_path_over_nccl_single_rank(eg, oracle):
+    """The multi-GPU code path (row-sharded projection, NCCL all-gathers of
+    codes/norms, unit ownership, edge gather + device merge) on one rank."""
+    import socket
+    import torch
+    import torch.distributed as tdist
+    from paper_0904_3151_b200 import distributed, workloads
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                             world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        x = workloads.cfg1_points(6000, clusters=60)
+        params = eg.MsmParams(0.1, 1e-6, 32, 2, 8, 2, 0)
+        res = distributed.build_step(torch.from_numpy(x).cuda(), params, "cosine", 1, 0,
+                                     force_dist=True)
+        ref = oracle.build_graph(x, 0.1, 32, 2, 8, 2, 0)
+        from paper_0904_3151_b200 import engine
+        pairs = engine.keys_to_pairs(res["keys"].cpu().numpy())
+        np.testing.assert_array_equal(pairs, ref.pairs)
+        np.testing.assert_allclose(res["dist"].cpu().numpy(), ref.distances, rtol=0, atol=1e-12)
+    finally:
+        tdist.destroy_process_group()
