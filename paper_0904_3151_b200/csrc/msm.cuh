@@ -524,12 +524,31 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     if (i < s && !(cand >> j & 1) && F[(uint32_t)(e[j] >> 32) >> (32 - FSB)] == 0xfffe)
       cand |= 1u << j;
   }
-  if (cand) atomicAdd(&S.ncand, (uint32_t)__popc(cand));
-  __syncthreads();
-  const uint32_t ncand = S.ncand;
-  if (ncand == 0) {
+  // compact the candidates to the front of the CTA (dense registers): the
+  //    sparse phases below then run ceil(ncand/NT) iterations, not PT
+  uint32_t ncand;
+  {
+    uint32_t coff = block_exclusive_scan<NT>((uint32_t)__popc(cand), ncand,
+                                             reinterpret_cast<uint32_t *>(S.sw));
+    if (ncand == 0) {
+      __syncthreads();
+      return true;
+    }
+    uint64_t *clist = reinterpret_cast<uint64_t *>(S.big);   // F is dead now
+#pragma unroll
+    for (int j = 0; j < PT; ++j)
+      if (cand >> j & 1) clist[coff++] = e[j];
     __syncthreads();
-    return true;
+    cand = 0;
+#pragma unroll
+    for (int j = 0; j < PT; ++j) {
+      const uint32_t i = threadIdx.x + j * NT;
+      if (i < ncand) {
+        e[j] = clist[i];
+        cand |= 1u << j;
+      }
+    }
+    __syncthreads();
   }
   const uint32_t T = pow2_at_least(2 * ncand);
   for (uint32_t i = threadIdx.x * 2; i < T; i += NT * 2)
