@@ -205,16 +205,24 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
   // (bucket << 13) | rank: B <= 2^14, rank < MSM_TILE = 2^13
   static_assert(MSM_TILE <= (1 << 13) && MSM_MAX_LGB <= 19, "br packing");
   uint32_t br[IPT], h2[IPT];
+  {
+    // all code loads first (the smem atomics below would otherwise
+    // serialise one load latency per item)
+    uint64_t c[IPT][W];
 #pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
-    if (row < a.n) {
-      uint64_t c[W];
-      load_code<W>(codes, row, c);
-      const uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
-      const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
-      h2[i] = (uint32_t)h;
-      br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
+    for (int i = 0; i < IPT; ++i) {
+      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+      if (row < a.n) load_code<W>(codes, row, c[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+      if (row < a.n) {
+        const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
+        const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
+        h2[i] = (uint32_t)h;
+        br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
+      }
     }
   }
   __syncthreads();
@@ -299,16 +307,24 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_tsort(const __grid_constan
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
   constexpr int IPT = MSM_TILE / MSM_SC_NT;
   uint32_t br[IPT], h2[IPT];
+  {
+    // all code loads first (the smem atomics below would otherwise
+    // serialise one load latency per item)
+    uint64_t c[IPT][W];
 #pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
-    if (row < a.n) {
-      uint64_t c[W];
-      load_code<W>(codes, row, c);
-      const uint64_t h = hash_key<W>(c, (const uint64_t *)kept, salt);
-      const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
-      h2[i] = (uint32_t)h;
-      br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
+    for (int i = 0; i < IPT; ++i) {
+      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+      if (row < a.n) load_code<W>(codes, row, c[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
+      if (row < a.n) {
+        const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
+        const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
+        h2[i] = (uint32_t)h;
+        br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
+      }
     }
   }
   __syncthreads();
