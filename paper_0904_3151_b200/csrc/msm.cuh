@@ -1019,13 +1019,14 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
               my_raw += v > 0;
               my_new += v == 2;
               emit = v == 2;
-              if (emit) {
-                unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
-                if (slot < a.out_cap) {
-                  a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-                  if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
-                }
-              }
+            }
+          }
+          {  // warp-aggregated emission (one global atomic per warp step)
+            const uint32_t rb = (uint32_t)f;
+            const unsigned long long slot = warp_append(emit, &a.ctr[0]);
+            if (emit && slot < a.out_cap) {
+              a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+              if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
             }
           }
         }
