@@ -845,7 +845,7 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   unsigned long long *bad = ar.take<unsigned long long>(1);
   if (!flags || !dist || !bad) return EG_ERR_WORKSPACE;
   EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 8, st));
-  unsigned grid = (unsigned)std::min<int64_t>((m + 31) / 32, (int64_t)num_sms() * 64);
+  unsigned grid = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)num_sms() * 64);
   {
   EG_PROF(PC_VERIFY, st);
   if (x_is_f64)

@@ -53,55 +53,29 @@ __global__ void __launch_bounds__(256) k_verify(const TX *__restrict__ x, int64_
                                                 uint8_t *__restrict__ flags,
                                                 double *__restrict__ dist,
                                                 unsigned long long *__restrict__ bad) {
-  // Four pairs per warp per step: their row loads are independent and in
-  // flight together (ILP); each pair keeps the fixed lane mapping and the
-  // fixed butterfly, so its distance does not depend on the grouping.
-  constexpr int PP = 4;
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
   const int64_t warps = (int64_t)gridDim.x * 8;
-  for (int64_t p0 = gw * PP; p0 < m; p0 += warps * PP) {
-    double acc[PP];
-    int64_t ii[PP], jj[PP];
-    bool ok[PP];
-#pragma unroll
-    for (int k = 0; k < PP; ++k) {
-      const int64_t p = p0 + k;
-      acc[k] = 0.0;
-      ok[k] = false;
-      if (p < m) {
-        const uint64_t key = keys[p];
-        ii[k] = (int64_t)(key >> 32);
-        jj[k] = (int64_t)(key & 0xffffffffu);
-        ok[k] = ii[k] < n && jj[k] < n;
-        if (!ok[k] && lane == 0) {
-          atomicMin(bad, (unsigned long long)p);
-          flags[p] = 0;
-          dist[p] = 0.0;
-        }
-      }
+  for (int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); p < m; p += warps) {
+    const uint64_t key = keys[p];
+    const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+    if (!(i < n && j < n)) {
+      if (lane == 0) { atomicMin(bad, (unsigned long long)p); flags[p] = 0; dist[p] = 0.0; }
+      continue;
     }
+    double acc = 0.0;
+    accum_pair<TX>(x + i * dim, x + j * dim, dim, lane, metric, acc);
 #pragma unroll
-    for (int k = 0; k < PP; ++k)
-      if (ok[k]) accum_pair<TX>(x + ii[k] * dim, x + jj[k] * dim, dim, lane, metric, acc[k]);
-#pragma unroll
-    for (int k = 0; k < PP; ++k) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
-    }
-#pragma unroll
-    for (int k = 0; k < PP; ++k) {
-      if (lane == k && ok[k]) {   // lane k finishes pair k
-        double dd;
-        if (metric == EG_METRIC_COSINE) {
-          dd = 1.0 - acc[k] / (norms[ii[k]] * norms[jj[k]]);
-          dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
-        } else {
-          dd = sqrt(acc[k]);
-        }
-        dist[p0 + k] = dd;
-        flags[p0 + k] = dd <= eps;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      double dd;
+      if (metric == EG_METRIC_COSINE) {
+        dd = 1.0 - acc / (norms[i] * norms[j]);
+        dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
+      } else {
+        dd = sqrt(acc);
       }
+      dist[p] = dd;
+      flags[p] = dd <= eps;
     }
   }
 }
