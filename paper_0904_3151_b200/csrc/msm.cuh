@@ -757,10 +757,19 @@ __device__ __forceinline__ bool spill_for_tiles(uint32_t tag, uint32_t s, uint32
 }
 
 template <int W>
+#ifndef EG_SMALL_CAP
+#define EG_SMALL_CAP 2048
+#endif
+#ifndef EG_SMALL_NT
+#define EG_SMALL_NT 256
+#endif
+#ifndef EG_SMALL_MINCTAS
+#define EG_SMALL_MINCTAS 4
+#endif
 struct SmallCfg {               // one CTA per bucket, several CTAs per SM
-  static constexpr int CAP = W <= 2 ? 2048 : 1024;
-  static constexpr int NT = 256;
-  static constexpr int MIN_CTAS = 4;
+  static constexpr int CAP = W <= 2 ? EG_SMALL_CAP : EG_SMALL_CAP / 2;
+  static constexpr int NT = EG_SMALL_NT;
+  static constexpr int MIN_CTAS = EG_SMALL_MINCTAS;
   static constexpr int MDIV = EG_SMALL_MDIV;
 };
 template <int W>
