@@ -123,6 +123,28 @@ void eg_debug_set_tc_dump(float *d_buf);
 /* [2+replicates+h] new pairs of replicate h (0 when deferred).           */
 /* --------------------------------------------------------------------- */
 size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates);
+
+/* --------------------------------------------------------------------- */
+/* Block-count plan for eg_msm_pairs.  The pair set the units emit is     */
+/* {(i,j): popcount(c_i^c_j) <= d}, independent of the block count        */
+/* (hamming_join.py:300-375), so the count is a cost knob:    */
+/* C(k',d) units of n rows each vs. the in-group pairs visited.  Samples  */
+/* up to 8192 rows of d_codes (replicate 0, n x W), counts sum C(g,2)     */
+/* and the largest group for probe masks of every k' in (d, min(L,64)],   */
+/* and returns in *h_k_out the k' minimising the modelled cost (k itself  */
+/* unless another is >= 5% cheaper).  k is always returned when the       */
+/* reference's oversized-group warning (largest group > fraction * n,     */
+/* hamming_join.py:341-348) could fire on the reference blocks, when      */
+/* n < 65536, or when C(k,d) > 4096.  Blocks of every k' follow the       */
+/* reference partition (first L % k' blocks one bit wider).  Synchronous. */
+/* h_cost (optional, 2 doubles): modelled ms of the chosen and of k.      */
+/* EG_MSM_BLOCKS env: >0 forces that k', <0 forces k.                      */
+/* --------------------------------------------------------------------- */
+size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d);
+int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k,
+                int32_t d, double oversized_fraction, int32_t *h_k_out,
+                double *h_cost, void *d_workspace, size_t workspace_bytes,
+                void *stream);
 int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
                  int32_t replicates, const int32_t *h_block_bounds, int32_t k,
                  int32_t d, const int32_t *h_unit_rep, const uint64_t *h_unit_mask,

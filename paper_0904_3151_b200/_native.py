@@ -66,6 +66,8 @@ def _declare(lib):
         "eg_project_workspace": ([i64, i32, i32, i32], sz),
         "eg_project": ([P, I, i64, i32, P, P, P, i32, i32, P, P, sz, P, P], I),
         "eg_msm_workspace": ([i64, i32, i32], sz),
+        "eg_msm_plan_workspace": ([i32, i32, i32], sz),
+        "eg_msm_plan": ([P, i64, i32, i32, i32, dbl, P, P, P, sz, P], I),
         "eg_msm_pairs": ([P, i64, i32, i32, P, i32, i32, P, P, i64, P, P, i64, P, P, sz, P], I),
         "eg_xrep_filter": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),
         "eg_grouped_sort_workspace": ([i64, i32], sz),

@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "msm.cuh"
+#include "plan.cuh"
 #include "project.cuh"
 #include "project_tc.cuh"
 #include <cudaTypedefs.h>
@@ -555,6 +556,194 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   EG_LAUNCH_CHECK();
   if (d_fixups)
     EG_CUDA_TRY(cudaMemcpyAsync(d_fixups, cnt, 8, cudaMemcpyDeviceToDevice, st));
+  return EG_OK;
+}
+
+
+// ------------------------------------------------------------- MSM plan
+// Block count for eg_msm_pairs (see plan.cuh).  Blocks follow the
+// reference's partition rule (first length % k blocks one bit wider,
+// bitpool.py:44-69) for every candidate k'.
+static double comb_sat(int a, int b) {
+  double r = 1;
+  for (int i = 0; i < b; ++i) r = r * (a - i) / (i + 1);
+  return r;
+}
+
+static void plan_kept(int length, int kk, uint64_t dropped_blocks, uint64_t kept[4]) {
+  const int base = length / kk, rem = length % kk;
+  for (int w = 0; w < 4; ++w) kept[w] = 0;
+  int t = 0;
+  for (int b = 0; b < kk; ++b) {
+    const int wd = base + (b < rem ? 1 : 0);
+    for (int q = 0; q < wd; ++q, ++t)
+      if (!(dropped_blocks >> b & 1)) kept[t >> 6] |= 1ull << (t & 63);
+  }
+}
+
+static double env_double(const char *name, double dflt) {
+  const char *v = getenv(name);
+  return (v && *v) ? atof(v) : dflt;
+}
+
+constexpr int PLAN_REF_MAX = 4096;     // reference masks probed for the oversize check
+constexpr int PLAN_PER_K = 4;          // masks probed per candidate block count
+constexpr int PLAN_MIN_ROWS = 65536;   // smaller pools keep the reference blocks
+
+size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d) {
+  (void)length; (void)k; (void)d;
+  const size_t P = PLAN_REF_MAX + PLAN_PER_K * EG_MAX_BLOCKS;
+  return ws_bytes(P * 4, 8) + ws_bytes(P, 8) + ws_bytes(P, 4) + 1024;
+}
+
+int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, int32_t d,
+                double oversized_fraction, int32_t *h_k_out, double *h_cost, void *d_workspace,
+                size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!h_k_out) return arg_error("eg_msm_plan: h_k_out is null");
+  if (n < 1 || length < 1 || length > EG_MAX_LENGTH)
+    return arg_error("eg_msm_plan: need n >= 1 and 1 <= length <= 256");
+  if (!(0 <= d && d < k && k <= length) || k > EG_MAX_BLOCKS)
+    return arg_error("eg_msm_plan: need 0 <= d < k <= min(length, 64)");
+  *h_k_out = k;
+  if (h_cost) h_cost[0] = h_cost[1] = 0;
+  const int kmax = std::min(length, EG_MAX_BLOCKS);
+  const int forced = env_int("EG_MSM_BLOCKS", 0);
+  if (forced > 0) {
+    if (forced > d && forced <= kmax) *h_k_out = forced;
+    return EG_OK;
+  }
+  if (forced < 0 || n < PLAN_MIN_ROWS) return EG_OK;
+  const double nref = comb_sat(k, d);
+  if (nref > PLAN_REF_MAX) return EG_OK;
+  const int W = (length + 63) / 64;
+  const int S = (int)std::min<int64_t>(n, PLAN_SAMPLE);
+  // probes: every reference mask (oversize check), then PLAN_PER_K masks of
+  // every candidate block count
+  std::vector<uint64_t> kept;
+  std::vector<int> probe_k;
+  auto add = [&](int kk, uint64_t dropped) {
+    uint64_t kw[4];
+    plan_kept(length, kk, dropped, kw);
+    kept.insert(kept.end(), kw, kw + 4);
+    probe_k.push_back(kk);
+  };
+  {
+    std::vector<int> c(d);
+    for (int i = 0; i < d; ++i) c[i] = i;
+    while (true) {
+      uint64_t m = 0;
+      for (int i = 0; i < d; ++i) m |= 1ull << c[i];
+      add(k, m);
+      probe_k.back() = -1;     // reference probe: oversize check only
+      int i = d - 1;
+      while (i >= 0 && c[i] == k - d + i) --i;
+      if (i < 0) break;
+      ++c[i];
+      for (int j = i + 1; j < d; ++j) c[j] = c[j - 1] + 1;
+    }
+  }
+  const int nref_probes = (int)probe_k.size();
+  for (int kk = d + 1; kk <= kmax; ++kk) {
+    const double units = comb_sat(kk, d);
+    if (units > 8192) break;
+    if (units <= PLAN_PER_K) {
+      std::vector<int> c(d);
+      for (int i = 0; i < d; ++i) c[i] = i;
+      while (true) {
+        uint64_t m = 0;
+        for (int i = 0; i < d; ++i) m |= 1ull << c[i];
+        add(kk, m);
+        int i = d - 1;
+        while (i >= 0 && c[i] == kk - d + i) --i;
+        if (i < 0) break;
+        ++c[i];
+        for (int j = i + 1; j < d; ++j) c[j] = c[j - 1] + 1;
+      }
+    } else {
+      uint64_t rng = 0x9e3779b97f4a7c15ULL * (uint64_t)(kk + 1);
+      std::vector<uint64_t> seen;
+      while ((int)seen.size() < PLAN_PER_K) {
+        uint64_t m = 0;
+        int cnt = 0;
+        while (cnt < d) {   // random d-subset of [0, kk)
+          rng = rng * 6364136223846793005ULL + 1442695040888963407ULL;
+          const int b = (int)((rng >> 33) % (uint64_t)kk);
+          if (!(m >> b & 1)) { m |= 1ull << b; ++cnt; }
+        }
+        if (std::find(seen.begin(), seen.end(), m) != seen.end()) continue;
+        seen.push_back(m);
+        add(kk, m);
+      }
+    }
+  }
+  const int P = (int)probe_k.size();
+  Arena ar(d_workspace, workspace_bytes);
+  unsigned long long *d_kept = ar.take<unsigned long long>((size_t)P * 4);
+  unsigned long long *d_pairs = ar.take<unsigned long long>((size_t)P);
+  uint32_t *d_max = ar.take<uint32_t>((size_t)P);
+  if (!d_kept || !d_pairs || !d_max) {
+    set_error("eg_msm_plan: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
+  EG_CUDA_TRY(cudaMemcpyAsync(d_kept, kept.data(), (size_t)P * 32, cudaMemcpyHostToDevice, st));
+  const size_t smem = (size_t)PLAN_TABLE * 12;
+  {
+    EG_PROF(PC_MISC, st);
+#define EG_PLAN_CASE(WW)                                                                     \
+  case WW:                                                                                   \
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_plan<WW>,                                         \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    k_msm_plan<WW><<<P, PLAN_NT, smem, st>>>(d_codes, n, S, d_kept, d_pairs, d_max);         \
+    break;
+    switch (W) {
+      EG_PLAN_CASE(1)
+      EG_PLAN_CASE(2)
+      EG_PLAN_CASE(3)
+      EG_PLAN_CASE(4)
+    }
+#undef EG_PLAN_CASE
+  }
+  EG_LAUNCH_CHECK();
+  std::vector<unsigned long long> pairs(P);
+  std::vector<uint32_t> mx(P);
+  EG_CUDA_TRY(cudaMemcpyAsync(pairs.data(), d_pairs, (size_t)P * 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaMemcpyAsync(mx.data(), d_max, (size_t)P * 4, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  // oversize check on the reference blocks: keep them whenever the
+  // reference's warning (largest group > fraction * n) could fire, so the
+  // caller's max_group is the reference's own
+  uint32_t rmax = 0;
+  for (int p = 0; p < nref_probes; ++p) rmax = std::max(rmax, mx[p]);
+  if (S == n) {
+    if (n > 16 && rmax > oversized_fraction * (double)n) return EG_OK;
+  } else if (oversized_fraction * S < 200 || rmax >= 0.5 * oversized_fraction * S) {
+    return EG_OK;
+  }
+  const double ce = env_double("EG_PLAN_CE_PS", 18.5) * 1e-12;   // per row per unit
+  const double cp = env_double("EG_PLAN_CP_PS", 4.0) * 1e-12;    // per visited pair
+  const double scale = S > 1 ? (double)n * (double)(n - 1) / ((double)S * (double)(S - 1)) : 0;
+  double best = -1, ref_cost = -1;
+  int best_k = k;
+  for (int p = nref_probes; p < P;) {
+    const int kk = probe_k[p];
+    double sum = 0;
+    int cnt = 0;
+    for (; p < P && probe_k[p] == kk; ++p, ++cnt) sum += (double)pairs[p];
+    const double est_pairs = sum / cnt * scale;
+    const double cost = comb_sat(kk, d) * ((double)n * ce + est_pairs * cp);
+    if (kk == k) ref_cost = cost;
+    if (best < 0 || cost < best) {
+      best = cost;
+      best_k = kk;
+    }
+  }
+  if (ref_cost >= 0 && best >= 0.95 * ref_cost) best_k = k;   // not worth a change
+  *h_k_out = best_k;
+  if (h_cost) {
+    h_cost[0] = (best_k == k ? ref_cost : best) * 1e3;
+    h_cost[1] = ref_cost * 1e3;
+  }
   return EG_OK;
 }
 

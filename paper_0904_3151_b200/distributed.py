@@ -8,7 +8,9 @@ with disjoint outputs and no cross-rank dedup.
     1. rows are split into equal shards; each rank projects its shard
        (eg_project) and computes its row norms (eg_row_stats);
     2. codes and norms are all-gathered over NVLink (NCCL all_gather);
-    3. units are assigned cyclically (unit u -> rank u % world), each rank
+    3. the block count is planned on the gathered codes (eg_msm_plan,
+       deterministic, so every rank agrees without a collective), units are
+       assigned cyclically (unit u -> rank u % world), each rank
        runs eg_msm_pairs on its units, sorts and verifies its candidates
        (rows are resident on every rank for the verify gathers);
     4. per-rank sorted edge runs are gathered to rank 0 and merged by one
@@ -50,10 +52,15 @@ class DeviceOps:
                                         list(range(1, params.replicates + 1)))
         return codes
 
-    def candidates(self, codes, params, units):
+    def plan(self, codes, params):
+        """Block count of the units (deterministic in the codes, so every
+        rank holding the gathered codes picks the same one)."""
+        return engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
+
+    def candidates(self, codes, params, units, blocks):
         from .bitpool import block_partition
-        bounds = block_partition(params.length, params.blocks)
-        reps, masks = engine.units_for(range(params.replicates), params.blocks, params.mismatch)
+        bounds = block_partition(params.length, blocks)
+        reps, masks = engine.units_for(range(params.replicates), blocks, params.mismatch)
         sel = np.asarray(units, dtype=np.int64)
         keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch,
                                       reps[sel], masks[sel])
@@ -142,9 +149,10 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
     codes_s = ops.project(xs, norms_s, params)
     codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
     from math import comb
-    units = my_units(params.replicates * comb(params.blocks, params.mismatch), world, rank)
-    from .pipeline import lsh_radius  # noqa: F401  (metric mapping lives there)
-    keys, info = ops.candidates(codes, params, units)
+    blocks = ops.plan(codes, params)
+    units = my_units(params.replicates * comb(blocks, params.mismatch), world, rank)
+    keys, info = ops.candidates(codes, params, units, blocks)
+    info = dict(info, blocks=blocks)
     keys = ops.sort(keys, n)
     ek, ed = ops.verify(x, norms, keys, metric, params.epsilon)
     mk, md = gather_edges(ek, ed, world, rank, ops, n)
@@ -155,11 +163,13 @@ def hamming_step(codes, params, world: int, rank: int):
     """Config 2: enumerate_pairs over resident words, units sharded."""
     from .bitpool import block_partition
     n = codes.shape[1]
-    bounds = block_partition(params.length, params.blocks)
-    reps, masks = engine.units_for([0], params.blocks, params.mismatch)
+    blocks = engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
+    bounds = block_partition(params.length, blocks)
+    reps, masks = engine.units_for([0], blocks, params.mismatch)
     sel = np.asarray(my_units(len(reps), world, rank), dtype=np.int64)
     keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, reps[sel],
                                   masks[sel])
+    info["blocks"] = blocks
     engine.sort_pair_keys(keys, n)
     if world > 1:
         dummy = torch.zeros(keys.numel(), dtype=torch.float64, device=keys.device)
@@ -174,4 +184,4 @@ def last_counts(res):
     keys = res.get("keys")
     return {"candidates": info.get("emitted"), "raw": info.get("raw"), "new": info.get("new"),
             "edges": int(keys.numel()) if keys is not None else None,
-            "max_group": info.get("max_group")}
+            "max_group": info.get("max_group"), "blocks": info.get("blocks")}

@@ -144,6 +144,32 @@ def units_for(replicates, k: int, d: int):
     return np.asarray(reps, dtype=np.int32), np.asarray(bits, dtype=np.uint64)
 
 
+def msm_plan(codes: torch.Tensor, length: int, k: int, d: int,
+             oversized_fraction: float = 0.25) -> int:
+    """Block count the MSM units run with (``eg_msm_plan``).
+
+    The emitted pair set does not depend on it (hamming_join.py:300-375), so
+    the library picks the count with the lowest modelled cost on a sample
+    of replicate 0's codes; it returns ``k`` itself whenever the reference's
+    oversized-group warning could fire on the reference blocks, so
+    ``max_group`` keeps the reference's meaning where it matters."""
+    reps, n, W = codes.shape
+    if n == 0:
+        return k
+    lib = _native.lib()
+    ws = _ws(lib.eg_msm_plan_workspace(length, k, d), codes.device)
+    out = ctypes.c_int32(k)
+    cost = (ctypes.c_double * 2)()
+    check(lib.eg_msm_plan(_p(codes), n, length, k, d, float(oversized_fraction),
+                          ctypes.addressof(out), ctypes.addressof(cost), _p(ws), ws.numel(),
+                          _stream(codes.device)), "msm_plan")
+    _last_plan.update(k=k, chosen=int(out.value), cost_ms=float(cost[0]), ref_ms=float(cost[1]))
+    return int(out.value)
+
+
+_last_plan: dict = {}
+
+
 def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps, unit_masks,
               capacity: int | None = None):
     """Run the MSM units; returns (keys tensor, counts dict)."""

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import engine
-from .bitpool import BitStringPool, block_mask_bits, validate_mask
+from .bitpool import BitStringPool, block_mask_bits, block_partition, validate_mask
 
 __all__ = ["PairSet", "SortScratch", "enumerate_pairs", "grouped_radix_sort", "mask_count"]
 
@@ -142,8 +142,11 @@ def enumerate_pairs(pool: BitStringPool, d: int, chunk_bits: int = 16,
     scratch.check(n, chunk_bits)
     dev = engine.require_device(device)
     codes = _codes_on_device(pool, dev)
-    reps, bits = engine.units_for([0], k, d)
-    keys, info = engine.msm_pairs(codes, pool.length, pool.block_bounds, d, reps, bits)
-    warn_oversized(info["max_group"], n, oversized_fraction)
+    kk = engine.msm_plan(codes, pool.length, k, d, oversized_fraction)
+    bounds = pool.block_bounds if kk == k else block_partition(pool.length, kk)
+    reps, bits = engine.units_for([0], kk, d)
+    keys, info = engine.msm_pairs(codes, pool.length, bounds, d, reps, bits)
+    if kk == k:      # else the plan ruled the warning out on the reference blocks
+        warn_oversized(info["max_group"], n, oversized_fraction)
     engine.sort_pair_keys(keys, n)
     return PairSet(engine.keys_to_pairs(keys.cpu().numpy()), assume_normalized=True)

@@ -101,13 +101,16 @@ def lsh_radius(params: MsmParams, metric: str) -> float:
 
 
 def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cosine",
-                       units=None, norms: torch.Tensor | None = None, codes=None):
+                       units=None, norms: torch.Tensor | None = None, codes=None,
+                       blocks: int | None = None):
     """Build with rows already resident on the device.
 
     Returns a dict of device tensors (``keys`` sorted uint64 pair keys,
     ``dist`` float64) plus counters and per-stage CUDA-event timings.
     ``units`` (optional) restricts the (replicate, mask) units, used by the
     multi-GPU driver; ``codes`` lets a caller pass pre-gathered codes.
+    ``blocks`` is the block count the units use (default: ``eg_msm_plan``'s
+    choice; the pair set is the same for every count).
     """
     dev = x.device
     n = x.shape[0]
@@ -122,12 +125,15 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
         codes, fix = engine.project_codes(x, norms, params.length, params.seed,
                                           list(range(1, params.replicates + 1)))
     ev[1].record()
-    bounds = _bounds(params.length, params.blocks)
+    if blocks is None:
+        blocks = engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
+    bounds = _bounds(params.length, blocks)
     if units is None:
-        ureps, umasks = engine.units_for(range(params.replicates), params.blocks, params.mismatch)
+        ureps, umasks = engine.units_for(range(params.replicates), blocks, params.mismatch)
     else:
         ureps, umasks = units
     keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, ureps, umasks)
+    info["blocks"] = blocks
     if bad is not None:
         engine.raise_bad_rows(bad)
     ev[2].record()
@@ -190,7 +196,8 @@ def build_graph(data, params: MsmParams, *, threads: int | None = None, chunk_bi
         keys = out["keys"].cpu().numpy()
         dist = out["dist"].cpu().numpy()
         info = out["info"]
-        warn_oversized(info["max_group"], n, 0.25)
+        if info["blocks"] == params.blocks:   # else the plan ruled the warning out
+            warn_oversized(info["max_group"], n, 0.25)
         timings = _event_timings(out["events"], 0.0)
     edges = EdgeList(engine.keys_to_pairs(keys), dist)
     timings["total_s"] = time.perf_counter() - t0

@@ -31,9 +31,10 @@ def _free_port():
 class OracleOps:
     """CPU stand-ins for DeviceOps, built on the oracle."""
 
-    def __init__(self, orc, x_full):
+    def __init__(self, orc, x_full, blocks=None):
         self.orc = orc
         self.x = np.asarray(x_full)
+        self.blocks = blocks
 
     def norms(self, xs):
         return torch.from_numpy(np.sqrt((xs.numpy().astype(np.float64) ** 2).sum(axis=1)))
@@ -43,15 +44,19 @@ class OracleOps:
                  for h in range(params.replicates)]
         return torch.from_numpy(np.stack(codes).view(np.int64))
 
-    def candidates(self, codes, params, units):
+    def plan(self, codes, params):
+        # the block count is a cost knob: any k' > d gives the same pairs
+        return self.blocks or params.blocks
+
+    def candidates(self, codes, params, units, blocks):
         """Pairs owned by `units`: owner = (replicate, canonical mask of the
         differing blocks) -- the rule the CUDA kernels implement."""
         orc = self.orc
         words = [c.numpy().view(np.uint64) for c in codes]
-        bounds = orc.block_partition(params.length, params.blocks)
-        masks = list(itertools.combinations(range(params.blocks), params.mismatch))
+        bounds = orc.block_partition(params.length, blocks)
+        masks = list(itertools.combinations(range(blocks), params.mismatch))
         blk = np.zeros(params.length, dtype=np.int64)
-        for b in range(params.blocks):
+        for b in range(blocks):
             blk[bounds[b]:bounds[b + 1]] = b
         mine = set(units)
         keys = []
@@ -61,7 +66,7 @@ class OracleOps:
             for (i, j) in pairs[keep]:
                 x = int(words[h][i, 0] ^ words[h][j, 0])
                 delta = sorted({int(blk[t]) for t in range(params.length) if x >> t & 1})
-                fill = [b for b in range(params.blocks) if b not in delta]
+                fill = [b for b in range(blocks) if b not in delta]
                 canon = tuple(sorted(delta + fill[:params.mismatch - len(delta)]))
                 unit = h * len(masks) + masks.index(canon)
                 if unit in mine:
@@ -84,7 +89,7 @@ class OracleOps:
         return keys[order], dists[order]
 
 
-def _worker(rank, world, port, out_path):
+def _worker(rank, world, port, out_path, blocks=None):
     import sys
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -96,16 +101,19 @@ def _worker(rank, world, port, out_path):
     params = eg.MsmParams(epsilon=0.05, gamma=1e-3, length=24, mismatch=2, blocks=4,
                           replicates=3, seed=7)
     res = distributed.build_step(torch.from_numpy(x), params, "cosine", world, rank,
-                                 ops=OracleOps(orc, x))
+                                 ops=OracleOps(orc, x, blocks))
     if rank == 0:
         np.savez(out_path, keys=res["keys"].numpy(), dist=res["dist"].numpy())
     tdist.barrier()
     tdist.destroy_process_group()
 
 
-def test_two_rank_build_equals_single_process(oracle, tmp_path):
+@pytest.mark.parametrize("blocks", [None, 3, 6])
+def test_two_rank_build_equals_single_process(oracle, tmp_path, blocks):
+    """Sharded build == single-process reference, for the reference block
+    count and for planned counts k' != k (the pair set is independent of k)."""
     out = str(tmp_path / "merged.npz")
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, blocks), nprocs=2, join=True)
     got = np.load(out)
     from paper_0904_3151_b200 import workloads
     x = workloads.planted_clusters(400, 8, 8, 20, 0.03, 5)

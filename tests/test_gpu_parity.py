@@ -422,3 +422,67 @@ def test_sharded_path_over_nccl_single_rank(eg, oracle):
         np.testing.assert_allclose(res["dist"].cpu().numpy(), ref.distances, rtol=0, atol=1e-12)
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("blocks", [4, 5, 7, 9, 16, 48])
+def test_forced_block_counts_same_pairs(eg, oracle, manifest, monkeypatch, blocks):
+    """The pair set does not depend on the block count the units run with
+    (hamming_join.py:300-375): every forced k' > d reproduces the
+    reference-k pairs, per-replicate raw/new counts and edges."""
+    monkeypatch.setenv("EG_MSM_BLOCKS", str(blocks))
+    rng = np.random.default_rng(blocks)
+    n, length, k, d = 5000, 48, 12, 3
+    base = (rng.random((n // 3, length)) < 0.3).astype(np.uint8)
+    bits = base[rng.integers(0, base.shape[0], n)] ^ (rng.random((n, length)) < 0.02)
+    words = pack_bits(bits.astype(np.uint8))
+    pool = eg.BitStringPool(words, length).partitioned(k)
+    got = eg.enumerate_pairs(pool, d)
+    want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+    np.testing.assert_array_equal(got.array, want)
+    g = golden("small_build")
+    rec = manifest["small_build"]
+    pp = rec["params"]
+    if pp["mismatch"] < blocks <= pp["length"]:
+        params = eg.MsmParams(epsilon=pp["epsilon"], gamma=1e-3, length=pp["length"],
+                              mismatch=pp["mismatch"], blocks=pp["blocks"],
+                              replicates=pp["replicates"], seed=pp["seed"])
+        graph = eg.build_graph(g["x"], params)
+        np.testing.assert_array_equal(graph.edge_list.pairs, g["edges"])
+        assert graph.stats.per_replicate_raw == tuple(rec["per_replicate_raw"])
+        assert graph.stats.per_replicate_new == tuple(rec["per_replicate_new"])
+        assert graph.stats.candidate_count == rec["candidate_count"]
+
+
+def test_block_plan_auto_large_pool(eg, oracle):
+    """Auto plan on a pool above the planning threshold (skewed bits, planted
+    near-duplicates): whatever k' the plan picks, pairs equal the oracle's."""
+    from paper_0904_3151_b200 import engine
+    rng = np.random.default_rng(11)
+    n, length, k, d = 120_000, 48, 12, 3
+    p1 = rng.uniform(0.05, 0.95, length)
+    bits = (rng.random((n, length)) < p1).astype(np.uint8)
+    src = rng.integers(0, n, n // 20)
+    dst = rng.integers(0, n, n // 20)
+    bits[dst] = bits[src] ^ (rng.random((len(src), length)) < 0.03)
+    words = pack_bits(bits)
+    pool = eg.BitStringPool(words, length).partitioned(k)
+    got = eg.enumerate_pairs(pool, d)
+    assert engine._last_plan["chosen"] > d
+    want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+    np.testing.assert_array_equal(got.array, want)
+
+
+def test_block_plan_keeps_reference_when_oversized(eg, caplog):
+    """Where the reference would warn about an oversized group, the plan
+    keeps the reference blocks, so the warning (and max_group) match."""
+    from paper_0904_3151_b200 import engine
+    rng = np.random.default_rng(5)
+    n, length = 70_000, 32
+    bits = (rng.random((n, length)) < 0.5).astype(np.uint8)
+    bits[: n // 3] = bits[0]                   # a third of the rows identical
+    pool = eg.BitStringPool(pack_bits(bits), length).partitioned(8)
+    with caplog.at_level(logging.WARNING, logger="paper_0904_3151_b200"):
+        codes_pairs = eg.enumerate_pairs(pool, 1)
+    assert engine._last_plan.get("chosen", 8) == 8
+    assert any("group" in r.message for r in caplog.records)
+    assert len(codes_pairs) >= (n // 3) * (n // 3 - 1) // 2
