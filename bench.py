@@ -87,12 +87,15 @@ def params_for(cfg, eg):
                         replicates=cfg.replicates, seed=cfg.seed)
 
 
-def sort_bytes_per_unit(n: int, cfg) -> int:
-    """B_sort = n (8W + P * 2 (kb + 4)), kb = P = ceil(kappa/8)."""
+def sort_bytes_per_unit(n: int, cfg, blocks: int | None = None) -> int:
+    """B_sort = n (8W + P * 2 (kb + 4)), kb = P = ceil(kappa/8),
+    kappa = masked-key bits of a unit under ``blocks`` blocks (the planned
+    block count; the reference's ``cfg.blocks`` by default)."""
+    k = blocks or cfg.blocks
     W = max(1, -(-cfg.length // 64))
-    base, rem = divmod(cfg.length, cfg.blocks)
-    # every config has equal blocks; kappa = length - d * block size (worst case)
-    kappa = cfg.length - sum(sorted([base + (1 if b < rem else 0) for b in range(cfg.blocks)])
+    base, rem = divmod(cfg.length, k)
+    # kappa = length - the d narrowest blocks (worst case over the masks)
+    kappa = cfg.length - sum(sorted([base + (1 if b < rem else 0) for b in range(k)])
                              [:cfg.mismatch])
     kb = -(-kappa // 8)
     return n * (8 * W + kb * 2 * (kb + 4))
@@ -107,8 +110,9 @@ class ClockSampler:
     was measured to stall this process's driver calls by ~100-400 ms per
     step on the box, so it is not used inside the timed region.)"""
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, mode: str = "thread"):
         self.index = index
+        self.mode = mode
         self.samples = []
         self.stop_flag = threading.Event()
         self.thread = None
@@ -124,8 +128,16 @@ class ClockSampler:
         except Exception as e:  # pragma: no cover
             self.err = str(e)
             return
-        self.thread = threading.Thread(target=self._run, daemon=True)
-        self.thread.start()
+        if self.mode == "thread":
+            self.thread = threading.Thread(target=self._run, daemon=True)
+            self.thread.start()
+
+    def sample(self):
+        """One sample from the calling thread (mode 'between')."""
+        if self.mode == "between" and self.err is None and hasattr(self, "h"):
+            nv = self.nv
+            self.samples.append((nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM),
+                                 nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
 
     def _run(self):
         nv = self.nv
@@ -139,11 +151,12 @@ class ClockSampler:
             self.stop_flag.wait(0.1)
 
     def stop(self):
-        if self.thread is None:
+        if self.thread is None and not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None,
                     "reasons": [f"nvml unavailable: {self.err}"]}
         self.stop_flag.set()
-        self.thread.join(timeout=2)
+        if self.thread is not None:
+            self.thread.join(timeout=2)
         nv = self.nv
         bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
                 "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
@@ -263,7 +276,7 @@ def main():
         step()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, os.environ.get("EG_BENCH_CLOCKS", "between"))
     clocks.start()
     prof = _native.Profile()
     l0 = _native.launch_count()
@@ -271,18 +284,26 @@ def main():
     if world > 1:
         tdist.barrier()
     torch.cuda.synchronize()
-    times = []
+    times, host_ms = [], []
     last = None
+    if os.environ.get("PYTHONGC") == "off":
+        import gc
+        gc.collect()
+        gc.disable()
     for _ in range(args.steps):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
         e0.record()
         last = step()
         e1.record()
         e1.synchronize()
+        host_ms.append((time.perf_counter() - t0) * 1e3)
         times.append(e0.elapsed_time(e1))
+        clocks.sample()
     print("step_ms", [round(t, 2) for t in times], file=sys.stderr, flush=True)
+    print("host_ms", [round(t, 2) for t in host_ms], file=sys.stderr, flush=True)
     torch.cuda.synchronize()
     if world > 1:
         tdist.barrier()
@@ -327,7 +348,9 @@ def main():
 
     # ------------------------------------------------------------ roofline
     peak, peak_kind = peaks()
-    units_total = cfg.replicates * math.comb(cfg.blocks, cfg.mismatch)
+    counts = distributed.last_counts(last) or {}
+    blocks = counts.get("blocks") or cfg.blocks
+    units_total = cfg.replicates * math.comb(blocks, cfg.mismatch)
     units_mine = len(distributed.my_units(units_total, world, rank))
     stage = kprof.get("msm_stage", {"ms": 0.0, "count": 0})
     roof = None
@@ -336,13 +359,14 @@ def main():
         # of the build through hist / scan / scatter / group / tiers
         units_per_launch = units_mine
         avg_ms = stage["ms"] / stage["count"]
-        alg = sort_bytes_per_unit(n, cfg) * units_per_launch
+        alg = sort_bytes_per_unit(n, cfg, blocks) * units_per_launch
         achieved = alg / (avg_ms / 1e3) / 1e9
         traffic = None
         try:
-            with open(os.path.join(ROOT, "profiles", "r1_traffic.json")) as f:
+            with open(os.path.join(ROOT, "profiles", "r1_traffic_planned.json")) as f:
                 tr = json.load(f).get(args.config)
-            if tr:   # measured DRAM bytes per 16-unit batch, scaled to the launch
+            if tr and tr.get("blocks", cfg.blocks) == blocks:
+                # measured DRAM bytes per 16-unit batch, scaled to the launch
                 traffic = tr["msm_batch_dram_bytes"] * units_per_launch / tr["units_per_batch"]
         except Exception:
             traffic = None
@@ -350,7 +374,7 @@ def main():
                           "over all units of the build",
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg),
+                "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg, blocks), "blocks": blocks,
                 "units_per_launch": units_per_launch, "avg_launch_ms": avg_ms}
     stage_ms = {k: v["ms"] / args.steps for k, v in kprof.items()}
 

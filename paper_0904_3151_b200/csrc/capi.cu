@@ -853,6 +853,19 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
           for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t)
             ub.kept[j][t >> 6] &= ~(1ull << (t & 63));
       ub.salt[j] = 0x2545f4914f6cdd1dULL * (uint64_t)(u0 + j + 1);
+      // tail blocks: masked blocks above the lowest kept block
+      int lowest_kept = 0;
+      while (lowest_kept < k && (mb >> lowest_kept & 1)) ++lowest_kept;
+      int nt = 0;
+      for (int b = lowest_kept + 1; b < k; ++b) {
+        if (!(mb >> b & 1)) continue;
+        if (nt < MSM_MAXT) {
+          ub.tail_lo[j][nt] = (uint16_t)h_block_bounds[b];
+          ub.tail_hi[j][nt] = (uint16_t)h_block_bounds[b + 1];
+        }
+        ++nt;
+      }
+      ub.ntail[j] = (uint8_t)std::min(nt, 255);
     }
     batches.push_back(ub);
   }

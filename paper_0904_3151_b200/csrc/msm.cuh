@@ -40,12 +40,20 @@ constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 14;         // at most 16384 buckets per unit
 constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to this B
 
+constexpr int MSM_MAXT = 8;             // tail blocks of the O(1) canonical test
+
 struct UnitBatch {
   int count;
   int rep[MSM_MAXU];
   unsigned long long maskbits[MSM_MAXU];
   unsigned long long kept[MSM_MAXU][4];
   unsigned long long salt[MSM_MAXU];
+  // Canonical-mask test without computing the mask (see canonical_tail_ok):
+  // the unit's masked blocks above its lowest kept block, as bit ranges
+  // [tail_lo, tail_hi); ntail > MSM_MAXT selects the general computation.
+  uint8_t ntail[MSM_MAXU];
+  uint16_t tail_lo[MSM_MAXU][MSM_MAXT];
+  uint16_t tail_hi[MSM_MAXU][MSM_MAXT];
 };
 
 struct MsmArgs {
@@ -391,13 +399,40 @@ __device__ __forceinline__ uint64_t canonical_mask(const uint64_t (&x)[W], const
   return delta;
 }
 
+// Canonical-mask test for a pair whose differing bits x all lie in the
+// unit's masked blocks M (x & kept == 0, so the differing-block set D is a
+// subset of M).  canonical(D) = D + the lowest d-|D| blocks outside D equals
+// M  iff  every block of M\D lies below the lowest kept block P  iff  every
+// block of M above P differs, i.e. x has a bit in each tail range.  O(|tail|)
+// word tests instead of a bit walk plus a fill loop.
+template <int W>
+__device__ __forceinline__ bool canonical_tail_ok(const uint64_t (&x)[W], const UnitBatch &ub,
+                                                  int u) {
+  const int nt = ub.ntail[u];
+  for (int t = 0; t < nt; ++t) {
+    const int lo = ub.tail_lo[u][t], hi = ub.tail_hi[u][t];
+    uint64_t any = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const int wl = max(lo - 64 * w, 0), wh = min(hi - 64 * w, 64);
+      if (wl < wh) {
+        const uint64_t m = (wh - wl == 64 ? ~0ull : ((1ull << (wh - wl)) - 1ull)) << wl;
+        any |= x[w] & m;
+      }
+    }
+    if (!any) return false;
+  }
+  return true;
+}
+
 // Full predicate for one in-group pair.  Returns 0 = rejected, 1 = raw only
 // (an earlier replicate owns it), 2 = emit.
 template <int W>
 __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint64_t (&cb)[W],
                                             uint32_t ra, uint32_t rb, const MsmArgs &a,
-                                            const unsigned long long *kept, uint64_t maskbits,
-                                            int rep, const uint8_t *b2b) {
+                                            const UnitBatch &ub, int u,
+                                            const unsigned long long *kept, int rep,
+                                            const uint8_t *b2b) {
   uint64_t x[W];
   int pc = 0;
   uint64_t keydiff = 0;
@@ -408,7 +443,11 @@ __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint6
     keydiff |= x[w] & kept[w];
   }
   if (keydiff || pc > a.d) return 0;
-  if (canonical_mask<W>(x, b2b, a.k, a.d) != maskbits) return 0;
+  if (ub.ntail[u] <= MSM_MAXT) {
+    if (!canonical_tail_ok<W>(x, ub, u)) return 0;
+  } else if (canonical_mask<W>(x, b2b, a.k, a.d) != ub.maskbits[u]) {
+    return 0;
+  }
   if (a.out_rep) return 2;
   for (int g = 0; g < rep; ++g) {
     const uint64_t *cg = a.codes + (int64_t)g * a.n * W;
@@ -466,7 +505,16 @@ struct HGroupSmem {
   uint32_t pp[GCAP + 1];     // pair prefix per group
   uint8_t b2b[EG_MAX_LENGTH];
   unsigned long long sw[NT / 32];
-  uint32_t nruns, maxrun, raw, neu, ncand;
+  uint32_t nruns, maxrun, raw, neu, ncand, nout;
+  unsigned long long obase;
+  // Emitted pairs are staged here during the pair loop (the table is dead
+  // by then; with OVERLAY only the part past the member arrays is free) and
+  // written out with one global reservation per bucket.
+  static constexpr size_t OUT_OFF = OVERLAY ? MEM_BYTES : 0;
+  static constexpr uint32_t OUTCAP = (uint32_t)((TAB_BYTES - OUT_OFF) / 8);
+  __device__ unsigned long long *outbuf() {
+    return reinterpret_cast<unsigned long long *>(big + OUT_OFF);
+  }
   // (h2 << 32 | rows) per slot; later (member offset << 32 | rows)
   __device__ unsigned long long *tab() { return reinterpret_cast<unsigned long long *>(big); }
   __device__ uint64_t *codes() {
@@ -494,6 +542,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   constexpr int PT = CAP / NT;
   constexpr uint32_t MCAP = HGroupSmem<W, CAP, NT, MDIV>::MCAP;
   constexpr uint32_t GCAP = HGroupSmem<W, CAP, NT, MDIV>::GCAP;
+  constexpr uint32_t OUTCAP = HGroupSmem<W, CAP, NT, MDIV>::OUTCAP;
   const int rep = ub.rep[u];
   // 1. load the bucket (coalesced; from global or from the smem stage)
   uint64_t e[PT];
@@ -515,7 +564,9 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   uint16_t *F = reinterpret_cast<uint16_t *>(S.tab());
   for (uint32_t i = threadIdx.x * 8; i < FS; i += NT * 8)
     *reinterpret_cast<uint4 *>(&F[i]) = make_uint4(~0u, ~0u, ~0u, ~0u);
-  if (threadIdx.x == 0) { S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; }
+  if (threadIdx.x == 0) {
+    S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; S.nout = 0;
+  }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
@@ -672,7 +723,6 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   // 5. every in-group pair once (load-balanced over the CTA)
   const uint32_t P = S.pp[R];
   const unsigned long long *kept = ub.kept[u];
-  const uint64_t maskbits = ub.maskbits[u];
   uint32_t my_raw = 0, my_new = 0;
   // Each thread takes a contiguous range of the flattened pair index and
   // walks it incrementally (one group lookup + triangular decode per thread).
@@ -699,14 +749,23 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
 #pragma unroll
       for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + ib) * W + w];
       const uint32_t rb = mrows[start + ib];
-      const int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, S.b2b);
+      const int v = pair_verdict<W>(ca, cb, ra, rb, a, ub, u, kept, rep, S.b2b);
       my_raw += v > 0;
       my_new += v == 2;
       const bool emit = v == 2;
-      const unsigned long long slot = warp_append(emit, &a.ctr[0]);
-      if (emit && slot < a.out_cap) {
-        a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-        if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+      const unsigned mask = __ballot_sync(__activemask(), emit);
+      if (mask) {   // stage in shared memory (global only on overflow)
+        const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+        const uint32_t so = smem_append(emit, mask, &S.nout);
+        const bool spill = emit && so >= OUTCAP;
+        if (emit && !spill) S.outbuf()[so] = key;
+        if (__any_sync(__activemask(), spill)) {
+          const unsigned long long slot = warp_append(spill, &a.ctr[0]);
+          if (spill && slot < a.out_cap) {
+            a.out_keys[slot] = key;
+            if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+          }
+        }
       }
       // advance (ia, ib) in (0,1),(0,2),..,(1,2),.. order, crossing groups
       if (++ib == len) {
@@ -730,12 +789,24 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   if (my_raw) atomicAdd(&S.raw, my_raw);
   if (my_new) atomicAdd(&S.neu, my_new);
   __syncthreads();
+  const uint32_t nst = min(S.nout, OUTCAP);
   if (threadIdx.x == 0) {
     if (S.raw) atomicAdd(&a.ctr[3 + rep], (unsigned long long)S.raw);
     if (S.neu) atomicAdd(&a.ctr[3 + a.reps + rep], (unsigned long long)S.neu);
     atomicMax(&a.ctr[1], (unsigned long long)S.maxrun);
+    if (nst) S.obase = atomicAdd(&a.ctr[0], (unsigned long long)nst);
   }
   __syncthreads();
+  if (nst) {
+    const unsigned long long base = S.obase;
+    for (uint32_t i = threadIdx.x; i < nst; i += NT) {
+      if (base + i < a.out_cap) {
+        a.out_keys[base + i] = S.outbuf()[i];
+        if (a.out_rep) a.out_rep[base + i] = (uint8_t)rep;
+      }
+    }
+    __syncthreads();
+  }
   return true;
 }
 
@@ -971,7 +1042,6 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
     const unsigned long long ntp = (unsigned long long)nt * (nt + 1) / 2;
     const int rep = ub.rep[u];
     const unsigned long long *kept = ub.kept[u];
-    const uint64_t maskbits = ub.maskbits[u];
     const uint64_t *el = spill_elems(a, u, s0);
     const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
     const bool count_groups = (int64_t)s * 4 > a.n;
@@ -1024,7 +1094,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
               ++my_eq;
               if (count_groups) atomicAdd(&gc[ib0 + j], 1u);
               const uint32_t rb = (uint32_t)f;
-              int v = pair_verdict<W>(ca, cb, ra, rb, a, kept, maskbits, rep, b2b);
+              int v = pair_verdict<W>(ca, cb, ra, rb, a, ub, u, kept, rep, b2b);
               my_raw += v > 0;
               my_new += v == 2;
               emit = v == 2;
