@@ -236,6 +236,8 @@ def main():
     ap.add_argument("--cpu-sample-rows", type=int, default=400_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--soak-s", type=float, default=2.0,
+                    help="untimed warm steps (seconds) after --warmup, before timing")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -272,7 +274,21 @@ def main():
             return distributed.hamming_step(x_dev, params, world, rank)
         return distributed.build_step(x_dev, params, cfg.metric, world, rank)
 
+    t_w = time.perf_counter()
     for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # untimed soak: the first builds after process start (allocator growth,
+    # clock ramp after the CPU-side input generation) run up to several
+    # times slower; add warm steps worth about --soak-s seconds (a step
+    # count agreed over ranks, since multi-rank steps hold collectives)
+    per = (time.perf_counter() - t_w) / max(1, args.warmup)
+    n_soak = int(min(1000, math.ceil(args.soak_s / max(per, 1e-4))))
+    if world > 1:
+        t = torch.tensor([n_soak], dtype=torch.int64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        n_soak = int(t.item())
+    for _ in range(n_soak):
         step()
     torch.cuda.synchronize()
 

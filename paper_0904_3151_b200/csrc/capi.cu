@@ -110,7 +110,9 @@ static double projection_tau(int dim) {
 
 static unsigned long long fixup_cap(int64_t n, int cols) {
   unsigned long long c = (unsigned long long)n * cols / 32;
-  return c < (1ull << 20) ? (1ull << 20) : c;
+  c = c < (1ull << 20) ? (1ull << 20) : c;
+  const int forced = env_int("EG_FIXUP_CAP", 0);   // tests: force the overflow path
+  return forced > 0 && (unsigned long long)forced < c ? (unsigned long long)forced : c;
 }
 
 template <typename TX, int TN>
@@ -493,6 +495,21 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
       EG_LAUNCH_CHECK();
       {
         EG_PROF(PC_FIXUP, st);
+        const int64_t words = (int64_t)replicates * n * W;
+        const int64_t per = (int64_t)COLLECT_NT * COLLECT_WPT;
+        k_collect_bits<<<(unsigned)std::min<int64_t>((words + per - 1) / per,
+                                                     (int64_t)num_sms() * 8),
+                         COLLECT_NT, 0, st>>>(unc, n, W, length, replicates, items, cnt, cap);
+        const size_t fxs = fixl_smem(cols);
+        static size_t fixl_set = 0;
+        if (fxs > 48 * 1024 && fxs > fixl_set) {
+          EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_list,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)fxs));
+          fixl_set = fxs;
+        }
+        k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
+            (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
         const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
         if (fsm > 48 * 1024)
           EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_bits,
@@ -500,7 +517,7 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
                                            (int)fsm));
         const unsigned fg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
         k_fixup_bits<<<fg, 256, fsm, st>>>((const float *)d_x, n, dim, d_r, length, W,
-                                           replicates, d_codes, unc, cnt);
+                                           replicates, d_codes, unc, cnt, cap);
       }
       EG_LAUNCH_CHECK();
       if (d_fixups)

@@ -525,21 +525,128 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// Band entries flagged in the bitmap (layout of the codes) -> entry list
+// (row << 32 | column).  Each CTA pass takes 8 words per thread, scans the
+// popcounts and reserves its output with ONE global atomic (a single shared
+// counter under per-warp atomics serialises at L2).  Entries past `cap` are
+// counted but not stored; k_fixup_bits then redoes the whole bitmap.
+constexpr int COLLECT_NT = 256, COLLECT_WPT = 8;
+__global__ void __launch_bounds__(COLLECT_NT) k_collect_bits(
+    const uint64_t *__restrict__ unc_bits, int64_t n, int W, int L, int reps,
+    unsigned long long *__restrict__ items, unsigned long long *__restrict__ count,
+    unsigned long long cap) {
+  __shared__ uint32_t sw[COLLECT_NT / 32];
+  __shared__ unsigned long long sbase;
+  const int64_t total = (int64_t)reps * n * W;
+  constexpr int64_t PER = (int64_t)COLLECT_NT * COLLECT_WPT;
+  for (int64_t b0 = (int64_t)blockIdx.x * PER; b0 < total; b0 += (int64_t)gridDim.x * PER) {
+    uint64_t u[COLLECT_WPT];
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < COLLECT_WPT; ++j) {
+      const int64_t i = b0 + (int64_t)j * COLLECT_NT + threadIdx.x;
+      u[j] = i < total ? unc_bits[i] : 0ull;
+      cnt += __popcll(u[j]);
+    }
+    uint32_t tot;
+    uint32_t off = block_exclusive_scan<COLLECT_NT>(cnt, tot, sw);
+    if (threadIdx.x == 0) sbase = tot ? atomicAdd(count, (unsigned long long)tot) : 0ull;
+    __syncthreads();
+    const unsigned long long base = sbase + off;
+    uint32_t k = 0;
+#pragma unroll
+    for (int j = 0; j < COLLECT_WPT; ++j) {
+      uint64_t x = u[j];
+      if (!x) continue;
+      const int64_t i = b0 + (int64_t)j * COLLECT_NT + threadIdx.x;
+      const int64_t hw = i / W;
+      const int h = (int)(hw / n), w = (int)(i - hw * W);
+      const int64_t row = hw - (int64_t)h * n;
+      while (x) {
+        const int bit = __ffsll((long long)x) - 1;
+        x &= x - 1;
+        if (base + k < cap)
+          items[base + k] = ((unsigned long long)row << 32) | (unsigned)(h * L + w * 64 + bit);
+        ++k;
+      }
+    }
+    __syncthreads();   // sbase / sw reused by the next pass
+  }
+}
+
+// Exact recompute of listed band entries, one thread per entry.  The
+// direction matrix is staged through shared memory in 32-wide q chunks
+// (shared by the CTA's 256 entries), each thread streams its own row with
+// 16-byte loads issued a whole chunk ahead, and adds the separately rounded
+// products in ascending q -- the reference's sequential fp64 sum
+// (lsh.py:107-112).  Positive sums set the code bit (atomicOr: two entries
+// may share a word).
+constexpr int FIXL_NT = 256, FIXL_QC = 32;
+__host__ __device__ inline size_t fixl_smem(int cols) { return (size_t)(FIXL_QC + 1) * cols * 8; }
+__global__ void __launch_bounds__(FIXL_NT) k_fixup_list(
+    const float *__restrict__ x, int dim, const double *__restrict__ r, int cols, int64_t n,
+    int L, int W, uint64_t *__restrict__ codes, const unsigned long long *__restrict__ items,
+    const unsigned long long *__restrict__ count, unsigned long long cap) {
+  extern __shared__ double rs[];                    // [cols][FIXL_QC + 1]
+  const unsigned long long total = min(*count, cap);
+  for (unsigned long long e0 = (unsigned long long)blockIdx.x * FIXL_NT; e0 < total;
+       e0 += (unsigned long long)gridDim.x * FIXL_NT) {
+    const unsigned long long ei = e0 + threadIdx.x;
+    const bool mine = ei < total;
+    const unsigned long long it = mine ? items[ei] : 0ull;
+    const int64_t row = (int64_t)(it >> 32);
+    const int c = (int)(it & 0xffffffffu);
+    const float4 *xr = reinterpret_cast<const float4 *>(x + row * dim);
+    double acc = 0.0;
+    for (int q0 = 0; q0 < dim; q0 += FIXL_QC) {
+      const int qn = min(FIXL_QC, dim - q0);        // multiple of 4
+      float4 xv[FIXL_QC / 4];
+#pragma unroll
+      for (int j = 0; j < FIXL_QC / 4; ++j)
+        xv[j] = (mine && 4 * j < qn) ? __ldg(xr + q0 / 4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      __syncthreads();                               // previous chunk consumed
+      for (int i = threadIdx.x; i < cols * FIXL_QC; i += FIXL_NT) {
+        const int cc = i / FIXL_QC, qq = i - cc * FIXL_QC;
+        rs[cc * (FIXL_QC + 1) + qq] = qq < qn ? __ldg(r + (int64_t)cc * dim + q0 + qq) : 0.0;
+      }
+      __syncthreads();
+      if (mine) {
+#pragma unroll
+        for (int j = 0; j < FIXL_QC / 4; ++j) {
+          if (4 * j >= qn) break;
+          const double *rq = rs + c * (FIXL_QC + 1) + 4 * j;
+          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].x, rq[0]));
+          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].y, rq[1]));
+          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].z, rq[2]));
+          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].w, rq[3]));
+        }
+      }
+    }
+    if (mine && acc > 0.0) {
+      const int h = c / L, t = c - h * L;
+      atomicOr((unsigned long long *)&codes[((int64_t)h * n + row) * W + (t >> 6)],
+               1ull << (t & 63));
+    }
+  }
+}
+
 // Exact recompute of the band entries flagged in the bitmap (same layout as
-// the codes).  One warp per 32 rows: lanes compute the separately rounded
-// products of one entry in parallel (coalesced row reads), lane 0 adds them
-// in ascending q -- the reference's sequential fp64 sum (lsh.py:107-112).
+// the codes) -- the overflow path of k_collect_bits/k_fixup_list (exits at
+// once unless the list overflowed).  One warp per 32 rows: lanes compute the
+// separately rounded products of one entry in parallel (coalesced row
+// reads), lane 0 adds them in ascending q (lsh.py:107-112).
 __global__ void __launch_bounds__(256) k_fixup_bits(const float *__restrict__ x, int64_t n,
                                                     int dim, const double *__restrict__ r, int L,
                                                     int W, int reps,
                                                     uint64_t *__restrict__ codes,
                                                     const uint64_t *__restrict__ unc_bits,
-                                                    unsigned long long *__restrict__ count) {
+                                                    const unsigned long long *__restrict__ count,
+                                                    unsigned long long cap) {
+  if (*count <= cap) return;
   extern __shared__ double prod_all[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   double *prod = prod_all + (int64_t)wib * dim;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  unsigned long long mine = 0;
   for (int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + wib) * 32; base < n;
        base += nwarps * 32) {
     const int64_t row = base + lane;
@@ -572,7 +679,6 @@ __global__ void __launch_bounds__(256) k_fixup_bits(const float *__restrict__ x,
               }
               for (; qq < dim; ++qq) acc = __dadd_rn(acc, prod[qq]);
               if (acc > 0.0) codes[((int64_t)h * n + rr) * W + w] |= 1ull << bit;
-              ++mine;
             }
             __syncwarp();
           }
@@ -581,7 +687,6 @@ __global__ void __launch_bounds__(256) k_fixup_bits(const float *__restrict__ x,
       }
     }
   }
-  if (lane == 0 && mine) atomicAdd(count, mine);
 }
 
 // Error band of the 3xTF32 product relative to ||x|| ||r|| (see header):

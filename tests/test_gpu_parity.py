@@ -200,6 +200,18 @@ def test_projection_vs_oracle_large(eg, oracle):
         np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("simt", ["0", "1"])
+def test_projection_fixup_overflow_path(eg, oracle, monkeypatch, simt):
+    """A tiny band-list capacity forces the overflow recompute (bitmap path on
+    the tensor cores, full recompute on the SIMT path): codes still exact."""
+    from paper_0904_3151_b200 import workloads
+    monkeypatch.setenv("EG_FIXUP_CAP", "64")
+    monkeypatch.setenv("EG_PROJECT_SIMT", simt)
+    x = workloads.cfg3_points(6_000, planted_rows=600)
+    got = eg.project(x, eg.ProjectionSpec(48, 0, 1)).words
+    np.testing.assert_array_equal(got, oracle.project_words(x, 48, 0, 1))
+
+
 def test_projection_validation(eg):
     with pytest.raises(eg.DataError, match="row 1"):
         eg.project(np.array([[1.0, 1.0], [0.0, 0.0]], dtype=np.float32), eg.ProjectionSpec(8))
