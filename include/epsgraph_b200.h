@@ -63,7 +63,8 @@ int eg_profile_read(double *ms_out, long long *count_out, int max_classes);
 /* (lsh.py:48-57), _check_norms (lsh.py:121-125) and the norm pass of     */
 /* filter_exact (pipeline.py:203).                                        */
 /* d_x: n x dim row-major, float32 (x_is_f64 = 0) or float64 (= 1).       */
-/* d_norms[n] = sqrt(sum_q x_q^2) in fp64.  d_bad (device uint64[2]):     */
+/* d_norms[n] = sqrt(sum_q x_q^2) in fp64, squares added by fma in        */
+/* ascending q (one fixed order on every path).  d_bad (device uint64[2]):*/
 /* [0] = first row with a non-finite entry, [1] = first zero-norm row,    */
 /* UINT64_MAX when none.  Asynchronous (no host synchronisation), so the  */
 /* build can check the flags once at its end.                             */
@@ -93,6 +94,17 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
                int32_t length, int32_t replicates, uint64_t *d_codes,
                void *d_workspace, size_t workspace_bytes, uint64_t *d_fixups,
                void *stream);
+
+/* eg_row_stats + eg_project in one call: d_norms / d_bad are OUTPUTS (as  */
+/* eg_row_stats).  On the tensor-core path the norms are accumulated by    */
+/* the projection kernel itself, so the rows cross HBM once; elsewhere the */
+/* two kernels run back to back.  Same results as the separate calls.      */
+/* Workspace: eg_project_workspace.  Asynchronous.                         */
+int eg_project_rows(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
+                    double *d_norms, uint64_t *d_bad, const double *d_r,
+                    const double *d_rnorm, int32_t length, int32_t replicates,
+                    uint64_t *d_codes, void *d_workspace, size_t workspace_bytes,
+                    uint64_t *d_fixups, void *stream);
 
 /* Test hook: when d_buf is non-null, the tensor-core projection path also */
 /* writes its raw fp32 accumulator (n x replicates*length) to d_buf, so the */

@@ -65,6 +65,7 @@ def _declare(lib):
         "eg_debug_set_tc_dump": ([P], None),
         "eg_project_workspace": ([i64, i32, i32, i32], sz),
         "eg_project": ([P, I, i64, i32, P, P, P, i32, i32, P, P, sz, P, P], I),
+        "eg_project_rows": ([P, I, i64, i32, P, P, P, P, i32, i32, P, P, sz, P, P], I),
         "eg_msm_workspace": ([i64, i32, i32], sz),
         "eg_msm_plan_workspace": ([i32, i32, i32], sz),
         "eg_msm_plan": ([P, i64, i32, i32, i32, dbl, P, P, P, sz, P], I),

@@ -373,14 +373,14 @@ int eg_row_stats(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *
   if (n < 0 || dim < 1 || !d_bad) return arg_error("eg_row_stats: bad shape");
   EG_CUDA_TRY(cudaMemsetAsync(d_bad, 0xff, 16, st));
   if (n == 0) return EG_OK;
-  unsigned grid = (unsigned)((n + 7) / 8);
+  unsigned grid = (unsigned)((n + ROWST_WARPS * 32 - 1) / (ROWST_WARPS * 32));
   EG_PROF(PC_ROW_STATS, st);
   if (x_is_f64)
-    k_row_stats<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms,
-                                              (unsigned long long *)d_bad);
+    k_row_stats<double><<<grid, ROWST_WARPS * 32, 0, st>>>((const double *)d_x, n, dim, d_norms,
+                                                        (unsigned long long *)d_bad);
   else
-    k_row_stats<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms,
-                                             (unsigned long long *)d_bad);
+    k_row_stats<float><<<grid, ROWST_WARPS * 32, 0, st>>>((const float *)d_x, n, dim, d_norms,
+                                                       (unsigned long long *)d_bad);
   EG_LAUNCH_CHECK();
   return EG_OK;
 }
@@ -426,11 +426,38 @@ static bool make_x_tensor_map(CUtensorMap *map, const void *d_x, int64_t n, int 
 static float *g_tc_debug = nullptr;
 extern "C" void eg_debug_set_tc_dump(float *d_buf) { g_tc_debug = d_buf; }
 
+// Shared body of eg_project / eg_project_rows.  d_bad != nullptr: also
+// produce the row norms into d_norms (and the bad-row flags) -- fused into
+// the tensor-core kernel where that path runs, else k_row_stats first.
+static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *d_norms,
+                        const double *d_r, const double *d_rnorm, int32_t length,
+                        int32_t replicates, uint64_t *d_codes, void *d_workspace,
+                        size_t workspace_bytes, uint64_t *d_fixups, uint64_t *d_bad,
+                        cudaStream_t st);
+
 int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const double *d_norms,
                const double *d_r, const double *d_rnorm, int32_t length, int32_t replicates,
                uint64_t *d_codes, void *d_workspace, size_t workspace_bytes, uint64_t *d_fixups,
                void *stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+  return project_impl(d_x, x_is_f64, n, dim, const_cast<double *>(d_norms), d_r, d_rnorm, length,
+                      replicates, d_codes, d_workspace, workspace_bytes, d_fixups, nullptr,
+                      (cudaStream_t)stream);
+}
+
+int eg_project_rows(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *d_norms,
+                    uint64_t *d_bad, const double *d_r, const double *d_rnorm, int32_t length,
+                    int32_t replicates, uint64_t *d_codes, void *d_workspace,
+                    size_t workspace_bytes, uint64_t *d_fixups, void *stream) {
+  if (!d_bad || !d_norms) return arg_error("eg_project_rows: d_norms and d_bad are required");
+  return project_impl(d_x, x_is_f64, n, dim, d_norms, d_r, d_rnorm, length, replicates, d_codes,
+                      d_workspace, workspace_bytes, d_fixups, d_bad, (cudaStream_t)stream);
+}
+
+static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *d_norms,
+                        const double *d_r, const double *d_rnorm, int32_t length,
+                        int32_t replicates, uint64_t *d_codes, void *d_workspace,
+                        size_t workspace_bytes, uint64_t *d_fixups, uint64_t *d_bad,
+                        cudaStream_t st) {
   if (n < 0 || dim < 1 || length < 1 || replicates < 1)
     return arg_error("eg_project: bad shape");
   if ((int64_t)length * replicates >= (1ll << 31) || n >= (1ll << 32))
@@ -440,7 +467,10 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   const int cols_pad = (cols + 31) / 32 * 32;
   EG_CUDA_TRY(cudaMemsetAsync(d_codes, 0, (size_t)replicates * n * W * 8, st));
   if (d_fixups) EG_CUDA_TRY(cudaMemsetAsync(d_fixups, 0, 8, st));
-  if (n == 0) return EG_OK;
+  if (n == 0) {
+    if (d_bad) EG_CUDA_TRY(cudaMemsetAsync(d_bad, 0xff, 16, st));
+    return EG_OK;
+  }
   Arena ar(d_workspace, workspace_bytes);
   float *rt = ar.take<float>((size_t)dim * cols_pad);
   unsigned long long *cnt = ar.take<unsigned long long>(1);
@@ -455,6 +485,16 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
   const int npad = (cols + 15) / 16 * 16;
   const bool use_tc = !x_is_f64 && dim % 4 == 0 && npad <= TC_MAXN &&
                       !env_int("EG_PROJECT_SIMT", 0);
+  CUtensorMap xmap;
+  const bool tma_ok = use_tc && !env_int("EG_PROJECT_TC1", 0) &&
+                      make_x_tensor_map(&xmap, d_x, n, dim);
+  const bool fuse = d_bad && tma_ok && !env_int("EG_PROJECT_UNFUSED", 0);
+  if (d_bad && !fuse) {   // norms first, then the projection reads them
+    int rc = eg_row_stats(d_x, x_is_f64, n, dim, d_norms, d_bad, st);
+    if (rc) return rc;
+  } else if (fuse) {
+    EG_CUDA_TRY(cudaMemsetAsync(d_bad, 0xff, 16, st));
+  }
   if (use_tc) {
     float *img = ar.take<float>((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK);
     if (!img) {
@@ -468,8 +508,6 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
     EG_LAUNCH_CHECK();
     const int64_t ntiles = (n + TC_M - 1) / TC_M;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
-    CUtensorMap xmap;
-    const bool tma_ok = !env_int("EG_PROJECT_TC1", 0) && make_x_tensor_map(&xmap, d_x, n, dim);
     if (tma_ok) {
       const size_t sbytes = tc2_stage_bytes(npad);
       const int nstages = (int)std::min<size_t>(4, ((size_t)212 << 10) / sbytes);
@@ -490,7 +528,10 @@ int eg_project(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doub
         k_project_tc2<<<grid, TC2_THREADS, smem, st>>>(xmap, n, dim, img, cols, npad, nstages,
                                                        d_norms, d_rnorm, tc_tau(dim), length, W,
                                                        d_codes, unc, g_tc_debug,
-                                                       env_int("EG_TC_EXP", 0));
+                                                       env_int("EG_TC_EXP", 0),
+                                                       fuse ? d_norms : nullptr,
+                                                       fuse ? (unsigned long long *)d_bad
+                                                            : nullptr);
       }
       EG_LAUNCH_CHECK();
       {

@@ -18,27 +18,40 @@
 namespace eg {
 
 // ----------------------------------------------------------- row stats
+constexpr int ROWST_WARPS = 4;
 template <typename TX>
-__global__ void __launch_bounds__(256) k_row_stats(const TX *__restrict__ x, int64_t n, int dim,
+__global__ void __launch_bounds__(ROWST_WARPS * 32) k_row_stats(const TX *__restrict__ x, int64_t n,
+                                                   int dim,
                                                    double *__restrict__ norms,
                                                    unsigned long long *__restrict__ bad) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (row >= n) return;
-  const TX *xr = x + row * dim;
+  // One warp per 32 rows: 32x32 tiles staged through shared memory with
+  // coalesced loads; each lane then adds its own row's squares in ascending
+  // q (fma, fp64) -- the order the tensor-core projection's converters use,
+  // so both paths produce bit-identical norms.
+  __shared__ TX tile[ROWST_WARPS][32][33];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * ROWST_WARPS + wib) * 32;
+  if (r0 >= n) return;
+  const int64_t row = r0 + lane;
   double s = 0.0;
   bool finite = true;
-  for (int q = lane; q < dim; q += 32) {
-    double v = (double)xr[q];
-    finite &= isfinite(v);
-    s = fma(v, v, s);
+  for (int q0 = 0; q0 < dim; q0 += 32) {
+    const int q = q0 + lane;
+#pragma unroll 8
+    for (int e = 0; e < 32; ++e)
+      tile[wib][e][lane] = (r0 + e < n && q < dim) ? x[(r0 + e) * dim + q] : (TX)0;
+    __syncwarp();
+    const int qn = min(32, dim - q0);
+    for (int j = 0; j < qn; ++j) {
+      const double v = (double)tile[wib][lane][j];
+      finite &= isfinite(v);
+      s = fma(v, v, s);
+    }
+    __syncwarp();
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  bool all_finite = __all_sync(0xffffffffu, finite);
-  if (lane == 0) {
+  if (row < n) {
     norms[row] = sqrt(s);
-    if (!all_finite) atomicMin(&bad[0], (unsigned long long)row);
+    if (!finite) atomicMin(&bad[0], (unsigned long long)row);
     if (s == 0.0) atomicMin(&bad[1], (unsigned long long)row);
   }
 }

@@ -342,8 +342,9 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 }
 
 struct Tc2Bars {
-  uint64_t full[4], conv[4], empty[4], accfull[2], accempty[2];
+  uint64_t full[4], conv[4], empty[4], accfull[2], accempty[2], normfull[2], normempty[2];
   uint32_t tmem_base;
+  float xnorm[2][TC_M];      // fused row norms (times 1 + 1e-6) per accumulator buffer
   // epilogue column tables: word index (h * W + t / 64), bit (t % 64),
   // tau * ||r_c|| (fp32, rounded up)
   uint16_t colw[TC_MAXN];
@@ -359,7 +360,13 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
     const __grid_constant__ CUtensorMap xmap, int64_t n, int dim, const float *__restrict__ img,
     int cols, int npad, int nstages, const double *__restrict__ xnorm,
     const double *__restrict__ rnorm, double tau, int L, int W, uint64_t *__restrict__ codes,
-    uint64_t *__restrict__ unc_bits, float *__restrict__ dbg, int exp_flags) {
+    uint64_t *__restrict__ unc_bits, float *__restrict__ dbg, int exp_flags,
+    double *__restrict__ norms_out, unsigned long long *__restrict__ bad) {
+  // norms_out != nullptr: the converters also produce the fp64 row norms
+  // (sequential fma over ascending q, as k_row_stats) and the bad-row flags,
+  // and hand the norms to the epilogue through shared memory (xnorm is not
+  // read); the rows then cross HBM once for norms and projection together.
+  const bool fuse = norms_out != nullptr;
   extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
   unsigned char *smem = tc_smem_raw + ((1024u - (smem_u32(tc_smem_raw) & 1023u)) & 1023u);
   const size_t sb = tc2_stage_bytes(npad);
@@ -389,6 +396,8 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
     for (int b = 0; b < 2; ++b) {
       mbar_init(&B.accfull[b], 1);
       mbar_init(&B.accempty[b], 128);
+      mbar_init(&B.normfull[b], 128);
+      mbar_init(&B.normempty[b], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&xmap) : "memory");
@@ -449,8 +458,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
   } else if (warp >= 4 && warp < 8) {
     // ---------------------------------------------------------- converters
     const uint32_t row = (uint32_t)(tid - 128);
-    uint32_t it = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t it = 0, t = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      double ss = 0.0;
       for (int kc = 0; kc < nkc; ++kc, ++it) {
         const int s = it % nstages;
         const uint32_t use = it / nstages;
@@ -461,6 +471,12 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         for (int c = 0; c < ((exp_flags & 2) ? 0 : 8); ++c) {
           const uint32_t off = sw128_off(row, (uint32_t)c) / 4;
           const float4 v = *reinterpret_cast<const float4 *>(xh + off);
+          if (fuse) {        // OOB columns are TMA zero-fill: fma(0, 0, s) == s
+            ss = fma((double)v.x, (double)v.x, ss);
+            ss = fma((double)v.y, (double)v.y, ss);
+            ss = fma((double)v.z, (double)v.z, ss);
+            ss = fma((double)v.w, (double)v.w, ss);
+          }
           const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
           *reinterpret_cast<float4 *>(xh + off) = h;
           *reinterpret_cast<float4 *>(xl + off) =
@@ -468,6 +484,19 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         }
         fence_async_smem();
         mbar_arrive(&B.conv[s]);
+      }
+      if (fuse) {
+        const uint32_t b = t & 1, buse = t >> 1;
+        const int64_t grow = tile * TC_M + row;
+        const double nrm = sqrt(ss);
+        if (grow < n) {
+          norms_out[grow] = nrm;
+          if (!isfinite(ss)) atomicMin(&bad[0], (unsigned long long)grow);
+          if (ss == 0.0) atomicMin(&bad[1], (unsigned long long)grow);
+        }
+        mbar_wait(&B.normempty[b], (buse & 1) ^ 1);
+        B.xnorm[b][row] = grow < n ? (float)(nrm * (1.0 + 1e-6)) : 0.f;
+        mbar_arrive(&B.normfull[b]);
       }
     }
   } else if (warp >= 8) {
@@ -480,7 +509,14 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       tc_fence_after();
       const int64_t grow = tile * TC_M + q * 32 + lane;
       const bool row_ok = grow < n;
-      const float xn = row_ok ? (float)(__ldg(xnorm + grow) * (1.0 + 1e-6)) : 0.f;
+      float xn;
+      if (fuse) {
+        mbar_wait(&B.normfull[b], buse & 1);
+        xn = B.xnorm[b][q * 32 + lane];
+        mbar_arrive(&B.normempty[b]);
+      } else {
+        xn = row_ok ? (float)(__ldg(xnorm + grow) * (1.0 + 1e-6)) : 0.f;
+      }
       uint64_t word = 0, uword = 0;
       uint32_t cur_word = 0xffffffffu;
       // Each row's words are produced entirely by this thread, in column

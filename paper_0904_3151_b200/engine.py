@@ -104,6 +104,46 @@ def directions(length: int, dim: int, seed: int, replicate_id: int) -> np.ndarra
     return np.random.Generator(np.random.PCG64(ss)).standard_normal((length, dim))
 
 
+_dir_cache: dict = {}
+
+
+def device_directions(length: int, dim: int, seed: int, replicate_ids, dev):
+    """Directions of the replicates and their norms, resident on ``dev``
+    (drawn once per (length, dim, seed, replicates, device) and kept: the
+    draw is deterministic, so repeated builds reuse the device copy)."""
+    key = (length, dim, int(seed), tuple(int(h) for h in replicate_ids), str(dev))
+    hit = _dir_cache.get(key)
+    if hit is None:
+        r = np.concatenate([directions(length, dim, seed, h) for h in replicate_ids], axis=0)
+        rnorm = np.sqrt(np.einsum("ij,ij->i", r, r))
+        hit = (torch.from_numpy(np.ascontiguousarray(r)).to(dev),
+               torch.from_numpy(rnorm).to(dev))
+        if len(_dir_cache) >= 8:
+            _dir_cache.pop(next(iter(_dir_cache)))
+        _dir_cache[key] = hit
+    return hit
+
+
+def project_rows(x: torch.Tensor, length: int, seed: int, replicate_ids):
+    """Row norms + bad-row flags + packed codes in one pass over the rows
+    (``eg_project_rows``); returns (codes, norms, bad, fixups), no sync."""
+    dev = x.device
+    n, dim = x.shape
+    reps = len(replicate_ids)
+    W = max(1, -(-length // 64))
+    r_d, rn_d = device_directions(length, dim, seed, replicate_ids, dev)
+    codes = torch.empty((reps, n, W), dtype=torch.int64, device=dev)
+    norms = torch.empty(n, dtype=torch.float64, device=dev)
+    bad = torch.empty(2, dtype=torch.int64, device=dev)
+    lib = _native.lib()
+    ws = _ws(lib.eg_project_workspace(n, dim, length, reps), dev)
+    fix = torch.zeros(1, dtype=torch.int64, device=dev)
+    check(lib.eg_project_rows(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms), _p(bad),
+                              _p(r_d), _p(rn_d), length, reps, _p(codes), _p(ws), ws.numel(),
+                              _p(fix), _stream(dev)), "project_rows")
+    return codes, norms, bad, fix
+
+
 def project_codes(x: torch.Tensor, norms: torch.Tensor, length: int, seed: int,
                   replicate_ids) -> tuple[torch.Tensor, torch.Tensor]:
     """Packed codes ``(r, n, W)`` uint64 for the given replicate ids, plus a
@@ -112,10 +152,7 @@ def project_codes(x: torch.Tensor, norms: torch.Tensor, length: int, seed: int,
     n, dim = x.shape
     reps = len(replicate_ids)
     W = max(1, -(-length // 64))
-    r = np.concatenate([directions(length, dim, seed, h) for h in replicate_ids], axis=0)
-    rnorm = np.sqrt(np.einsum("ij,ij->i", r, r))
-    r_d = torch.from_numpy(np.ascontiguousarray(r)).to(dev)
-    rn_d = torch.from_numpy(rnorm).to(dev)
+    r_d, rn_d = device_directions(length, dim, seed, replicate_ids, dev)
     codes = torch.empty((reps, n, W), dtype=torch.int64, device=dev)
     lib = _native.lib()
     ws = _ws(lib.eg_project_workspace(n, dim, length, reps), dev)

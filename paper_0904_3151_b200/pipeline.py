@@ -118,12 +118,16 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     ev[0].record()
     bad = None
-    if norms is None:
-        norms, bad = engine.row_stats_async(x)     # checked once msm_pairs syncs
     fix = None
-    if codes is None:
-        codes, fix = engine.project_codes(x, norms, params.length, params.seed,
-                                          list(range(1, params.replicates + 1)))
+    reps = list(range(1, params.replicates + 1))
+    if norms is None and codes is None:
+        # one pass over the rows: norms + flags fused into the projection
+        codes, norms, bad, fix = engine.project_rows(x, params.length, params.seed, reps)
+    else:
+        if norms is None:
+            norms, bad = engine.row_stats_async(x)     # checked once msm_pairs syncs
+        if codes is None:
+            codes, fix = engine.project_codes(x, norms, params.length, params.seed, reps)
     ev[1].record()
     if blocks is None:
         blocks = engine.msm_plan(codes, params.length, params.blocks, params.mismatch)

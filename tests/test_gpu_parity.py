@@ -290,6 +290,34 @@ def test_build_edge_cases(eg):
         eg.build_graph(x, params)
 
 
+@pytest.mark.parametrize("env", [{}, {"EG_PROJECT_UNFUSED": "1"}, {"EG_PROJECT_SIMT": "1"}])
+def test_fused_norms_and_flags(eg, oracle, monkeypatch, env):
+    """eg_project_rows: norms accumulated inside the tensor-core projection
+    are bit-identical to k_row_stats' (unfused and SIMT paths), codes equal
+    the oracle's, and the bad-row flags give the reference's errors."""
+    import torch
+    from paper_0904_3151_b200 import engine, workloads
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    x = workloads.cfg3_points(5_000, planted_rows=500)
+    xd = torch.from_numpy(x).cuda()
+    codes, norms, bad, _ = engine.project_rows(xd, 48, 0, [1, 2])
+    ref_norms, _ = engine.row_stats_async(xd)
+    assert torch.equal(norms, ref_norms)
+    np.testing.assert_allclose(norms.cpu().numpy(),
+                               np.sqrt((x.astype(np.float64) ** 2).sum(axis=1)), rtol=1e-14)
+    assert bad.cpu().tolist() == [-1, -1]
+    got = codes.cpu().numpy().view(np.uint64)
+    np.testing.assert_array_equal(got[0], oracle.project_words(x, 48, 0, 1))
+    np.testing.assert_array_equal(got[1], oracle.project_words(x, 48, 0, 2))
+    params = eg.MsmParams(0.05, 1e-3, 48, 3, 12, 2, 0)
+    for bad_row, val in [(4321, np.nan), (777, 0.0), (130, np.inf)]:
+        y = x.copy()
+        y[bad_row] = val
+        with pytest.raises(eg.DataError, match=f"row {bad_row}"):
+            eg.build_graph(y, params)
+
+
 def _config_build(eg, oracle, manifest, name, x, metric="cosine"):
     rec = manifest[name]
     p = rec["params"]
