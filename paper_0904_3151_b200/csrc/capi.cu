@@ -645,13 +645,13 @@ static double env_double(const char *name, double dflt) {
 }
 
 constexpr int PLAN_REF_MAX = 4096;     // reference masks probed for the oversize check
-constexpr int PLAN_PER_K = 4;          // masks probed per candidate block count
+constexpr int PLAN_PER_K = 12;         // masks probed per candidate block count
 constexpr int PLAN_MIN_ROWS = 65536;   // smaller pools keep the reference blocks
 
 size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d) {
   (void)length; (void)k; (void)d;
   const size_t P = PLAN_REF_MAX + PLAN_PER_K * EG_MAX_BLOCKS;
-  return ws_bytes(P * 4, 8) + ws_bytes(P, 8) + ws_bytes(P, 4) + 1024;
+  return ws_bytes(P * 4, 8) + ws_bytes(P, 8) + ws_bytes(P, 4) + ws_bytes(P, 4) + 1024;
 }
 
 int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, int32_t d,
@@ -676,6 +676,7 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   if (nref > PLAN_REF_MAX) return EG_OK;
   const int W = (length + 63) / 64;
   const int S = (int)std::min<int64_t>(n, PLAN_SAMPLE);
+  const int SR = (int)std::min<int64_t>(n, PLAN_REF_SAMPLE);
   // probes: every reference mask (oversize check), then PLAN_PER_K masks of
   // every candidate block count
   std::vector<uint64_t> kept;
@@ -702,7 +703,9 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     }
   }
   const int nref_probes = (int)probe_k.size();
-  for (int kk = d + 1; kk <= kmax; ++kk) {
+  // candidates: d < k' <= k + 2 (finer blocks than the reference's only pay
+  // off marginally; coarser ones are where skewed or clustered codes win)
+  for (int kk = d + 1; kk <= std::min(kmax, k + 2); ++kk) {
     const double units = comb_sat(kk, d);
     if (units > 8192) break;
     if (units <= PLAN_PER_K) {
@@ -736,15 +739,19 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     }
   }
   const int P = (int)probe_k.size();
+  std::vector<int> samples(P);
+  for (int p = 0; p < P; ++p) samples[p] = p < nref_probes ? SR : S;
   Arena ar(d_workspace, workspace_bytes);
   unsigned long long *d_kept = ar.take<unsigned long long>((size_t)P * 4);
   unsigned long long *d_pairs = ar.take<unsigned long long>((size_t)P);
   uint32_t *d_max = ar.take<uint32_t>((size_t)P);
-  if (!d_kept || !d_pairs || !d_max) {
+  int *d_samp = ar.take<int>((size_t)P);
+  if (!d_kept || !d_pairs || !d_max || !d_samp) {
     set_error("eg_msm_plan: workspace too small");
     return EG_ERR_WORKSPACE;
   }
   EG_CUDA_TRY(cudaMemcpyAsync(d_kept, kept.data(), (size_t)P * 32, cudaMemcpyHostToDevice, st));
+  EG_CUDA_TRY(cudaMemcpyAsync(d_samp, samples.data(), (size_t)P * 4, cudaMemcpyHostToDevice, st));
   const size_t smem = (size_t)PLAN_TABLE * 12;
   {
     EG_PROF(PC_MISC, st);
@@ -752,7 +759,7 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   case WW:                                                                                   \
     EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_plan<WW>,                                         \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-    k_msm_plan<WW><<<P, PLAN_NT, smem, st>>>(d_codes, n, S, d_kept, d_pairs, d_max);         \
+    k_msm_plan<WW><<<P, PLAN_NT, smem, st>>>(d_codes, n, d_samp, d_kept, d_pairs, d_max);    \
     break;
     switch (W) {
       EG_PLAN_CASE(1)
@@ -773,13 +780,13 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   // caller's max_group is the reference's own
   uint32_t rmax = 0;
   for (int p = 0; p < nref_probes; ++p) rmax = std::max(rmax, mx[p]);
-  if (S == n) {
+  if (SR == n) {
     if (n > 16 && rmax > oversized_fraction * (double)n) return EG_OK;
-  } else if (oversized_fraction * S < 200 || rmax >= 0.5 * oversized_fraction * S) {
+  } else if (oversized_fraction * SR < 200 || rmax >= 0.5 * oversized_fraction * SR) {
     return EG_OK;
   }
   const double ce = env_double("EG_PLAN_CE_PS", 18.5) * 1e-12;   // per row per unit
-  const double cp = env_double("EG_PLAN_CP_PS", 4.0) * 1e-12;    // per visited pair
+  const double cp = env_double("EG_PLAN_CP_PS", 3.0) * 1e-12;    // per visited pair
   const double scale = S > 1 ? (double)n * (double)(n - 1) / ((double)S * (double)(S - 1)) : 0;
   double best = -1, ref_cost = -1;
   int best_k = k;
@@ -790,6 +797,9 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     for (; p < P && probe_k[p] == kk; ++p, ++cnt) sum += (double)pairs[p];
     const double est_pairs = sum / cnt * scale;
     const double cost = comb_sat(kk, d) * ((double)n * ce + est_pairs * cp);
+    if (env_int("EG_PLAN_DEBUG", 0))
+      fprintf(stderr, "eg_msm_plan: k'=%d units=%.0f est_pairs/mask=%.4g cost=%.3f ms\n", kk,
+              comb_sat(kk, d), est_pairs, cost * 1e3);
     if (kk == k) ref_cost = cost;
     if (best < 0 || cost < best) {
       best = cost;

@@ -16,16 +16,19 @@
 
 namespace eg {
 
-constexpr int PLAN_SAMPLE = 8192;          // rows per probe (max)
-constexpr int PLAN_TABLE = 2 * PLAN_SAMPLE;
+constexpr int PLAN_SAMPLE = 12288;         // rows per cost probe (max)
+constexpr int PLAN_REF_SAMPLE = 2048;      // rows per oversize probe (max)
+constexpr int PLAN_TABLE = 16384;          // load factor <= 0.75
 constexpr int PLAN_NT = 512;
 constexpr uint64_t PLAN_SALT = 0x6a09e667f3bcc909ULL;
 
-// One CTA per probe.  kept[p][4]: bits of the code kept by probe p.
+// One CTA per probe.  kept[p][4]: bits of the code kept by probe p;
+// sample[p]: rows it hashes (strided over [0, n)).
 // out_pairs[p] = sum over sampled groups of C(g, 2); out_max[p] = max g.
 template <int W>
 __global__ void __launch_bounds__(PLAN_NT) k_msm_plan(const uint64_t *__restrict__ codes,
-                                                      int64_t n, int S,
+                                                      int64_t n,
+                                                      const int *__restrict__ sample,
                                                       const unsigned long long *__restrict__ kept,
                                                       unsigned long long *out_pairs,
                                                       uint32_t *out_max) {
@@ -34,6 +37,7 @@ __global__ void __launch_bounds__(PLAN_NT) k_msm_plan(const uint64_t *__restrict
   __shared__ unsigned long long red[PLAN_NT / 32];
   __shared__ uint32_t redm[PLAN_NT / 32];
   const int p = blockIdx.x;
+  const int S = sample[p];
   uint64_t kp[4];
 #pragma unroll
   for (int w = 0; w < 4; ++w) kp[w] = kept[p * 4 + w];

@@ -1,5 +1,5 @@
-timeout 300 python tools/blocks_sweep.py --config cfg3 --blocks 12,auto,6,7,8,9,10,16
-timeout 200 python tools/blocks_sweep.py --config cfg2 --blocks 8,auto,3,4,5,6,10
-timeout 300 python tools/blocks_sweep.py --config cfg4 --blocks 16,auto,3,4,6,8,12 --reps 1
-timeout 400 python tools/blocks_sweep.py --config cfg5 --blocks 16,auto,6,8,10,12 --reps 1
-timeout 100 python tools/blocks_sweep.py --config cfg1 --blocks 8,auto,4,6
+# device time of the MSM stage per forced block count (tools/blocks_sweep.py)
+timeout 300 python tools/blocks_sweep.py --config cfg3 --blocks auto,6,7,8,9,10 --reps 3 | grep blocks=
+timeout 200 python tools/blocks_sweep.py --config cfg2 --blocks auto,3,4,5 --reps 3 | grep blocks=
+timeout 400 python tools/blocks_sweep.py --config cfg5 --blocks auto,4,5,6,7 --reps 1 | grep blocks=
+timeout 400 python tools/blocks_sweep.py --config cfg4 --blocks auto,3,4 --reps 1 | grep blocks=
