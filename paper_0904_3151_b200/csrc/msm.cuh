@@ -39,6 +39,8 @@ constexpr int MSM_TARGET = 3072;        // default target mean bucket size (tune
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 14;         // at most 16384 buckets per unit
 constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to this B
+constexpr uint32_t MSM_PAIR_SPLIT = 65536;  // small-tier buckets with more pairs -> medium
+constexpr int MSM_MED_SLICES = 8;       // medium tier: CTAs sharing one bucket's pairs
 
 constexpr int MSM_MAXT = 8;             // tail blocks of the O(1) canonical test
 
@@ -534,11 +536,16 @@ __device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
 // Returns false (without emitting anything) if the bucket's multi-row groups
 // hold more rows than the member capacity (CAP/2) or more groups than CAP/4;
 // the caller then re-queues it for the next tier.
+// slice / nslices: this CTA walks only its share of the bucket's flattened
+// pairs (the medium tier splits pair-heavy buckets over several CTAs);
+// pair_limit: return false (re-queue) when the bucket holds more pairs.
 template <int W, int CAP, int NT, int MDIV>
 __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
                                                const MsmArgs &a, const UnitBatch &ub, int u,
                                                const uint64_t *el, uint32_t s,
-                                               bool el_in_smem) {
+                                               bool el_in_smem, uint32_t slice = 0,
+                                               uint32_t nslices = 1,
+                                               uint32_t pair_limit = 0xffffffffu) {
   constexpr int PT = CAP / NT;
   constexpr uint32_t MCAP = HGroupSmem<W, CAP, NT, MDIV>::MCAP;
   constexpr uint32_t GCAP = HGroupSmem<W, CAP, NT, MDIV>::GCAP;
@@ -722,13 +729,19 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   __syncthreads();
   // 5. every in-group pair once (load-balanced over the CTA)
   const uint32_t P = S.pp[R];
+  if (P > pair_limit) {    // uniform: hand the bucket to the sliced medium tier
+    __syncthreads();
+    return false;
+  }
   const unsigned long long *kept = ub.kept[u];
   uint32_t my_raw = 0, my_new = 0;
   // Each thread takes a contiguous range of the flattened pair index and
   // walks it incrementally (one group lookup + triangular decode per thread).
-  const uint32_t chunk = (P + NT - 1) / NT;
-  uint32_t p = threadIdx.x * chunk;
-  const uint32_t pend = min(P, p + chunk);
+  const uint32_t pb = (uint32_t)((unsigned long long)P * slice / nslices);
+  const uint32_t pe = (uint32_t)((unsigned long long)P * (slice + 1) / nslices);
+  const uint32_t chunk = (pe - pb + NT - 1) / NT;
+  uint32_t p = pb + threadIdx.x * chunk;
+  const uint32_t pend = min(pe, p + chunk);
   if (p < pend) {
     uint32_t lo = 0, hi = R;  // r with pp[r] <= p < pp[r+1]
     while (hi - lo > 1) {
@@ -949,10 +962,11 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
     return;
   }
   for (int i = threadIdx.x; i < a.L; i += NT) S.b2b[i] = a.bit2blk[i];
-  const bool ok = process_bucket(S, a, ub, u, src, s, in_smem);
+  const bool ok = process_bucket(S, a, ub, u, src, s, in_smem, 0, 1, MSM_PAIR_SPLIT);
   if (!ok) {
-    // grouped rows exceed the member capacity: hand the bucket to the
-    // medium tier (it accepts any size up to its own capacity)
+    // grouped rows exceed the member capacity, or the groups hold more than
+    // MSM_PAIR_SPLIT pairs: hand the bucket to the medium tier (any size up
+    // to its own capacity, pairs split over MSM_MED_SLICES CTAs)
     if (a.tiled) {   // the smem stage is gone: re-gather into sel
       if (threadIdx.x == 0) S.ncand = (uint32_t)atomicAdd(a.sel_ctr, (unsigned long long)s);
       __syncthreads();
@@ -992,7 +1006,9 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
   Smem &S = *reinterpret_cast<Smem *>(smraw);
   const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
-  for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
+  for (unsigned long long wi = blockIdx.x; wi < nspill * MSM_MED_SLICES; wi += gridDim.x) {
+    const unsigned long long sb = wi / MSM_MED_SLICES;
+    const uint32_t slice = (uint32_t)(wi % MSM_MED_SLICES);
     const uint32_t s = a.spill[sb * 3 + 2];
     const uint32_t tag = a.spill[sb * 3];
     const bool requeued = tag & SPILL_FROM_SMALL;     // small tier ran out of member room
@@ -1001,7 +1017,8 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
       continue;
     const int u = (int)(tag & 0x3fffffffu);
     const uint32_t s0 = a.spill[sb * 3 + 1];
-    if (!process_bucket(S, a, ub, u, spill_elems(a, u, s0), s, false)) {
+    if (!process_bucket(S, a, ub, u, spill_elems(a, u, s0), s, false, slice, MSM_MED_SLICES) &&
+        slice == 0) {
       // still too many grouped rows: the tile kernel takes it
       if ((int64_t)s * 4 > a.n) {
         uint32_t *g = spill_gcnt(a, u, s0);
