@@ -161,15 +161,18 @@ __device__ __forceinline__ unsigned long long warp_append(bool pred,
   return base + __popc(mask & ((1u << lane) - 1u));
 }
 
-// Warp-aggregated append onto a shared-memory counter; `mask` is the
-// ballot of `pred` over the currently active lanes.
-__device__ __forceinline__ uint32_t smem_append(bool pred, unsigned mask, uint32_t *counter) {
+// Warp-aggregated append onto a shared-memory counter.  `active` is the
+// lane set captured ONCE by the caller (the same mask must be used for the
+// ballot and the broadcast: a second __activemask() may see a different set
+// after divergence, and lanes outside the shuffle would read garbage);
+// `mask` = __ballot_sync(active, pred).
+__device__ __forceinline__ uint32_t smem_append(unsigned active, unsigned mask,
+                                                uint32_t *counter) {
   const int lane = threadIdx.x & 31;
   const int leader = __ffs(mask) - 1;
   uint32_t base = 0;
   if (lane == leader) base = atomicAdd(counter, (uint32_t)__popc(mask));
-  base = __shfl_sync(__activemask(), base, leader);
-  (void)pred;
+  base = __shfl_sync(active, base, leader);
   return base + __popc(mask & ((1u << lane) - 1u));
 }
 

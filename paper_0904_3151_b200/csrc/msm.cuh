@@ -39,8 +39,10 @@ constexpr int MSM_TARGET = 3072;        // default target mean bucket size (tune
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 14;         // at most 16384 buckets per unit
 constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to this B
-constexpr uint32_t MSM_PAIR_SPLIT = 65536;  // small-tier buckets with more pairs -> medium
-constexpr int MSM_MED_SLICES = 8;       // medium tier: CTAs sharing one bucket's pairs
+#ifndef EG_PAIR_SPLIT
+#define EG_PAIR_SPLIT 65536u
+#endif
+constexpr uint32_t MSM_PAIR_SPLIT = EG_PAIR_SPLIT;  // small-tier buckets with more pairs -> medium
 
 constexpr int MSM_MAXT = 8;             // tail blocks of the O(1) canonical test
 
@@ -536,15 +538,15 @@ __device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
 // Returns false (without emitting anything) if the bucket's multi-row groups
 // hold more rows than the member capacity (CAP/2) or more groups than CAP/4;
 // the caller then re-queues it for the next tier.
-// slice / nslices: this CTA walks only its share of the bucket's flattened
-// pairs (the medium tier splits pair-heavy buckets over several CTAs);
-// pair_limit: return false (re-queue) when the bucket holds more pairs.
+// pair_limit: return false (re-queue) when the bucket's groups hold more
+// pairs.  (Splitting one bucket's flattened pairs over several CTAs would
+// need a canonical member order: group and member positions come from
+// shared-memory atomics and differ from CTA to CTA.)
 template <int W, int CAP, int NT, int MDIV>
 __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
                                                const MsmArgs &a, const UnitBatch &ub, int u,
                                                const uint64_t *el, uint32_t s,
-                                               bool el_in_smem, uint32_t slice = 0,
-                                               uint32_t nslices = 1,
+                                               bool el_in_smem,
                                                uint32_t pair_limit = 0xffffffffu) {
   constexpr int PT = CAP / NT;
   constexpr uint32_t MCAP = HGroupSmem<W, CAP, NT, MDIV>::MCAP;
@@ -737,11 +739,9 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   uint32_t my_raw = 0, my_new = 0;
   // Each thread takes a contiguous range of the flattened pair index and
   // walks it incrementally (one group lookup + triangular decode per thread).
-  const uint32_t pb = (uint32_t)((unsigned long long)P * slice / nslices);
-  const uint32_t pe = (uint32_t)((unsigned long long)P * (slice + 1) / nslices);
-  const uint32_t chunk = (pe - pb + NT - 1) / NT;
-  uint32_t p = pb + threadIdx.x * chunk;
-  const uint32_t pend = min(pe, p + chunk);
+  const uint32_t chunk = (P + NT - 1) / NT;
+  uint32_t p = threadIdx.x * chunk;
+  const uint32_t pend = min(P, p + chunk);
   if (p < pend) {
     uint32_t lo = 0, hi = R;  // r with pp[r] <= p < pp[r+1]
     while (hi - lo > 1) {
@@ -766,14 +766,19 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
       my_raw += v > 0;
       my_new += v == 2;
       const bool emit = v == 2;
-      const unsigned mask = __ballot_sync(__activemask(), emit);
+      const unsigned active = __activemask();
+      const unsigned mask = __ballot_sync(active, emit);
       if (mask) {   // stage in shared memory (global only on overflow)
         const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-        const uint32_t so = smem_append(emit, mask, &S.nout);
+        const uint32_t so = smem_append(active, mask, &S.nout);
         const bool spill = emit && so >= OUTCAP;
         if (emit && !spill) S.outbuf()[so] = key;
-        if (__any_sync(__activemask(), spill)) {
-          const unsigned long long slot = warp_append(spill, &a.ctr[0]);
+        const unsigned smask = __ballot_sync(active, spill);
+        if (smask) {
+          const int lane = threadIdx.x & 31, leader = __ffs(smask) - 1;
+          unsigned long long slot = 0;
+          if (lane == leader) slot = atomicAdd(&a.ctr[0], (unsigned long long)__popc(smask));
+          slot = __shfl_sync(active, slot, leader) + __popc(smask & ((1u << lane) - 1u));
           if (spill && slot < a.out_cap) {
             a.out_keys[slot] = key;
             if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
@@ -962,11 +967,12 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
     return;
   }
   for (int i = threadIdx.x; i < a.L; i += NT) S.b2b[i] = a.bit2blk[i];
-  const bool ok = process_bucket(S, a, ub, u, src, s, in_smem, 0, 1, MSM_PAIR_SPLIT);
+  const bool ok = process_bucket(S, a, ub, u, src, s, in_smem, MSM_PAIR_SPLIT);
   if (!ok) {
     // grouped rows exceed the member capacity, or the groups hold more than
     // MSM_PAIR_SPLIT pairs: hand the bucket to the medium tier (any size up
-    // to its own capacity, pairs split over MSM_MED_SLICES CTAs)
+    // to its own capacity; 512 threads per bucket, off the small tier's
+    // critical path)
     if (a.tiled) {   // the smem stage is gone: re-gather into sel
       if (threadIdx.x == 0) S.ncand = (uint32_t)atomicAdd(a.sel_ctr, (unsigned long long)s);
       __syncthreads();
@@ -1006,9 +1012,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
   Smem &S = *reinterpret_cast<Smem *>(smraw);
   const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
-  for (unsigned long long wi = blockIdx.x; wi < nspill * MSM_MED_SLICES; wi += gridDim.x) {
-    const unsigned long long sb = wi / MSM_MED_SLICES;
-    const uint32_t slice = (uint32_t)(wi % MSM_MED_SLICES);
+  for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
     const uint32_t s = a.spill[sb * 3 + 2];
     const uint32_t tag = a.spill[sb * 3];
     const bool requeued = tag & SPILL_FROM_SMALL;     // small tier ran out of member room
@@ -1017,8 +1021,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
       continue;
     const int u = (int)(tag & 0x3fffffffu);
     const uint32_t s0 = a.spill[sb * 3 + 1];
-    if (!process_bucket(S, a, ub, u, spill_elems(a, u, s0), s, false, slice, MSM_MED_SLICES) &&
-        slice == 0) {
+    if (!process_bucket(S, a, ub, u, spill_elems(a, u, s0), s, false)) {
       // still too many grouped rows: the tile kernel takes it
       if ((int64_t)s * 4 > a.n) {
         uint32_t *g = spill_gcnt(a, u, s0);

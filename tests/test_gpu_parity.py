@@ -526,3 +526,21 @@ def test_block_plan_keeps_reference_when_oversized(eg, caplog):
     assert engine._last_plan.get("chosen", 8) == 8
     assert any("group" in r.message for r in caplog.records)
     assert len(codes_pairs) >= (n // 3) * (n // 3 - 1) // 2
+
+
+@pytest.mark.parametrize("blocks", [4, 5, 6])
+def test_coarse_blocks_all_tiers_deterministic(eg, oracle, monkeypatch, blocks):
+    """Coarse forced block counts on skewed bits send buckets through every
+    tier (small, pair-heavy -> medium, giant -> tiles); the pair set must
+    equal the oracle's and be identical run to run."""
+    monkeypatch.setenv("EG_MSM_BLOCKS", str(blocks))
+    rng = np.random.default_rng(blocks + 100)
+    n, length, k, d = 50_000, 48, 12, 3
+    bits = (rng.random((n, length)) < 0.8).astype(np.uint8)
+    words = pack_bits(bits)
+    pool = eg.BitStringPool(words, length).partitioned(k)
+    first = eg.enumerate_pairs(pool, d).array
+    again = eg.enumerate_pairs(pool, d).array
+    np.testing.assert_array_equal(first, again)
+    want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+    np.testing.assert_array_equal(first, want)
