@@ -101,6 +101,24 @@ def sort_bytes_per_unit(n: int, cfg, blocks: int | None = None) -> int:
     return n * (8 * W + kb * 2 * (kb + 4))
 
 
+# Output counts of the reference's own CPU build at the full configs,
+# measured during the survey.
+REFERENCE_COUNTS = {
+    "cfg1": {"edges": 809_648, "candidates": 809_654},
+    "cfg2": {"edges": 500_000, "candidates": 500_000},
+    "cfg3": {"edges": 244_617, "candidates": 2_478_622, "raw": [1_942_637, 311_325, 713_791]},
+}
+
+
+def parity_vs_reference(config: str, counts):
+    ref = REFERENCE_COUNTS.get(config)
+    if not ref or not counts:
+        return None
+    got = {k: (list(counts[k]) if isinstance(counts.get(k), (list, tuple)) else counts.get(k))
+           for k in ref}
+    return {"reference": ref, "match": got == ref, "source": "SURVEY.md section 6 [measured]"}
+
+
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
     """SM clock + throttle reasons sampled during the timed region.
@@ -426,6 +444,7 @@ def main():
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
             "cpu_baseline": cpu, "stage_ms": stage_ms,
             "counts": distributed.last_counts(last),
+            "parity": parity_vs_reference(args.config, distributed.last_counts(last)),
         }
         print(json.dumps(out), flush=True)
     if world > 1:

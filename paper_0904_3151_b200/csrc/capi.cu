@@ -966,8 +966,16 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
                    uint8_t *d_keep, int64_t *h_new_counts, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (replicates < 1 || replicates > 255) return arg_error("eg_xrep_filter: replicates outside [1, 255]");
-  unsigned long long *nc;
-  EG_CUDA_TRY(cudaMallocAsync(&nc, 8 * (size_t)replicates, st));
+  // per-device counter block, allocated once: a stream-ordered allocation
+  // here released its pool at every synchronise and stalled some calls by
+  // tens of ms.  The mutex covers the call up to its final synchronise.
+  static std::mutex mu;
+  static unsigned long long *small[64];
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  EG_CUDA_TRY(cudaGetDevice(&dev));
+  if (!small[dev]) EG_CUDA_TRY(cudaMalloc(&small[dev], 8 * 256));
+  unsigned long long *nc = small[dev];
   EG_CUDA_TRY(cudaMemsetAsync(nc, 0, 8 * (size_t)replicates, st));
   if (m > 0) {
     unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
@@ -978,7 +986,6 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
   }
   std::vector<unsigned long long> h(replicates);
   EG_CUDA_TRY(cudaMemcpyAsync(h.data(), nc, 8 * (size_t)replicates, cudaMemcpyDeviceToHost, st));
-  EG_CUDA_TRY(cudaFreeAsync(nc, st));
   EG_CUDA_TRY(cudaStreamSynchronize(st));
   for (int i = 0; i < replicates; ++i) h_new_counts[i] = (int64_t)h[i];
   return EG_OK;

@@ -15,7 +15,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_0904_3151_b200 as eg  # noqa: E402
-from paper_0904_3151_b200 import distributed, engine, pipeline  # noqa: E402
+from paper_0904_3151_b200 import _native, distributed, engine, pipeline  # noqa: E402
 from paper_0904_3151_b200.workloads import CONFIGS  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -50,10 +50,25 @@ for nm in ["row_stats_async", "project_codes", "msm_plan", "msm_pairs", "raise_b
            "sort_pair_keys", "verify", "compact_keys"]:
     wrap(engine, nm)
 pipeline.engine = engine
+import gc  # noqa: E402
+gc_log = []
+
+
+def _gc_cb(phase, info):
+    if phase == "start":
+        _gc_cb.t = time.perf_counter()
+    else:
+        gc_log.append((info["generation"], (time.perf_counter() - _gc_cb.t) * 1e3))
+
+
+gc.callbacks.append(_gc_cb)
 for _ in range(3):
     distributed.build_step(x, params, cfg.metric, 1, 0)
 for rep in range(args.builds):
     marks.clear()
+    gc_log.clear()
+    prof = _native.Profile()
+    prof.start()
     torch.cuda.synchronize()
     s = torch.cuda.Event(enable_timing=True)
     s.record()
@@ -63,7 +78,13 @@ for rep in range(args.builds):
     e.record()
     torch.cuda.synchronize()
     print(f"--- build {rep}: device {s.elapsed_time(e):.3f} ms, host {(time.perf_counter() - t0) * 1e3:.3f} ms")
-    if args.quiet:
+    pr = prof.stop()
+    if gc_log:
+        print("   gc:", [(g, round(ms, 2)) for g, ms in gc_log])
+    if s.elapsed_time(e) >= 13.0:
+        print("   classes:", {k: (round(v["ms"], 3), v["count"]) for k, v in pr.items()})
+        print("   capacity hint:", dict(engine._capacity_hint))
+    if args.quiet and s.elapsed_time(e) < 13.0:
         continue
     prev = s
     for name, e0, e1, h0, h1 in marks:
