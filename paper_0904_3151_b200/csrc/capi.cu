@@ -253,22 +253,31 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
   // scatter of batch i+1 while a side stream groups batch i (the first is
   // L2/atomic bound, the second issue bound).  Events order the reuse of a
   // set and the final join.
-  static cudaStream_t side[64];
-  static cudaEvent_t ev_scat[64][2], ev_done[64][2];
+  // A third stream runs the tail tiers (medium / spill / max group) of
+  // batch i concurrently with the small-tier group kernel of batch i+1:
+  // the tails occupy few SMs (a handful of heavy buckets) and would
+  // otherwise serialise behind it.
+  static cudaStream_t side[64], tail[64];
+  static cudaEvent_t ev_scat[64][2], ev_grp[64][2], ev_done[64][2], ev_end[64];
   int dev = 0;
   cudaGetDevice(&dev);
   const bool two = lay.sets == 2;
   if (two && !side[dev]) {
     EG_CUDA_TRY(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
+    EG_CUDA_TRY(cudaStreamCreateWithFlags(&tail[dev], cudaStreamNonBlocking));
     for (int i = 0; i < 2; ++i) {
       EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_scat[dev][i], cudaEventDisableTiming));
+      EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_grp[dev][i], cudaEventDisableTiming));
       EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_done[dev][i], cudaEventDisableTiming));
     }
+    EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_end[dev], cudaEventDisableTiming));
   }
   cudaStream_t gs = two ? side[dev] : st;
-  if (two) {   // the side stream starts after everything already on st
+  cudaStream_t ts = two ? tail[dev] : st;
+  if (two) {   // the side streams start after everything already on st
     EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][0], st));
     EG_CUDA_TRY(cudaStreamWaitEvent(gs, ev_scat[dev][0], 0));
+    EG_CUDA_TRY(cudaStreamWaitEvent(ts, ev_scat[dev][0], 0));
   }
   for (size_t bi = 0; bi < batches.size(); ++bi) {
     const UnitBatch &ub = batches[bi];
@@ -305,24 +314,30 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
       EG_PROF(PC_MSM_GROUP, gs);
       k_msm_group<W><<<g4, SmallCfg<W>::NT, smem_group, gs>>>(x, ub);
     }
-    {
-      EG_PROF(PC_MSM_SPILL, gs);
-      k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, gs>>>(x, ub);
+    if (two) {
+      EG_CUDA_TRY(cudaEventRecord(ev_grp[dev][si], gs));
+      EG_CUDA_TRY(cudaStreamWaitEvent(ts, ev_grp[dev][si], 0));
     }
     {
-      EG_PROF(PC_MSM_SPILL, gs);
-      k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, gs>>>(x, ub);
+      EG_PROF(PC_MSM_SPILL, ts);
+      k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, ts>>>(x, ub);
     }
     {
-      EG_PROF(PC_MSM_SPILL, gs);
-      k_msm_spill_maxgroup<<<64, 256, 0, gs>>>(x);
+      EG_PROF(PC_MSM_SPILL, ts);
+      k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, ts>>>(x, ub);
     }
-    if (two) EG_CUDA_TRY(cudaEventRecord(ev_done[dev][si], gs));
+    {
+      EG_PROF(PC_MSM_SPILL, ts);
+      k_msm_spill_maxgroup<<<64, 256, 0, ts>>>(x);
+    }
+    if (two) EG_CUDA_TRY(cudaEventRecord(ev_done[dev][si], ts));
     EG_LAUNCH_CHECK();
   }
-  if (two) {
-    EG_CUDA_TRY(cudaEventRecord(ev_done[dev][0], gs));
+  if (two) {   // join: the tails are last on ts, the group kernels on gs
+    EG_CUDA_TRY(cudaEventRecord(ev_done[dev][0], ts));
     EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_done[dev][0], 0));
+    EG_CUDA_TRY(cudaEventRecord(ev_end[dev], gs));
+    EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_end[dev], 0));
   }
   return EG_OK;
 }

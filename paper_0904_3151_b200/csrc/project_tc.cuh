@@ -109,6 +109,21 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // Byte offset of (row, 16-byte chunk c) in a 128B-swizzled K-major tile.
 __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t c) {
   return row * 128u + ((c ^ (row & 7u)) << 4);
@@ -347,9 +362,7 @@ struct Tc2Bars {
   float xnorm[2][TC_M];      // fused row norms (times 1 + 1e-6) per accumulator buffer
   // epilogue column tables: word index (h * W + t / 64), bit (t % 64),
   // tau * ||r_c|| (fp32, rounded up)
-  uint16_t colw[TC_MAXN];
-  uint8_t colb[TC_MAXN];
-  float colband[TC_MAXN];
+  alignas(16) float colband[TC_MAXN];
 };
 
 __host__ __device__ inline size_t tc2_stage_bytes(int npad) {
@@ -381,12 +394,8 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         smem_u32(&B.tmem_base)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  for (int c = tid; c < npad; c += TC2_THREADS) {
-    const int h = c / L, t = c - h * L;
-    B.colw[c] = (uint16_t)(c < cols ? h * W + (t >> 6) : 0xffff);
-    B.colb[c] = (uint8_t)(t & 63);
+  for (int c = tid; c < TC_MAXN; c += TC2_THREADS)
     B.colband[c] = c < cols ? (float)(tau * rnorm[c] * (1.0 + 1e-6)) : 0.f;
-  }
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&B.full[s], 1);
@@ -517,40 +526,47 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       } else {
         xn = row_ok ? (float)(__ldg(xnorm + grow) * (1.0 + 1e-6)) : 0.f;
       }
-      uint64_t word = 0, uword = 0;
-      uint32_t cur_word = 0xffffffffu;
       // Each row's words are produced entirely by this thread, in column
-      // order, so they are stored (not OR-ed) when the word index changes.
-      auto flush = [&](void) {
-        if (cur_word != 0xffffffffu && row_ok) {
-          const int64_t idx = ((int64_t)(cur_word / W) * n + grow) * W + (cur_word % W);
-          codes[idx] = word;
-          unc_bits[idx] = uword;
-        }
-      };
-      for (int c0 = 0; c0 < ((exp_flags & 1) ? 0 : npad); c0 += 16) {
-        uint32_t acc[16];
-        tmem_ld16(tmem + b * 256 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, acc);
+      // order: (replicate h, bit t) advance with the column, a word is
+      // stored (not OR-ed) when it completes (64 bits or the row's end).
+      // Bands come from smem as float4s, accumulators 32 columns per
+      // tcgen05.ld.
+      uint64_t word = 0, uword = 0;
+      int h = 0, t = 0;
+      for (int c0 = 0; c0 < ((exp_flags & 1) ? 0 : cols); c0 += 32) {
+        uint32_t acc[32];
+        tmem_ld32(tmem + b * 256 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, acc);
+        float bnd[32];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int v = 0; v < 8; ++v)
+          *reinterpret_cast<float4 *>(&bnd[4 * v]) =
+              *reinterpret_cast<const float4 *>(&B.colband[c0 + 4 * v]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
           const int c = c0 + j;
-          const uint32_t wi = B.colw[c];
-          if (wi == 0xffffu) continue;
+          if (c >= cols) break;
           const float sv = __uint_as_float(acc[j]);
           if (dbg && row_ok) dbg[grow * cols + c] = sv;
-          const float band = B.colband[c] * xn + 1e-30f;
-          if (wi != cur_word) {
-            flush();
-            cur_word = wi;
-            word = 0;
-            uword = 0;
-          }
-          const uint64_t bit = 1ull << B.colb[c];
+          const float band = bnd[j] * xn + 1e-30f;
+          const uint64_t bit = 1ull << (t & 63);
           if (sv > band) word |= bit;
           else if (!(sv < -band)) uword |= bit;
+          ++t;
+          if ((t & 63) == 0 || t == L) {
+            if (row_ok) {
+              const int64_t idx = ((int64_t)h * n + grow) * W + ((t - 1) >> 6);
+              codes[idx] = word;
+              unc_bits[idx] = uword;
+            }
+            word = 0;
+            uword = 0;
+            if (t == L) {
+              t = 0;
+              ++h;
+            }
+          }
         }
       }
-      flush();
       tc_fence_before();
       mbar_arrive(&B.accempty[b]);
     }
