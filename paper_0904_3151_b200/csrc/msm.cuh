@@ -44,7 +44,7 @@ constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to thi
 #endif
 constexpr uint32_t MSM_PAIR_SPLIT = EG_PAIR_SPLIT;  // small-tier buckets with more pairs -> medium
 
-constexpr int MSM_MAXT = 8;             // tail blocks of the O(1) canonical test
+constexpr int MSM_MAXT = 4;             // tail blocks of the O(1) canonical test
 
 struct UnitBatch {
   int count;
@@ -407,34 +407,48 @@ __device__ __forceinline__ uint64_t canonical_mask(const uint64_t (&x)[W], const
 // unit's masked blocks M (x & kept == 0, so the differing-block set D is a
 // subset of M).  canonical(D) = D + the lowest d-|D| blocks outside D equals
 // M  iff  every block of M\D lies below the lowest kept block P  iff  every
-// block of M above P differs, i.e. x has a bit in each tail range.  O(|tail|)
-// word tests instead of a bit walk plus a fill loop.
+// block of M above P differs, i.e. x has a bit in each tail range.  The tail
+// ranges become W-word masks once per bucket (registers), so the test is
+// |tail| AND-and-compare steps instead of a bit walk plus a fill loop.
 template <int W>
-__device__ __forceinline__ bool canonical_tail_ok(const uint64_t (&x)[W], const UnitBatch &ub,
-                                                  int u) {
-  const int nt = ub.ntail[u];
-  for (int t = 0; t < nt; ++t) {
-    const int lo = ub.tail_lo[u][t], hi = ub.tail_hi[u][t];
-    uint64_t any = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w) {
+struct TailTest {
+  int nt;                          // tail blocks; > MSM_MAXT: general path
+  uint64_t maskbits;
+  const uint64_t *m;               // [MSM_MAXT][W] masks in shared memory
+  // every thread calls load (same u); the masks are written by the first
+  // MSM_MAXT * W threads -- the caller synchronises before the first ok()
+  __device__ __forceinline__ void load(const UnitBatch &ub, int u, uint64_t *sm) {
+    nt = ub.ntail[u];
+    maskbits = ub.maskbits[u];
+    m = sm;
+    const int i = threadIdx.x;
+    if (i < MSM_MAXT * W) {
+      const int t = i / W, w = i - t * W;
+      const int lo = t < nt ? ub.tail_lo[u][t] : 0, hi = t < nt ? ub.tail_hi[u][t] : 0;
       const int wl = max(lo - 64 * w, 0), wh = min(hi - 64 * w, 64);
-      if (wl < wh) {
-        const uint64_t m = (wh - wl == 64 ? ~0ull : ((1ull << (wh - wl)) - 1ull)) << wl;
-        any |= x[w] & m;
-      }
+      sm[i] = wl < wh ? (wh - wl == 64 ? ~0ull : ((1ull << (wh - wl)) - 1ull)) << wl : 0ull;
     }
-    if (!any) return false;
   }
-  return true;
-}
+  __device__ __forceinline__ bool ok(const uint64_t (&x)[W], int pc, const uint8_t *b2b, int k,
+                                     int d) const {
+    if (nt > MSM_MAXT) return canonical_mask<W>(x, b2b, k, d) == maskbits;
+    if (nt > pc) return false;       // every tail block needs a differing bit
+    for (int t = 0; t < nt; ++t) {
+      uint64_t any = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) any |= x[w] & m[t * W + w];
+      if (!any) return false;
+    }
+    return true;
+  }
+};
 
 // Full predicate for one in-group pair.  Returns 0 = rejected, 1 = raw only
 // (an earlier replicate owns it), 2 = emit.
 template <int W>
 __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint64_t (&cb)[W],
                                             uint32_t ra, uint32_t rb, const MsmArgs &a,
-                                            const UnitBatch &ub, int u,
+                                            const TailTest<W> &tt,
                                             const unsigned long long *kept, int rep,
                                             const uint8_t *b2b) {
   uint64_t x[W];
@@ -447,11 +461,7 @@ __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint6
     keydiff |= x[w] & kept[w];
   }
   if (keydiff || pc > a.d) return 0;
-  if (ub.ntail[u] <= MSM_MAXT) {
-    if (!canonical_tail_ok<W>(x, ub, u)) return 0;
-  } else if (canonical_mask<W>(x, b2b, a.k, a.d) != ub.maskbits[u]) {
-    return 0;
-  }
+  if (!tt.ok(x, pc, b2b, a.k, a.d)) return 0;
   if (a.out_rep) return 2;
   for (int g = 0; g < rep; ++g) {
     const uint64_t *cg = a.codes + (int64_t)g * a.n * W;
@@ -511,6 +521,7 @@ struct HGroupSmem {
   unsigned long long sw[NT / 32];
   uint32_t nruns, maxrun, raw, neu, ncand, nout;
   unsigned long long obase;
+  uint64_t tmask[MSM_MAXT * W];    // tail masks of the bucket's unit (TailTest)
   // Emitted pairs are staged here during the pair loop (the table is dead
   // by then; with OVERLAY only the part past the member arrays is free) and
   // written out with one global reservation per bucket.
@@ -736,6 +747,9 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     return false;
   }
   const unsigned long long *kept = ub.kept[u];
+  TailTest<W> tt;
+  tt.load(ub, u, S.tmask);
+  __syncthreads();
   uint32_t my_raw = 0, my_new = 0;
   // Each thread takes a contiguous range of the flattened pair index and
   // walks it incrementally (one group lookup + triangular decode per thread).
@@ -762,7 +776,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
 #pragma unroll
       for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + ib) * W + w];
       const uint32_t rb = mrows[start + ib];
-      const int v = pair_verdict<W>(ca, cb, ra, rb, a, ub, u, kept, rep, S.b2b);
+      const int v = pair_verdict<W>(ca, cb, ra, rb, a, tt, kept, rep, S.b2b);
       my_raw += v > 0;
       my_new += v == 2;
       const bool emit = v == 2;
@@ -1049,6 +1063,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
                                                                 const __grid_constant__ UnitBatch ub) {
   __shared__ uint64_t ea[MSM_SPILL_T], eb[MSM_SPILL_T];
   __shared__ uint64_t cb_s[MSM_SPILL_T * W];
+  __shared__ uint64_t tmask_s[MSM_MAXT * W];
   __shared__ uint8_t b2b[EG_MAX_LENGTH];
   __shared__ uint32_t sraw, sneu;
   for (int i = threadIdx.x; i < a.L; i += MSM_SPILL_T) b2b[i] = a.bit2blk[i];
@@ -1062,6 +1077,9 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
     const unsigned long long ntp = (unsigned long long)nt * (nt + 1) / 2;
     const int rep = ub.rep[u];
     const unsigned long long *kept = ub.kept[u];
+    TailTest<W> tt;
+    __syncthreads();                  // previous entry done with tmask_s
+    tt.load(ub, u, tmask_s);
     const uint64_t *el = spill_elems(a, u, s0);
     const uint64_t *codes = a.codes + (int64_t)rep * a.n * W;
     const bool count_groups = (int64_t)s * 4 > a.n;
@@ -1114,7 +1132,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
               ++my_eq;
               if (count_groups) atomicAdd(&gc[ib0 + j], 1u);
               const uint32_t rb = (uint32_t)f;
-              int v = pair_verdict<W>(ca, cb, ra, rb, a, ub, u, kept, rep, b2b);
+              int v = pair_verdict<W>(ca, cb, ra, rb, a, tt, kept, rep, b2b);
               my_raw += v > 0;
               my_new += v == 2;
               emit = v == 2;
