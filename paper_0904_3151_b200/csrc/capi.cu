@@ -146,14 +146,16 @@ static int env_int(const char *name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
-static int msm_lgb(int64_t n) {
-  // mean bucket size: the tuned target, but never above 80% of the small
-  // tier's capacity (so Poisson tails and fully clustered buckets still fit)
-  const int64_t cap_mean = (int64_t)(0.8 * SmallCfg<1>::CAP);
+static int msm_buckets(int64_t n) {
+  // mean bucket size: the tuned target, but never above EG_MSM_FILL (default
+  // 80%) of the small tier's capacity.  Buckets are hash-balanced (Poisson,
+  // sd = sqrt(mean)), so the few that overflow go to the medium tier.
+  const double fill = env_int("EG_MSM_FILL", 80) / 100.0;
+  const int64_t cap_mean = (int64_t)(fill * SmallCfg<1>::CAP);
   const int64_t tgt = std::min<int64_t>(env_int("EG_MSM_TARGET", MSM_TARGET), cap_mean);
-  int64_t target = (n + tgt - 1) / tgt;
-  int l = ilog2_ceil((uint64_t)(target < 1 ? 1 : target));
-  return l > MSM_MAX_LGB ? MSM_MAX_LGB : l;
+  int64_t b = (n + tgt - 1) / tgt;
+  if (b < 1) b = 1;
+  return (int)std::min<int64_t>(b, (int64_t)1 << MSM_MAX_LGB);
 }
 
 static int msm_batch_units(int64_t n) {
@@ -172,8 +174,8 @@ struct MsmLayout {
 
 static MsmLayout msm_layout(int64_t n, int reps) {
   MsmLayout l;
-  l.lgB = msm_lgb(n);
-  l.B = 1 << l.lgB;
+  l.B = msm_buckets(n);
+  l.lgB = ilog2_ceil((uint64_t)l.B);
   l.U = msm_batch_units(n);
   // two scratch sets: batch i+1's hist/scatter overlap batch i's grouping
   l.sets = env_int("EG_MSM_STREAMS", 2) >= 2 ? 2 : 1;
@@ -440,6 +442,17 @@ static bool make_x_tensor_map(CUtensorMap *map, const void *d_x, int64_t n, int 
 // accumulator (n x cols) here (used to validate the error band).
 static float *g_tc_debug = nullptr;
 extern "C" void eg_debug_set_tc_dump(float *d_buf) { g_tc_debug = d_buf; }
+// Debug: copy (and optionally reset) the MSM bucket counters (all zero
+// unless the library was compiled with -DEG_MSM_STATS=1).
+extern "C" int eg_debug_msm_stats(unsigned long long *out8, int reset) {
+  if (cudaMemcpyFromSymbol(out8, eg::g_msm_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return EG_ERR_CUDA;
+  if (reset) {
+    static const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(eg::g_msm_stats, z, sizeof(z)) != cudaSuccess) return EG_ERR_CUDA;
+  }
+  return EG_OK;
+}
 
 // Shared body of eg_project / eg_project_rows.  d_bad != nullptr: also
 // produce the row norms into d_norms (and the bad-row flags) -- fused into
@@ -872,6 +885,7 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   a.k = k;
   a.d = d;
   a.lgB = lay.lgB;
+  a.B = lay.B;
   a.reps = replicates;
   uint8_t *b2b_d = ar.take<uint8_t>(EG_MAX_LENGTH);
   a.bit2blk = b2b_d;

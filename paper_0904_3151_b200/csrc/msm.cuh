@@ -64,6 +64,7 @@ struct MsmArgs {
   const uint64_t *codes;         // [reps][n][W]
   int64_t n;
   int L, W, k, d, lgB, reps;
+  int B;                         // buckets per unit (any count <= 2^MSM_MAX_LGB)
   uint32_t *counts;              // [MAXU][B]
   uint32_t *starts;              // [MAXU][B+1]
   uint32_t *cursor;              // [MAXU][B]
@@ -104,6 +105,12 @@ __device__ __forceinline__ void load_code(const uint64_t *__restrict__ codes, in
   }
 }
 
+// MSD bucket of a key hash: multiply-high of the top 32 bits (any bucket
+// count, not only powers of two; the low 32 bits stay the secondary key h2).
+__device__ __forceinline__ uint32_t bucket_of(uint64_t h, int B) {
+  return (uint32_t)(((h >> 32) * (uint64_t)(uint32_t)B) >> 32);
+}
+
 // ------------------------------------------------------------------ 1
 // Bucket histogram for every unit of the batch: each CTA reads its code tile
 // once (registers) and hashes it under each unit's mask, so the codes cross
@@ -114,9 +121,8 @@ template <int W>
 __global__ void __launch_bounds__(MSM_NT) k_msm_hist(const __grid_constant__ MsmArgs a,
                                                      const __grid_constant__ UnitBatch ub) {
   extern __shared__ uint32_t hist[];
-  const int B = 1 << a.lgB;
+  const int B = a.B;
   const int upp = max(1, min(ub.count, (int)(a.hist_smem / (B * 4))));
-  const int sh = 64 - a.lgB;
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
   // all units of one batch share a replicate except at replicate boundaries
   for (int u0 = 0; u0 < ub.count; u0 += upp) {
@@ -144,7 +150,7 @@ __global__ void __launch_bounds__(MSM_NT) k_msm_hist(const __grid_constant__ Msm
         const int64_t row = base + (int64_t)i * MSM_NT + threadIdx.x;
         if (row < a.n) {
           const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
-          atomicAdd(&hu[a.lgB ? (uint32_t)(h >> sh) : 0u], 1u);
+          atomicAdd(&hu[bucket_of(h, B)], 1u);
         }
       }
     }
@@ -161,7 +167,7 @@ __global__ void __launch_bounds__(MSM_NT) k_msm_hist(const __grid_constant__ Msm
 __global__ void __launch_bounds__(1024) k_msm_scan(const __grid_constant__ MsmArgs a) {
   __shared__ uint32_t sw[32];
   const int u = blockIdx.x;
-  const int B = 1 << a.lgB;
+  const int B = a.B;
   uint32_t *cnt = a.counts + (int64_t)u * B;
   uint32_t *st = a.starts + (int64_t)u * (B + 1);
   uint32_t *cur = a.cursor + (int64_t)u * B;
@@ -197,7 +203,7 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
                                                               const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smsc[];
   const int u = blockIdx.y;
-  const int B = 1 << a.lgB;
+  const int B = a.B;
   const bool staged = a.scatter_staged;
   uint64_t *stage = reinterpret_cast<uint64_t *>(smsc);                    // [MSM_TILE]
   uint16_t *sbk = reinterpret_cast<uint16_t *>(stage + MSM_TILE);        // [MSM_TILE]
@@ -211,7 +217,6 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
   const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
   const unsigned long long *kept = ub.kept[u];
   const uint64_t salt = ub.salt[u];
-  const int sh = 64 - a.lgB;
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
   constexpr int IPT = MSM_TILE / MSM_SC_NT;
   // (bucket << 13) | rank: B <= 2^14, rank < MSM_TILE = 2^13
@@ -231,7 +236,7 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
       const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
       if (row < a.n) {
         const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
-        const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
+        const uint32_t b = bucket_of(h, B);
         h2[i] = (uint32_t)h;
         br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
       }
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_tsort(const __grid_constan
                                                             const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smts[];
   const int u = blockIdx.y;
-  const int B = 1 << a.lgB;
+  const int B = a.B;
   uint64_t *stage = reinterpret_cast<uint64_t *>(smts);                    // [MSM_TILE]
   uint32_t *hist = reinterpret_cast<uint32_t *>(stage + MSM_TILE);       // [B]
   __shared__ uint32_t sw[MSM_SC_NT / 32];
@@ -315,7 +320,6 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_tsort(const __grid_constan
   const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
   const unsigned long long *kept = ub.kept[u];
   const uint64_t salt = ub.salt[u];
-  const int sh = 64 - a.lgB;
   const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
   constexpr int IPT = MSM_TILE / MSM_SC_NT;
   uint32_t br[IPT], h2[IPT];
@@ -333,7 +337,7 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_tsort(const __grid_constan
       const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
       if (row < a.n) {
         const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
-        const uint32_t b = a.lgB ? (uint32_t)(h >> sh) : 0u;
+        const uint32_t b = bucket_of(h, B);
         h2[i] = (uint32_t)h;
         br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
       }
@@ -474,6 +478,38 @@ __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint6
   return 2;
 }
 
+// pair_verdict with the second row read lazily (only the in-kernel
+// cross-replicate rule needs it).
+template <int W>
+__device__ __forceinline__ int pair_verdict_rows(const uint64_t (&ca)[W], const uint64_t (&cb)[W],
+                                                 uint32_t ra, const uint32_t *mrows, uint32_t ib,
+                                                 const MsmArgs &a, const TailTest<W> &tt,
+                                                 const unsigned long long *kept, int rep,
+                                                 const uint8_t *b2b) {
+  uint64_t x[W];
+  int pc = 0;
+  uint64_t keydiff = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    x[w] = ca[w] ^ cb[w];
+    pc += __popcll(x[w]);
+    keydiff |= x[w] & kept[w];
+  }
+  if (keydiff || pc > a.d) return 0;
+  if (!tt.ok(x, pc, b2b, a.k, a.d)) return 0;
+  if (a.out_rep) return 2;
+  const uint32_t rb = mrows[ib];
+  for (int g = 0; g < rep; ++g) {
+    const uint64_t *cg = a.codes + (int64_t)g * a.n * W;
+    int pg = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w)
+      pg += __popcll(__ldg(cg + (int64_t)ra * W + w) ^ __ldg(cg + (int64_t)rb * W + w));
+    if (pg <= a.d) return 1;
+  }
+  return 2;
+}
+
 __device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia, uint32_t &ib) {
   // pairs (0,1),(0,2),..,(0,c-1),(1,2),...; T(a) = a*c - a*(a+1)/2
   float disc = (float)(2 * c - 1) * (float)(2 * c - 1) - 8.0f * (float)q;
@@ -497,6 +533,15 @@ __device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia,
 // hamming_join.py:116-122) and applies pair_verdict.
 #ifndef EG_SMALL_MDIV
 #define EG_SMALL_MDIV 1
+#endif
+#ifndef EG_GROUP_FILTER
+#define EG_GROUP_FILTER 1
+#endif
+#ifndef EG_PAIR_WARPVOTE
+#define EG_PAIR_WARPVOTE 0
+#endif
+#ifndef EG_RANK_ATOMIC32
+#define EG_RANK_ATOMIC32 1
 #endif
 // Member capacity of a bucket tier: CAP / MDIV grouped rows, half as many
 // groups.
@@ -542,6 +587,14 @@ struct HGroupSmem {
 
 constexpr unsigned long long HG_EMPTY = ~0ull;
 
+// Optional per-bucket counters (compile with -DEG_MSM_STATS=1): buckets
+// reaching the group stage, rows, filter candidates, groups, grouped rows,
+// in-group pair visits.  Read with eg_debug_msm_stats.
+#ifndef EG_MSM_STATS
+#define EG_MSM_STATS 0
+#endif
+__device__ unsigned long long g_msm_stats[8];
+
 __device__ __forceinline__ uint32_t pow2_at_least(uint32_t v) {
   return v <= 1 ? 1u : 1u << (32 - __clz(v - 1));
 }
@@ -572,6 +625,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     e[j] = i < s ? el[i] : 0ull;
   }
   if (el_in_smem) __syncthreads();   // the stage overlays the table
+#if EG_GROUP_FILTER
   // 2. atomic-free singleton filter: every row writes its local index into
   //    a slot chosen by the high bits of h2 (plain stores, last writer
   //    wins); a row that reads back someone else's index, or finds its slot
@@ -637,6 +691,22 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     }
     __syncthreads();
   }
+#else
+  // no prefilter: every row enters the exact table (cheaper when most rows
+  // sit in multi-row groups)
+  uint32_t cand = 0;
+#pragma unroll
+  for (int j = 0; j < PT; ++j)
+    if (threadIdx.x + j * NT < s) cand |= 1u << j;
+  const uint32_t ncand = s;
+  if (threadIdx.x == 0) {
+    S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; S.nout = 0;
+  }
+  if (ncand == 0) {
+    __syncthreads();
+    return true;
+  }
+#endif
   const uint32_t T = pow2_at_least(2 * ncand);
   for (uint32_t i = threadIdx.x * 2; i < T; i += NT * 2)
     *reinterpret_cast<ulonglong2 *>(&S.tab()[i]) = make_ulonglong2(HG_EMPTY, HG_EMPTY);
@@ -655,7 +725,13 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
         const unsigned long long old = atomicCAS(&S.tab()[slot], HG_EMPTY, mine);
         if (old == HG_EMPTY) break;
         if ((uint32_t)(old >> 32) == h2) {
+          // 32-bit add on the count word (a 64-bit shared atomic add is a
+          // CAS loop, which a large group's members serialise on)
+#if EG_RANK_ATOMIC32
+          rank = atomicAdd(reinterpret_cast<uint32_t *>(&S.tab()[slot]), 1u);
+#else
           rank = (uint32_t)atomicAdd(&S.tab()[slot], 1ull);
+#endif
           break;
         }
         slot = (slot + 1) & (T - 1);
@@ -720,6 +796,16 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     }
   }
   if (threadIdx.x == 0) S.pp[R] = (uint32_t)tot;
+#if EG_MSM_STATS
+  if (threadIdx.x == 0) {
+    atomicAdd(&g_msm_stats[0], 1ull);
+    atomicAdd(&g_msm_stats[1], (unsigned long long)s);
+    atomicAdd(&g_msm_stats[2], (unsigned long long)ncand);
+    atomicAdd(&g_msm_stats[3], (unsigned long long)R);
+    atomicAdd(&g_msm_stats[4], tot >> 32);
+    atomicAdd(&g_msm_stats[5], tot & 0xffffffffull);
+  }
+#endif
   __syncthreads();
   // member positions out of the table first; then the (possibly overlaid)
   // member arrays are written
@@ -741,7 +827,11 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   }
   __syncthreads();
   // 5. every in-group pair once (load-balanced over the CTA)
+#if EG_EXP_NOPAIRS   // timing experiment only: skip the pair loop
+  const uint32_t P = 0;
+#else
   const uint32_t P = S.pp[R];
+#endif
   if (P > pair_limit) {    // uniform: hand the bucket to the sliced medium tier
     __syncthreads();
     return false;
@@ -775,6 +865,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
       uint64_t cb[W];
 #pragma unroll
       for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + ib) * W + w];
+#if EG_PAIR_WARPVOTE
       const uint32_t rb = mrows[start + ib];
       const int v = pair_verdict<W>(ca, cb, ra, rb, a, tt, kept, rep, S.b2b);
       my_raw += v > 0;
@@ -799,6 +890,31 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
           }
         }
       }
+#else
+      // Emits are rare next to visits (a few per thousand at the planned
+      // block count): no per-visit warp vote; an emitting lane takes its
+      // staging slot with its own shared-memory atomic, and the row index
+      // is read only then.
+      const int v = pair_verdict_rows<W>(ca, cb, ra, mrows, start + ib, a, tt, kept, rep, S.b2b);
+      if (v) {
+        my_raw += 1;
+        if (v == 2) {
+          ++my_new;
+          const uint32_t rb = mrows[start + ib];
+          const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+          const uint32_t so = atomicAdd(&S.nout, 1u);
+          if (so < OUTCAP) {
+            S.outbuf()[so] = key;
+          } else {
+            const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
+            if (slot < a.out_cap) {
+              a.out_keys[slot] = key;
+              if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+            }
+          }
+        }
+      }
+#endif
       // advance (ia, ib) in (0,1),(0,2),..,(1,2),.. order, crossing groups
       if (++ib == len) {
         if (++ia == len - 1) {
@@ -892,7 +1008,7 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
   Smem &S = *reinterpret_cast<Smem *>(smraw);
   const int u = blockIdx.y;
   const int b = blockIdx.x;
-  const int B = 1 << a.lgB;
+  const int B = a.B;
   uint32_t s0 = 0, s = 0;
   const uint64_t *src = nullptr;
   bool in_smem = false;

@@ -3,6 +3,7 @@
     python tools/blocks_sweep.py --config cfg3 --blocks 6,8,10,12,auto
 """
 import argparse
+import ctypes
 import os
 import sys
 import time
@@ -63,3 +64,11 @@ for b in args.blocks.split(","):
           f"group={best[1].get('msm_group')} spill={best[1].get('msm_spill')} "
           f"max_group={c['max_group']} plan={engine._last_plan}{ok}", flush=True)
     print("   ", best[1], flush=True)
+    try:
+        st = (ctypes.c_ulonglong * 8)()
+        _native.lib().eg_debug_msm_stats(st, 1)
+        if st[0]:
+            print("    msm stats (last build window): buckets %d rows %d cand %d groups %d grouped %d pairs %d"
+                  % tuple(st[:6]), flush=True)
+    except AttributeError:
+        pass
