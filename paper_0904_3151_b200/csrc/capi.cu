@@ -538,7 +538,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
     if (tma_ok) {
       const size_t sbytes = tc2_stage_bytes(npad);
-      const int nstages = (int)std::min<size_t>(4, ((size_t)212 << 10) / sbytes);
+      const int nstages = (int)std::min<size_t>(env_int("EG_TC2_STAGES", 4), ((size_t)212 << 10) / sbytes);
       const size_t smem = nstages * sbytes + sizeof(Tc2Bars) + 1024;
       static size_t tc2_smem_set = 0;
       if (smem > tc2_smem_set) {

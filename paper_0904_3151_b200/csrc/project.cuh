@@ -25,15 +25,17 @@ __global__ void __launch_bounds__(ROWST_WARPS * 32) k_row_stats(const TX *__rest
                                                    double *__restrict__ norms,
                                                    unsigned long long *__restrict__ bad) {
   // One warp per 32 rows: 32x32 tiles staged through shared memory with
-  // coalesced loads; each lane then adds its own row's squares in ascending
-  // q (fma, fp64) -- the order the tensor-core projection's converters use,
-  // so both paths produce bit-identical norms.
+  // coalesced loads; each lane then adds its own row's squares (fma, fp64)
+  // into eight partial sums by (q mod 32 >= 16, q mod 4), each in ascending
+  // q, combined pairwise -- the order the tensor-core projection's two
+  // converter threads per row use, so both paths give bit-identical norms.
   __shared__ TX tile[ROWST_WARPS][32][33];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t r0 = ((int64_t)blockIdx.x * ROWST_WARPS + wib) * 32;
   if (r0 >= n) return;
   const int64_t row = r0 + lane;
-  double s = 0.0;
+  // partial sums by (q mod 32 >= 16, q mod 4), each in ascending q
+  double s8[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
   bool finite = true;
   for (int q0 = 0; q0 < dim; q0 += 32) {
     const int q = q0 + lane;
@@ -41,14 +43,16 @@ __global__ void __launch_bounds__(ROWST_WARPS * 32) k_row_stats(const TX *__rest
     for (int e = 0; e < 32; ++e)
       tile[wib][e][lane] = (r0 + e < n && q < dim) ? x[(r0 + e) * dim + q] : (TX)0;
     __syncwarp();
-    const int qn = min(32, dim - q0);
-    for (int j = 0; j < qn; ++j) {
+    // OOB columns are zero: fma(0, 0, s) == s, so every row sums 32 columns
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
       const double v = (double)tile[wib][lane][j];
       finite &= isfinite(v);
-      s = fma(v, v, s);
+      s8[(j >> 4) * 4 + (j & 3)] = fma(v, v, s8[(j >> 4) * 4 + (j & 3)]);
     }
     __syncwarp();
   }
+  const double s = ((s8[0] + s8[1]) + (s8[2] + s8[3])) + ((s8[4] + s8[5]) + (s8[6] + s8[7]));
   if (row < n) {
     norms[row] = sqrt(s);
     if (!finite) atomicMin(&bad[0], (unsigned long long)row);

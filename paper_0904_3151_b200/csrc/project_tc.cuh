@@ -326,7 +326,7 @@ __global__ void __launch_bounds__(TC_NT, 1) k_project_tc(
 //                 list; arrive accempty[b]
 // Stages are ring-buffered with mbarrier phase parity; the accumulator is
 // double-buffered so the epilogue of tile t overlaps the MMAs of tile t+1.
-constexpr int TC2_THREADS = 384;
+constexpr int TC2_THREADS = 512;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -359,7 +359,7 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 struct Tc2Bars {
   uint64_t full[4], conv[4], empty[4], accfull[2], accempty[2], normfull[2], normempty[2];
   uint32_t tmem_base;
-  float xnorm[2][TC_M];      // fused row norms (times 1 + 1e-6) per accumulator buffer
+  double xss[2][2][TC_M];    // fused half-row sums of squares [buffer][half][row]
   // epilogue column tables: word index (h * W + t / 64), bit (t % 64),
   // tau * ||r_c|| (fp32, rounded up)
   alignas(16) float colband[TC_MAXN];
@@ -399,13 +399,13 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
   if (tid == 0) {
     for (int s = 0; s < nstages; ++s) {
       mbar_init(&B.full[s], 1);
-      mbar_init(&B.conv[s], 128);
+      mbar_init(&B.conv[s], 256);
       mbar_init(&B.empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&B.accfull[b], 1);
       mbar_init(&B.accempty[b], 128);
-      mbar_init(&B.normfull[b], 128);
+      mbar_init(&B.normfull[b], 256);
       mbar_init(&B.normempty[b], 128);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -464,12 +464,16 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         }
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 12) {
     // ---------------------------------------------------------- converters
-    const uint32_t row = (uint32_t)(tid - 128);
+    // two threads per row: warps 4-7 take 16-byte chunks 0-3 of the row's
+    // 128-byte K chunk, warps 8-11 chunks 4-7
+    const uint32_t row = (uint32_t)((warp & 3) * 32 + lane), half = (uint32_t)(warp - 4) >> 2;
     uint32_t it = 0, t = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
-      double ss = 0.0;
+      // four interleaved partial sums per half (q mod 4; k_row_stats uses
+      // the same order), so each fp64 fma chain is an eighth of the row
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       for (int kc = 0; kc < nkc; ++kc, ++it) {
         const int s = it % nstages;
         const uint32_t use = it / nstages;
@@ -477,14 +481,14 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         float *xh = reinterpret_cast<float *>(smem + s * sb);
         float *xl = xh + TC_M * TC_BK;
 #pragma unroll
-        for (int c = 0; c < ((exp_flags & 2) ? 0 : 8); ++c) {
-          const uint32_t off = sw128_off(row, (uint32_t)c) / 4;
+        for (int cc = 0; cc < ((exp_flags & 2) ? 0 : 4); ++cc) {
+          const uint32_t off = sw128_off(row, half * 4 + (uint32_t)cc) / 4;
           const float4 v = *reinterpret_cast<const float4 *>(xh + off);
-          if (fuse) {        // OOB columns are TMA zero-fill: fma(0, 0, s) == s
-            ss = fma((double)v.x, (double)v.x, ss);
-            ss = fma((double)v.y, (double)v.y, ss);
-            ss = fma((double)v.z, (double)v.z, ss);
-            ss = fma((double)v.w, (double)v.w, ss);
+          if (fuse && !(exp_flags & 8)) {   // OOB columns are TMA zero-fill: fma(0, 0, s) == s
+            s0 = fma((double)v.x, (double)v.x, s0);
+            s1 = fma((double)v.y, (double)v.y, s1);
+            s2 = fma((double)v.z, (double)v.z, s2);
+            s3 = fma((double)v.w, (double)v.w, s3);
           }
           const float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
           *reinterpret_cast<float4 *>(xh + off) = h;
@@ -496,21 +500,14 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       }
       if (fuse) {
         const uint32_t b = t & 1, buse = t >> 1;
-        const int64_t grow = tile * TC_M + row;
-        const double nrm = sqrt(ss);
-        if (grow < n) {
-          norms_out[grow] = nrm;
-          if (!isfinite(ss)) atomicMin(&bad[0], (unsigned long long)grow);
-          if (ss == 0.0) atomicMin(&bad[1], (unsigned long long)grow);
-        }
         mbar_wait(&B.normempty[b], (buse & 1) ^ 1);
-        B.xnorm[b][row] = grow < n ? (float)(nrm * (1.0 + 1e-6)) : 0.f;
+        B.xss[b][half][row] = (exp_flags & 8) ? 0.5 : (s0 + s1) + (s2 + s3);
         mbar_arrive(&B.normfull[b]);
       }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp - 8;                       // == warp % 4: TMEM lane quarter
+    const int q = warp - 12;                      // == warp % 4: TMEM lane quarter
     uint32_t t = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
       const uint32_t b = t & 1, buse = t >> 1;
@@ -520,20 +517,29 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       const bool row_ok = grow < n;
       float xn;
       if (fuse) {
+        // the row's norm: the two halves' sums, then the flags (as k_row_stats)
         mbar_wait(&B.normfull[b], buse & 1);
-        xn = B.xnorm[b][q * 32 + lane];
+        const double ss = B.xss[b][0][q * 32 + lane] + B.xss[b][1][q * 32 + lane];
         mbar_arrive(&B.normempty[b]);
+        const double nrm = sqrt(ss);
+        if (row_ok) {
+          norms_out[grow] = nrm;
+          if (!isfinite(ss)) atomicMin(&bad[0], (unsigned long long)grow);
+          if (ss == 0.0) atomicMin(&bad[1], (unsigned long long)grow);
+        }
+        xn = row_ok ? (float)(nrm * (1.0 + 1e-6)) : 0.f;
       } else {
         xn = row_ok ? (float)(__ldg(xnorm + grow) * (1.0 + 1e-6)) : 0.f;
       }
       // Each row's words are produced entirely by this thread, in column
-      // order: (replicate h, bit t) advance with the column, a word is
-      // stored (not OR-ed) when it completes (64 bits or the row's end).
-      // Bands come from smem as float4s, accumulators 32 columns per
-      // tcgen05.ld.
+      // order.  Per 32-column group the certified signs and the band flags
+      // become two 32-bit masks (one predicated OR per column); the masks
+      // are then cut at replicate / word boundaries into the row's code
+      // words (a word is stored, not OR-ed, when it completes).
+      const int ncols = (exp_flags & 1) ? 0 : cols;
       uint64_t word = 0, uword = 0;
-      int h = 0, t = 0;
-      for (int c0 = 0; c0 < ((exp_flags & 1) ? 0 : cols); c0 += 32) {
+      int h = 0, t = 0;                 // (replicate, bit) of column c0
+      for (int c0 = 0; c0 < ncols; c0 += 32) {
         uint32_t acc[32];
         tmem_ld32(tmem + b * 256 + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, acc);
         float bnd[32];
@@ -541,18 +547,31 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         for (int v = 0; v < 8; ++v)
           *reinterpret_cast<float4 *>(&bnd[4 * v]) =
               *reinterpret_cast<const float4 *>(&B.colband[c0 + 4 * v]);
+        uint32_t pos = 0, unc = 0;
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const int c = c0 + j;
-          if (c >= cols) break;
           const float sv = __uint_as_float(acc[j]);
-          if (dbg && row_ok) dbg[grow * cols + c] = sv;
           const float band = bnd[j] * xn + 1e-30f;
-          const uint64_t bit = 1ull << (t & 63);
-          if (sv > band) word |= bit;
-          else if (!(sv < -band)) uword |= bit;
-          ++t;
-          if ((t & 63) == 0 || t == L) {
+          if (sv > band) pos |= 1u << j;
+          else if (!(sv < -band)) unc |= 1u << j;
+        }
+        if (dbg && row_ok) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (c0 + j < cols) dbg[grow * cols + c0 + j] = __uint_as_float(acc[j]);
+        }
+        int j = 0;
+        const int jend = min(32, ncols - c0);
+        while (j < jend) {
+          // segment: columns up to the end of the current word / replicate
+          const int wend = min(L, ((t >> 6) + 1) << 6);
+          const int len = min(jend - j, wend - t);
+          const uint64_t m = len >= 32 ? 0xffffffffull : ((1ull << len) - 1ull);
+          word |= ((uint64_t)(pos >> j) & m) << (t & 63);
+          uword |= ((uint64_t)(unc >> j) & m) << (t & 63);
+          t += len;
+          j += len;
+          if (t == wend) {
             if (row_ok) {
               const int64_t idx = ((int64_t)h * n + grow) * W + ((t - 1) >> 6);
               codes[idx] = word;
