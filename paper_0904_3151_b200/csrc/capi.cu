@@ -569,16 +569,30 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
         k_collect_bits<<<(unsigned)std::min<int64_t>((words + per - 1) / per,
                                                      (int64_t)num_sms() * 8),
                          COLLECT_NT, 0, st>>>(unc, n, W, length, replicates, items, cnt, cap);
-        const size_t fxs = fixl_smem(cols);
-        static size_t fixl_set = 0;
-        if (fxs > 48 * 1024 && fxs > fixl_set) {
-          EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_list,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)fxs));
-          fixl_set = fxs;
+        if (env_int("EG_FIXUP_LIST", 0)) {   // thread-per-entry variant (comparison)
+          const size_t fxs = fixl_smem(cols);
+          static size_t fixl_set = 0;
+          if (fxs > 48 * 1024 && fxs > fixl_set) {
+            EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_list,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)fxs));
+            fixl_set = fxs;
+          }
+          k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
+              (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
+        } else {
+          const size_t fws = (size_t)(FIXW_NT / 32) * dim * 8;
+          static size_t fixw_set = 0;
+          if (fws > 48 * 1024 && fws > fixw_set) {
+            EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_warp,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)fws));
+            fixw_set = fws;
+          }
+          k_fixup_warp<<<(unsigned)num_sms() * 8, FIXW_NT, fws, st>>>(
+              (const float *)d_x, dim, d_r, n, length, W, d_codes, items, cnt, cap,
+              env_int("EG_FIXUP_FORCE_SEQ", 0));
         }
-        k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
-            (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
         const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
         if (fsm > 48 * 1024)
           EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_bits,
@@ -1154,12 +1168,25 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   unsigned grid = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)num_sms() * 64);
   {
   EG_PROF(PC_VERIFY, st);
+  const int vu = (!x_is_f64 && dim % 4 == 0 && dim <= 128 * VER_VU) ? (dim + 127) / 128 : 0;
   if (x_is_f64)
-    k_verify<double><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, d_keys, m,
-                                           metric, eps, flags, dist, bad);
+    k_verify<double, 0><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, d_keys, m,
+                                              metric, eps, flags, dist, bad);
+  else if (vu == 1)
+    k_verify<float, 1><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m,
+                                             metric, eps, flags, dist, bad);
+  else if (vu == 2)
+    k_verify<float, 2><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m,
+                                             metric, eps, flags, dist, bad);
+  else if (vu == 3)
+    k_verify<float, 3><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m,
+                                             metric, eps, flags, dist, bad);
+  else if (vu == 4)
+    k_verify<float, 4><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m,
+                                             metric, eps, flags, dist, bad);
   else
-    k_verify<float><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m, metric,
-                                          eps, flags, dist, bad);
+    k_verify<float, 0><<<grid, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m,
+                                             metric, eps, flags, dist, bad);
   }
   EG_LAUNCH_CHECK();
   int rc = compact<double>(d_keys, dist, flags, m, d_out_keys, d_out_dist, h_count, ar, st);

@@ -701,6 +701,78 @@ __global__ void __launch_bounds__(FIXL_NT) k_fixup_list(
   }
 }
 
+// Band entries, one warp per entry (the production fix-up).  The lanes form
+// the entry's separately rounded products x_q * r_q (__dmul_rn, as the
+// reference), add them in a fixed tree and also add S = sum |x_q r_q|.  The
+// reference's sequential sum differs from the exact dot product by at most
+// (D + 1) u S (u = 2^-53: D product roundings and D additions, each bounded
+// by u S), and so does the tree sum; when |tree| exceeds twice that bound
+// (inflated by 1 %) the exact value, and with it the sequential sum, has the
+// tree's sign.  Otherwise (|dot| within ~1e-13 relative of zero, exact
+// zeros included) lane 0 redoes the reference's sequential sum in ascending
+// q from the products staged in shared memory (lsh.py:107-112).
+constexpr int FIXW_NT = 256;
+__global__ void __launch_bounds__(FIXW_NT) k_fixup_warp(
+    const float *__restrict__ x, int dim, const double *__restrict__ r, int64_t n, int L, int W,
+    uint64_t *__restrict__ codes, const unsigned long long *__restrict__ items,
+    const unsigned long long *__restrict__ count, unsigned long long cap, int force_seq) {
+  extern __shared__ double fw_prod[];                 // [warps][dim] (fallback only)
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  double *prod = fw_prod + (size_t)wib * dim;
+  const unsigned long long total = min(*count, cap);
+  const unsigned long long nw = (unsigned long long)gridDim.x * (FIXW_NT / 32);
+  // force_seq (tests): every entry takes the sequential path
+  const double bound = force_seq ? INFINITY : 2.02 * (double)(dim + 1) * 0x1p-53;
+  for (unsigned long long e = (unsigned long long)blockIdx.x * (FIXW_NT / 32) + wib; e < total;
+       e += nw) {
+    const unsigned long long it = items[e];
+    const int64_t row = (int64_t)(it >> 32);
+    const int c = (int)(it & 0xffffffffu);
+    const float *xr = x + row * dim;
+    const double *rr = r + (int64_t)c * dim;
+    double sum = 0.0, sabs = 0.0;
+    constexpr int U = 4;
+    for (int q0 = lane; q0 < dim; q0 += 32 * U) {
+      float xv[U];
+      double rv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int q = q0 + 32 * u;
+        xv[u] = q < dim ? __ldg(xr + q) : 0.f;
+        rv[u] = q < dim ? __ldg(rr + q) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double p = __dmul_rn((double)xv[u], rv[u]);
+        sum += p;
+        sabs += fabs(p);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      sabs += __shfl_xor_sync(0xffffffffu, sabs, o);
+    }
+    bool pos;
+    if (fabs(sum) > bound * sabs) {
+      pos = sum > 0.0;
+    } else {
+      for (int q = lane; q < dim; q += 32) prod[q] = __dmul_rn((double)__ldg(xr + q), __ldg(rr + q));
+      __syncwarp();
+      double acc = 0.0;
+      if (lane == 0)
+        for (int q = 0; q < dim; ++q) acc = __dadd_rn(acc, prod[q]);
+      pos = __shfl_sync(0xffffffffu, acc, 0) > 0.0;
+      __syncwarp();
+    }
+    if (lane == 0 && pos) {
+      const int h = c / L, t = c - h * L;
+      atomicOr((unsigned long long *)&codes[((int64_t)h * n + row) * W + (t >> 6)],
+               1ull << (t & 63));
+    }
+  }
+}
+
 // Exact recompute of the band entries flagged in the bitmap (same layout as
 // the codes) -- the overflow path of k_collect_bits/k_fixup_list (exits at
 // once unless the list overflowed).  One warp per 32 rows: lanes compute the

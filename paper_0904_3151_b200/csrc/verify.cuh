@@ -45,7 +45,25 @@ __device__ __forceinline__ void accum_pair(const TX *__restrict__ xi, const TX *
   }
 }
 
-template <typename TX>
+// Fast path (fp32 rows, dim % 4 == 0, dim <= 512): each warp takes a
+// contiguous run of the (i, j)-sorted candidates, so consecutive pairs share
+// x_i, which stays in registers (each lane holds its <= 4 float4 slices);
+// only x_j is loaded per pair, all of a lane's slices at once.  Same
+// per-lane summation order as accum_pair, so distances are identical.
+constexpr int VER_VU = 4;
+template <int VU>
+__device__ __forceinline__ void ver_load_row(const float *__restrict__ xr, int d4, int lane,
+                                             float4 (&v)[VU]) {
+  const float4 *x4 = reinterpret_cast<const float4 *>(xr);
+#pragma unroll
+  for (int u = 0; u < VU; ++u) {
+    const int q = lane + 32 * u;
+    v[u] = q < d4 ? __ldg(x4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+// VU = ceil(dim / 128) float4 slices per lane on the fast path (0: general path)
+template <typename TX, int VU>
 __global__ void __launch_bounds__(256) k_verify(const TX *__restrict__ x, int64_t n, int dim,
                                                 const double *__restrict__ norms,
                                                 const uint64_t *__restrict__ keys, int64_t m,
@@ -55,7 +73,60 @@ __global__ void __launch_bounds__(256) k_verify(const TX *__restrict__ x, int64_
                                                 unsigned long long *__restrict__ bad) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * 8;
-  for (int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); p < m; p += warps) {
+  const int64_t wid = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if constexpr (VU > 0) {
+    const int d4 = dim / 4;
+    const int64_t per = (m + warps - 1) / warps;
+    const int64_t p0 = wid * per, p1 = min(m, p0 + per);
+    int64_t cur = -1;
+    float4 a[VU];
+    for (int64_t p = p0; p < p1; ++p) {
+      const uint64_t key = keys[p];
+      const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+      if (!(i < n && j < n)) {
+        if (lane == 0) { atomicMin(bad, (unsigned long long)p); flags[p] = 0; dist[p] = 0.0; }
+        continue;
+      }
+      float4 b[VU];
+      ver_load_row(reinterpret_cast<const float *>(x) + j * dim, d4, lane, b);
+      if (i != cur) {
+        ver_load_row(reinterpret_cast<const float *>(x) + i * dim, d4, lane, a);
+        cur = i;
+      }
+      double acc = 0.0;
+#pragma unroll
+      for (int u = 0; u < VU; ++u) {
+        if (lane + 32 * u >= d4) break;
+        if (metric == EG_METRIC_COSINE) {
+          acc = fma((double)a[u].x, (double)b[u].x, acc);
+          acc = fma((double)a[u].y, (double)b[u].y, acc);
+          acc = fma((double)a[u].z, (double)b[u].z, acc);
+          acc = fma((double)a[u].w, (double)b[u].w, acc);
+        } else {
+          double t;
+          t = (double)a[u].x - (double)b[u].x; acc = fma(t, t, acc);
+          t = (double)a[u].y - (double)b[u].y; acc = fma(t, t, acc);
+          t = (double)a[u].z - (double)b[u].z; acc = fma(t, t, acc);
+          t = (double)a[u].w - (double)b[u].w; acc = fma(t, t, acc);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        double dd;
+        if (metric == EG_METRIC_COSINE) {
+          dd = 1.0 - acc / (norms[i] * norms[j]);
+          dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
+        } else {
+          dd = sqrt(acc);
+        }
+        dist[p] = dd;
+        flags[p] = dd <= eps;
+      }
+    }
+    return;
+  }
+  for (int64_t p = wid; p < m; p += warps) {
     const uint64_t key = keys[p];
     const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
     if (!(i < n && j < n)) {

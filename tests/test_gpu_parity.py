@@ -290,7 +290,8 @@ def test_build_edge_cases(eg):
         eg.build_graph(x, params)
 
 
-@pytest.mark.parametrize("env", [{}, {"EG_PROJECT_UNFUSED": "1"}, {"EG_PROJECT_SIMT": "1"}])
+@pytest.mark.parametrize("env", [{}, {"EG_PROJECT_UNFUSED": "1"}, {"EG_PROJECT_SIMT": "1"},
+                                 {"EG_FIXUP_FORCE_SEQ": "1"}, {"EG_FIXUP_LIST": "1"}])
 def test_fused_norms_and_flags(eg, oracle, monkeypatch, env):
     """eg_project_rows: norms accumulated inside the tensor-core projection
     are bit-identical to k_row_stats' (unfused and SIMT paths), codes equal
