@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "msm.cuh"
 #include "plan.cuh"
+#include "project_h16.cuh"
 #include "project.cuh"
 #include "project_tc.cuh"
 #include <cudaTypedefs.h>
@@ -410,7 +411,8 @@ size_t eg_project_workspace(int64_t n, int32_t dim, int32_t length, int32_t repl
   return ws_bytes((size_t)dim * cols_pad, 4) + ws_bytes(1, 8) +
          ws_bytes(fixup_cap(n, cols), 8) +
          ws_bytes((size_t)((dim + TC_BK - 1) / TC_BK) * 2 * npad * TC_BK, 4) +
-         ws_bytes((size_t)replicates * n * ((length + 63) / 64), 8) + 2048;
+         ws_bytes((size_t)replicates * n * ((length + 63) / 64), 8) + ws_bytes(TC_MAXN, 8) +
+         2048;
 }
 
 // TMA descriptor of the row-major fp32 rows: box = 32 columns (128 B, one
@@ -481,6 +483,59 @@ int eg_project_rows(const void *d_x, int x_is_f64, int64_t n, int32_t dim, doubl
                       d_workspace, workspace_bytes, d_fixups, d_bad, (cudaStream_t)stream);
 }
 
+// Exact recompute of the band entries flagged in `unc` (the codes layout):
+// entry list (k_collect_bits), warp-per-entry fix-up, and the bitmap pass
+// that redoes everything if the list overflowed.
+static int run_band_fixup(const void *d_x, int32_t dim, const double *d_r, int64_t n,
+                          int32_t length, int W, int32_t replicates, int cols, uint64_t *d_codes,
+                          uint64_t *unc, unsigned long long *items, unsigned long long *cnt,
+                          unsigned long long cap, uint64_t *d_fixups, cudaStream_t st) {
+  {
+    EG_PROF(PC_FIXUP, st);
+    const int64_t words = (int64_t)replicates * n * W;
+    const int64_t per = (int64_t)COLLECT_NT * COLLECT_WPT;
+    k_collect_bits<<<(unsigned)std::min<int64_t>((words + per - 1) / per,
+                                                 (int64_t)num_sms() * 8),
+                     COLLECT_NT, 0, st>>>(unc, n, W, length, replicates, items, cnt, cap);
+    if (env_int("EG_FIXUP_LIST", 0)) {   // thread-per-entry variant (comparison)
+      const size_t fxs = fixl_smem(cols);
+      static size_t fixl_set = 0;
+      if (fxs > 48 * 1024 && fxs > fixl_set) {
+        EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_list,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fxs));
+        fixl_set = fxs;
+      }
+      k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
+          (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
+    } else {
+      const size_t fws = (size_t)(FIXW_NT / 32) * dim * 8;
+      static size_t fixw_set = 0;
+      if (fws > 48 * 1024 && fws > fixw_set) {
+        EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_warp,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)fws));
+        fixw_set = fws;
+      }
+      k_fixup_warp<<<(unsigned)num_sms() * 8, FIXW_NT, fws, st>>>(
+          (const float *)d_x, dim, d_r, n, length, W, d_codes, items, cnt, cap,
+          env_int("EG_FIXUP_FORCE_SEQ", 0));
+    }
+    const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
+    if (fsm > 48 * 1024)
+      EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_bits,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)fsm));
+    const unsigned fg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    k_fixup_bits<<<fg, 256, fsm, st>>>((const float *)d_x, n, dim, d_r, length, W,
+                                       replicates, d_codes, unc, cnt, cap);
+  }
+  EG_LAUNCH_CHECK();
+  if (d_fixups)
+    EG_CUDA_TRY(cudaMemcpyAsync(d_fixups, cnt, 8, cudaMemcpyDeviceToDevice, st));
+  return EG_OK;
+}
+
 static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, double *d_norms,
                         const double *d_r, const double *d_rnorm, int32_t length,
                         int32_t replicates, uint64_t *d_codes, void *d_workspace,
@@ -536,6 +591,47 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
     EG_LAUNCH_CHECK();
     const int64_t ntiles = (n + TC_M - 1) / TC_M;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
+    const int h16_no = std::max(2, std::min(H16_MAXSLOTS, env_int("EG_H16_OSLOTS", 2)));
+    const int h16_npad = std::max(npad, std::min(TC_MAXN, env_int("EG_H16_NPAD", 0)) / 16 * 16);
+    const bool h16 = tma_ok && !env_int("EG_PROJECT_TF32", 0) && h16_fits(h16_npad, h16_no);
+    if (h16) {
+      // kind::f16 (2-term fp16 splits): the production path for fp32 rows
+      double *colscale = ar.take<double>(TC_MAXN);
+      uint64_t *unc = ar.take<uint64_t>((size_t)replicates * n * W);
+      if (!colscale || !unc) {
+        set_error("eg_project: workspace too small");
+        return EG_ERR_WORKSPACE;
+      }
+      __half *himg = reinterpret_cast<__half *>(img);
+      {
+        EG_PROF(PC_MISC, st);
+        k_h16_prep_directions<<<h16_npad, 128, 0, st>>>(d_r, cols, dim, h16_npad, himg, colscale);
+      }
+      EG_LAUNCH_CHECK();
+      const size_t ob = h16_oslot_bytes(h16_npad);
+      const int no = h16_no;
+      const size_t budget = ((size_t)220 << 10) - sizeof(H16Bars) - 1024;
+      const int nx = (int)std::min<size_t>(env_int("EG_H16_XSLOTS", H16_MAXSLOTS),
+                                           (budget - no * ob) / H16_XSLOT);
+      if (nx < 2) return arg_error("eg_project: too many direction columns for the f16 path");
+      const size_t smem = nx * H16_XSLOT + no * ob + sizeof(H16Bars) + 1024;
+      static size_t h16_smem_set = 0;
+      if (smem > h16_smem_set) {
+        EG_CUDA_TRY(cudaFuncSetAttribute(k_project_h16,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        h16_smem_set = smem;
+      }
+      {
+        EG_PROF(PC_PROJECT, st);
+        k_project_h16<<<grid, H16_THREADS, smem, st>>>(
+            xmap, n, dim, himg, colscale, cols, h16_npad, nx, no, d_norms, d_rnorm, h16_tau(dim),
+            length, W, d_codes, unc, g_tc_debug, fuse ? d_norms : nullptr,
+            fuse ? (unsigned long long *)d_bad : nullptr, env_int("EG_TC_EXP", 0));
+      }
+      EG_LAUNCH_CHECK();
+      return run_band_fixup(d_x, dim, d_r, n, length, W, replicates, cols, d_codes, unc, items,
+                            cnt, cap, d_fixups, st);
+    }
     if (tma_ok) {
       const size_t sbytes = tc2_stage_bytes(npad);
       const int nstages = (int)std::min<size_t>(env_int("EG_TC2_STAGES", 4), ((size_t)212 << 10) / sbytes);
@@ -562,50 +658,8 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
                                                             : nullptr);
       }
       EG_LAUNCH_CHECK();
-      {
-        EG_PROF(PC_FIXUP, st);
-        const int64_t words = (int64_t)replicates * n * W;
-        const int64_t per = (int64_t)COLLECT_NT * COLLECT_WPT;
-        k_collect_bits<<<(unsigned)std::min<int64_t>((words + per - 1) / per,
-                                                     (int64_t)num_sms() * 8),
-                         COLLECT_NT, 0, st>>>(unc, n, W, length, replicates, items, cnt, cap);
-        if (env_int("EG_FIXUP_LIST", 0)) {   // thread-per-entry variant (comparison)
-          const size_t fxs = fixl_smem(cols);
-          static size_t fixl_set = 0;
-          if (fxs > 48 * 1024 && fxs > fixl_set) {
-            EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_list,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)fxs));
-            fixl_set = fxs;
-          }
-          k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
-              (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
-        } else {
-          const size_t fws = (size_t)(FIXW_NT / 32) * dim * 8;
-          static size_t fixw_set = 0;
-          if (fws > 48 * 1024 && fws > fixw_set) {
-            EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_warp,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)fws));
-            fixw_set = fws;
-          }
-          k_fixup_warp<<<(unsigned)num_sms() * 8, FIXW_NT, fws, st>>>(
-              (const float *)d_x, dim, d_r, n, length, W, d_codes, items, cnt, cap,
-              env_int("EG_FIXUP_FORCE_SEQ", 0));
-        }
-        const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
-        if (fsm > 48 * 1024)
-          EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_bits,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)fsm));
-        const unsigned fg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
-        k_fixup_bits<<<fg, 256, fsm, st>>>((const float *)d_x, n, dim, d_r, length, W,
-                                           replicates, d_codes, unc, cnt, cap);
-      }
-      EG_LAUNCH_CHECK();
-      if (d_fixups)
-        EG_CUDA_TRY(cudaMemcpyAsync(d_fixups, cnt, 8, cudaMemcpyDeviceToDevice, st));
-      return EG_OK;
+      return run_band_fixup(d_x, dim, d_r, n, length, W, replicates, cols, d_codes, unc, items,
+                            cnt, cap, d_fixups, st);
     } else {
       const size_t smem = 2 * tc_stage_bytes(npad) + sizeof(TcSmem) + 1024;
       static size_t tc_smem_set = 0;

@@ -378,19 +378,27 @@ def test_cfg5_small_euclidean(eg, oracle, manifest):
                   workloads.cfg5_points(40_000, clusters=2_000), metric="euclidean")
 
 
-def _tc_tau(dim):
-    import math
-    mmas = 3.0 * ((dim + 7) // 8)
-    return 2.0 * (mmas * 2.0 ** -22 + 3.0 * 2.0 ** -20) + dim * 2.0 ** -52
+def _tc_tau(dim, tf32):
+    """Relative band of the tensor-core projection (project_tc.cuh tc_tau,
+    project_h16.cuh h16_tau)."""
+    if tf32:
+        mmas = 3.0 * ((dim + 7) // 8)
+        return 2.0 * (mmas * 2.0 ** -22 + 3.0 * 2.0 ** -20) + dim * 2.0 ** -52
+    mmas = 3.0 * ((dim + 15) // 16)
+    return 2.0 * (mmas + 3.0) * 2.0 ** -22 + dim * 2.0 ** -52
 
 
+@pytest.mark.parametrize("tf32", [False, True])
 @pytest.mark.parametrize("n,dim,length,reps", [(20000, 384, 48, 3), (7000, 100, 64, 2),
                                                (5000, 128, 64, 1), (3000, 64, 32, 1)])
-def test_tc_projection_error_band(eg, oracle, n, dim, length, reps):
-    """The tensor-core (3xTF32) projection's raw accumulator stays well inside
-    the certified band it uses to decide signs; signs equal the oracle."""
+def test_tc_projection_error_band(eg, oracle, monkeypatch, n, dim, length, reps, tf32):
+    """The tensor-core projection's raw accumulator (kind::f16 2-term fp16
+    splits by default, kind::tf32 3xTF32 with EG_PROJECT_TF32=1) stays well
+    inside the certified band it uses to decide signs; signs equal the
+    oracle."""
     import torch
     from paper_0904_3151_b200 import _native, engine
+    monkeypatch.setenv("EG_PROJECT_TF32", "1" if tf32 else "0")
     rng = np.random.default_rng(n + dim)
     x = rng.standard_normal((n, dim)).astype(np.float32)
     x[: n // 4] = np.abs(x[: n // 4])          # skewed rows like config 3
@@ -411,7 +419,7 @@ def test_tc_projection_error_band(eg, oracle, n, dim, length, reps):
     exact = x.astype(np.float64) @ r.T
     scale = np.linalg.norm(x.astype(np.float64), axis=1)[:, None] * np.linalg.norm(r, axis=1)[None, :]
     ratio = np.abs(acc - exact) / scale
-    tau = _tc_tau(dim)
+    tau = _tc_tau(dim, tf32)
     print(f"tc band: max err/(|x||r|) = {ratio.max():.3e}, tau = {tau:.3e}, "
           f"in-band share = {np.mean(np.abs(exact) <= tau * scale):.2e}")
     assert ratio.max() < tau / 2, (ratio.max(), tau)
@@ -545,3 +553,21 @@ def test_coarse_blocks_all_tiers_deterministic(eg, oracle, monkeypatch, blocks):
     np.testing.assert_array_equal(first, again)
     want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
     np.testing.assert_array_equal(first, want)
+
+
+@pytest.mark.parametrize("tf32", ["0", "1"])
+def test_projection_extreme_magnitudes(eg, oracle, monkeypatch, tf32):
+    """Rows outside the fp16 range of the kind::f16 split: entries >= 2^15
+    (the row goes to the exact fix-up whole), rows of tiny magnitude (fp16
+    subnormals: the absolute floor of the band) and mixed-scale rows --
+    codes still bit-exact with the oracle."""
+    monkeypatch.setenv("EG_PROJECT_TF32", tf32)
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((4000, 96)).astype(np.float32)
+    x[:500] *= np.float32(1e5)                         # fp16 overflow
+    x[500:1000] *= np.float32(1e-6)                    # fp16 subnormal range
+    x[1000:1500, ::3] *= np.float32(3e4)               # mixed scales
+    x[1500:1600] = np.abs(x[1500:1600]) * np.float32(1e-30)
+    for rep in (1, 2):
+        got = eg.project(x, eg.ProjectionSpec(64, 3, rep)).words
+        np.testing.assert_array_equal(got, oracle.project_words(x, 64, 3, rep))
