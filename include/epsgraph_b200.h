@@ -236,6 +236,29 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
               int64_t *h_count, void *d_workspace, size_t workspace_bytes,
               void *stream);
 
+/* --------------------------------------------------------------------- */
+/* Exhaustive oracle on the GPU.                   */
+/* eg_bf_cosine_candidates replaces the all-pairs product of              */
+/* exact.brute_force_cosine (exact.py:57-95): every pair i < j whose      */
+/* cosine distance can be <= eps (fp16 tensor-core screen with a          */
+/* certified margin) as keys (i << 32) | j, unordered.  The exact fp64    */
+/* decision and distance come from eg_verify on the sorted keys.          */
+/* h_count receives the candidate count; when it exceeds cap only cap     */
+/* keys were written (call again with a larger buffer).  dim <= 512.      */
+/* eg_bf_hamming replaces exact.brute_force_hamming (exact.py:98-121):    */
+/* all pairs i < j with popcount(c_i ^ c_j) <= d (words <= 4), unordered, */
+/* same capacity contract.  Both synchronise the stream before return.    */
+/* --------------------------------------------------------------------- */
+size_t eg_bf_cosine_workspace(int64_t n, int32_t dim);
+int eg_bf_cosine_candidates(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
+                            const double *d_norms, double eps, uint64_t *d_keys,
+                            int64_t cap, int64_t *h_count, void *d_workspace,
+                            size_t workspace_bytes, void *stream);
+size_t eg_bf_hamming_workspace(void);
+int eg_bf_hamming(const uint64_t *d_codes, int64_t n, int32_t words, int32_t d,
+                  uint64_t *d_keys, int64_t cap, int64_t *h_count, void *d_workspace,
+                  size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,10 @@ def _declare(lib):
         "eg_compact_keys": ([P, P, i64, P, P, P, sz, P], I),
         "eg_verify_workspace": ([i64], sz),
         "eg_verify": ([P, I, i64, i32, P, P, i64, i32, dbl, P, P, P, P, sz, P], I),
+        "eg_bf_cosine_workspace": ([i64, i32], sz),
+        "eg_bf_cosine_candidates": ([P, I, i64, i32, P, dbl, P, i64, P, P, sz, P], I),
+        "eg_bf_hamming_workspace": ([], sz),
+        "eg_bf_hamming": ([P, i64, i32, i32, P, i64, P, P, sz, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

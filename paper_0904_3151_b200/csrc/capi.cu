@@ -15,6 +15,7 @@
 #include "msm.cuh"
 #include "plan.cuh"
 #include "project_h16.cuh"
+#include "exact.cuh"
 #include "project.cuh"
 #include "project_tc.cuh"
 #include <cudaTypedefs.h>
@@ -1252,6 +1253,132 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
     set_error("eg_verify: candidate %llu has an index out of range", hb);
     return EG_ERR_ARG;
   }
+  return EG_OK;
+}
+
+
+// ------------------------------------------------------ exhaustive oracle
+// TMA descriptor of the fp16 unit rows (row stride dp): box 64 x rows, SW128.
+static bool make_f16_map(CUtensorMap *map, const void *d_u, int64_t n, int dp, int rows) {
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = (PFN_cuTensorMapEncodeTiled)fn;
+  }
+  cuuint64_t gdim[2] = {(cuuint64_t)dp, (cuuint64_t)n};
+  cuuint64_t gstride[1] = {(cuuint64_t)dp * 2};
+  cuuint32_t box[2] = {BF_BK, (cuuint32_t)rows};
+  cuuint32_t estride[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void *>(d_u), gdim, gstride,
+                box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t eg_bf_cosine_workspace(int64_t n, int32_t dim) {
+  return ws_bytes((size_t)n * bf_dpad(dim), 2) + ws_bytes(1, 8) + 1024;
+}
+
+int eg_bf_cosine_candidates(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
+                            const double *d_norms, double eps, uint64_t *d_keys, int64_t cap,
+                            int64_t *h_count, void *d_workspace, size_t workspace_bytes,
+                            void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *h_count = 0;
+  if (n < 0 || dim < 1 || cap < 0) return arg_error("eg_bf_cosine_candidates: bad shape");
+  if (n >= (1ll << 31)) return arg_error("eg_bf_cosine_candidates: too many rows");
+  const int dp = bf_dpad(dim);
+  if (dp > 512)
+    {
+      set_error("eg_bf_cosine_candidates: dim > 512 (the A tile is kept in shared memory)");
+      return EG_ERR_UNSUPPORTED;
+    }
+  if (n < 2) return EG_OK;
+  Arena ar(d_workspace, workspace_bytes);
+  __half *u = ar.take<__half>((size_t)n * dp);
+  unsigned long long *cnt = ar.take<unsigned long long>(1);
+  if (!u || !cnt) {
+    set_error("eg_bf_cosine_candidates: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
+  EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
+  const unsigned g = (unsigned)std::min<int64_t>((n * dp + 255) / 256, (int64_t)num_sms() * 16);
+  if (x_is_f64)
+    k_unit_f16<double><<<g, 256, 0, st>>>((const double *)d_x, n, dim, dp, d_norms, u);
+  else
+    k_unit_f16<float><<<g, 256, 0, st>>>((const float *)d_x, n, dim, dp, d_norms, u);
+  EG_LAUNCH_CHECK();
+  CUtensorMap amap, bmap;
+  if (!make_f16_map(&amap, u, n, dp, BF_BM) || !make_f16_map(&bmap, u, n, dp, BF_BN))
+    {
+    set_error("eg_bf_cosine_candidates: tensor map encoding failed");
+    return EG_ERR_UNSUPPORTED;
+  }
+  // screen: fp16 unit rows (2 x 2^-11 relative each, 2^-25 subnormal floor)
+  // and fp32 accumulation over dp / 16 MMAs -- |error| < 1.1e-3 for unit
+  // rows; 4x margin
+  const double delta = 4.0 * (2.0 * ldexp(1.0, -11) + ldexp(1.0, -22) +
+                              sqrt((double)dp) * ldexp(1.0, -24) +
+                              (dp / 16) * ldexp(1.0, -22));
+  const float thr = (float)(1.0 - eps - delta);
+  const int nkc = dp / BF_BK;
+  const size_t budget = ((size_t)220 << 10) - sizeof(BfBars) - 1024;
+  const int nb = (int)std::min<size_t>(BF_MAXSTAGES, (budget - nkc * BF_ACHUNK) / BF_BSTAGE);
+  const size_t smem = nkc * BF_ACHUNK + nb * BF_BSTAGE + sizeof(BfBars) + 1024;
+  static size_t bf_smem_set = 0;
+  if (smem > bf_smem_set) {
+    EG_CUDA_TRY(cudaFuncSetAttribute(k_bf_cosine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    bf_smem_set = smem;
+  }
+  const int64_t ti = (n + BF_BM - 1) / BF_BM;
+  const unsigned grid = (unsigned)std::min<int64_t>(ti, (int64_t)num_sms());
+  {
+    EG_PROF(PC_VERIFY, st);
+    k_bf_cosine_tc<<<grid, BF_THREADS, smem, st>>>(amap, bmap, n, dp, nb, thr,
+                                                   (unsigned long long *)d_keys,
+                                                   (unsigned long long)cap, cnt);
+  }
+  EG_LAUNCH_CHECK();
+  EG_CUDA_TRY(cudaMemcpyAsync(h_count, cnt, 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  return EG_OK;
+}
+
+size_t eg_bf_hamming_workspace(void) { return ws_bytes(1, 8) + 256; }
+
+int eg_bf_hamming(const uint64_t *d_codes, int64_t n, int32_t words, int32_t d, uint64_t *d_keys,
+                  int64_t cap, int64_t *h_count, void *d_workspace, size_t workspace_bytes,
+                  void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *h_count = 0;
+  if (n < 0 || words < 1 || words > BFH_MAXW || d < 0 || cap < 0)
+    return arg_error("eg_bf_hamming: bad arguments");
+  if (n >= (1ll << 32)) return arg_error("eg_bf_hamming: too many rows");
+  if (n < 2) return EG_OK;
+  Arena ar(d_workspace, workspace_bytes);
+  unsigned long long *cnt = ar.take<unsigned long long>(1);
+  if (!cnt) {
+    set_error("eg_bf_hamming: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
+  EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
+  const int64_t nblk = (n + BFH_ROWS - 1) / BFH_ROWS;
+  dim3 grid((unsigned)std::max<int64_t>(1, std::min<int64_t>((n + BFH_NT - 1) / BFH_NT, 64)),
+            (unsigned)std::min<int64_t>(nblk, 65535));
+  {
+    EG_PROF(PC_MSM_GROUP, st);
+    k_bf_hamming<<<grid, BFH_NT, 0, st>>>(d_codes, n, words, d, (unsigned long long *)d_keys,
+                                          (unsigned long long)cap, cnt);
+  }
+  EG_LAUNCH_CHECK();
+  EG_CUDA_TRY(cudaMemcpyAsync(h_count, cnt, 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
   return EG_OK;
 }
 

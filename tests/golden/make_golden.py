@@ -197,12 +197,50 @@ def gen_hamming_config(manifest, name, words, k, d):
     print(name, pairs.shape[0], f"{wall:.1f}s", flush=True)
 
 
+def gen_exact(manifest):
+    """The reference's exhaustive oracle (exact.py:57-121) on seeded inputs:
+    brute_force_cosine on a cfg1-shaped and a cfg3-shaped sample,
+    brute_force_hamming on a cfg2-shaped pool and a random 48-bit pool."""
+    out = {}
+    meta = {}
+    cases = {
+        "cos_cfg1": (workloads.cfg1_points(3_000, clusters=60), 0.1),
+        "cos_cfg3": (workloads.cfg3_points(6_000, planted_rows=600), 0.05),
+    }
+    for name, (x, eps) in cases.items():
+        e = ref.brute_force_cosine(x, eps)
+        out[f"{name}_pairs"] = e.pairs
+        out[f"{name}_dist"] = e.distances
+        meta[name] = {"n": int(x.shape[0]), "eps": eps, "edges": int(len(e.pairs)),
+                      "pairs_sha256": digest(e.pairs)}
+    words = workloads.cfg2_words(20_000, 1_000)
+    pool = ref.BitStringPool(words, 64)
+    p = ref.brute_force_hamming(pool, 2)
+    out["ham_cfg2_pairs"] = p.array
+    meta["ham_cfg2"] = {"n": int(words.shape[0]), "d": 2, "pairs": int(len(p.array)),
+                        "pairs_sha256": digest(p.array)}
+    rng = np.random.default_rng(21)
+    bits = (rng.random((4_000, 48)) < 0.5).astype(np.uint8)
+    bits[2_000:2_400] = bits[:400]
+    flip = rng.integers(0, 48, size=400)
+    bits[np.arange(2_000, 2_400), flip] ^= 1
+    pool = ref.BitStringPool.from_bits(bits)
+    out["ham_rand_words"] = pool.words
+    for d in (0, 1, 3, 6):
+        p = ref.brute_force_hamming(pool, d)
+        out[f"ham_rand_d{d}_pairs"] = p.array
+        meta[f"ham_rand_d{d}"] = {"pairs": int(len(p.array)), "pairs_sha256": digest(p.array)}
+    np.savez_compressed(os.path.join(HERE, "exact.npz"), **out)
+    manifest["exact"] = meta
+
+
 def main():
     manifest = {"numpy": np.__version__, "reference": ref.__version__}
     gen_fig2(manifest)
     gen_random_pools(manifest)
     gen_projection(manifest)
     gen_small_build(manifest)
+    gen_exact(manifest)
     # Config 1 at full size (SURVEY App. C: 809,648 edges).
     gen_config(manifest, "cfg1", workloads.cfg1_points(),
                {"epsilon": 0.1, "length": 32, "blocks": 8, "mismatch": 2,
@@ -229,4 +267,12 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "exact":   # only the exhaustive-oracle fixtures
+        path = os.path.join(HERE, "manifest.json")
+        with open(path) as f:
+            manifest = json.load(f)
+        gen_exact(manifest)
+        with open(path, "w") as f:
+            json.dump(manifest, f, indent=1, sort_keys=True)
+    else:
+        main()
