@@ -234,6 +234,11 @@ def run_reference(args, rank, world):
     }), flush=True)
 
 
+def _native_keys_to_pairs(keys):
+    from paper_0904_3151_b200 import engine
+    return engine.keys_to_pairs(keys.cpu().numpy())
+
+
 def config_block(args, cfg, n, world):
     return {"workload": f"{args.config}: n={n}, " + (
         f"D={384 if args.config == 'cfg3' else 'var'}, " if cfg.metric != "hamming" else "")
@@ -254,6 +259,8 @@ def main():
     ap.add_argument("--cpu-sample-rows", type=int, default=400_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-quality", action="store_true",
+                    help="skip the untimed recall check against the GPU brute force")
     ap.add_argument("--soak-s", type=float, default=2.0,
                     help="untimed warm steps (seconds) after --warmup, before timing")
     args = ap.parse_args()
@@ -306,8 +313,11 @@ def main():
         t = torch.tensor([n_soak], dtype=torch.int64, device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         n_soak = int(t.item())
+    last = None
     for _ in range(n_soak):
-        step()
+        # hold the previous result like the timed loop does, so the caching
+        # allocator already owns blocks for two live results
+        last = step()
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local, os.environ.get("EG_BENCH_CLOCKS", "between"))
@@ -319,13 +329,14 @@ def main():
         tdist.barrier()
     torch.cuda.synchronize()
     times, host_ms = [], []
-    last = None
     if os.environ.get("PYTHONGC") == "off":
         import gc
         gc.collect()
         gc.disable()
+    noflush = os.environ.get("EG_BENCH_NOFLUSH") == "1"    # diagnostics only
     for _ in range(args.steps):
-        flush.zero_()
+        if not noflush:
+            flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         t0 = time.perf_counter()
@@ -335,7 +346,10 @@ def main():
         e1.synchronize()
         host_ms.append((time.perf_counter() - t0) * 1e3)
         times.append(e0.elapsed_time(e1))
-        clocks.sample()
+        # NVML queries perturb the following step on some boxes: sample the
+        # clocks after every 4th step and after the last one
+        if len(times) % 4 == 1 or len(times) == args.steps:
+            clocks.sample()
     print("step_ms", [round(t, 2) for t in times], file=sys.stderr, flush=True)
     print("host_ms", [round(t, 2) for t in host_ms], file=sys.stderr, flush=True)
     torch.cuda.synchronize()
@@ -379,6 +393,25 @@ def main():
         e2e = {"value": n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}
     clk = clocks.stop()
+
+    # ------------------------------------------------------------- quality
+    # untimed: recall of the build against the GPU exhaustive oracle
+    # (exact.brute_force_cosine, the reference's exact.py:57 ground truth)
+    quality = None
+    if (rank == 0 and world == 1 and not hamming and not args.no_quality
+            and n <= 2_000_000 and last is not None and last.get("keys") is not None):
+        torch.cuda.synchronize()
+        tq = time.perf_counter()
+        eps_cos = cfg.epsilon if cfg.metric == "cosine" else cfg.epsilon ** 2 / 2.0
+        exact = eg.brute_force_cosine(x_dev, eps_cos, limit=None)
+        tq = time.perf_counter() - tq
+        built = _native_keys_to_pairs(last["keys"])
+        r = eg.measure_errors(built, exact)
+        quality = {"exact_edges": r.true_edge_count, "build_edges": int(built.shape[0]),
+                   "missing": r.missing_count, "false_edges": r.false_candidate_count,
+                   "recall": 1.0 - r.missing_ratio, "brute_force_s": round(tq, 3),
+                   "source": "GPU exhaustive oracle (brute_force_cosine, limit=None; "
+                             "tcgen05 fp16 screen + exact fp64 verify), untimed"}
 
     # ------------------------------------------------------------ roofline
     peak, peak_kind = peaks()
@@ -442,7 +475,7 @@ def main():
             "data": "synthetic (seeded generator, SURVEY.md App. C)",
             "config": config_block(args, cfg, n, world),
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
-            "cpu_baseline": cpu, "stage_ms": stage_ms,
+            "cpu_baseline": cpu, "stage_ms": stage_ms, "quality": quality,
             "counts": distributed.last_counts(last),
             "parity": parity_vs_reference(args.config, distributed.last_counts(last)),
         }

@@ -356,7 +356,20 @@ const char *eg_last_error(void) { return g_err; }
 
 long long eg_launch_count(void) { return g_launches.load(); }
 
-void eg_profile_enable(int on) { g_prof_on = on ? 1 : 0; }
+void eg_profile_enable(int on) {
+  if (on) {
+    // pre-create the event pool (and the record list) so that the first
+    // profiled builds do not pay for cudaEventCreate / vector growth
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    while (g_event_pool.size() < 8192) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) break;
+      g_event_pool.push_back(e);
+    }
+    g_prof_done.reserve(8192);
+  }
+  g_prof_on = on ? 1 : 0;
+}
 
 const char *eg_profile_class_name(int cls) {
   return (cls >= 0 && cls < PC_COUNT) ? g_prof_names[cls] : "";
