@@ -195,18 +195,236 @@ __global__ void __launch_bounds__(RS_NT) k_radix_downsweep(
   }
 }
 
+// ------------------------------------------------- onesweep radix sort
+// One kernel per 8-bit digit pass (after one histogram pass over all
+// digits): each CTA takes the next tile from an atomic ticket, ranks its
+// keys as k_radix_downsweep does, publishes its per-digit counts and finds
+// its global per-digit offsets by decoupled look-back over the tiles before
+// it, then scatters the tile-locally sorted run.  Status words are 64-bit:
+// flag (bits 62-63: 1 = tile aggregate, 2 = inclusive prefix) | count.
+constexpr int OS_MAXPASS = 8;
+#ifndef EG_OS_IPT
+#define EG_OS_IPT 16
+#endif
+// keys per thread of a onesweep tile (key-value sorts use RS_IPT: the value
+// stage must fit the 48 KB of static shared memory)
+constexpr int OS_IPT = EG_OS_IPT;
+constexpr unsigned long long OS_AGG = 1ull << 62, OS_INC = 2ull << 62,
+                             OS_VAL = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(RS_NT) k_radix_hist_all(const uint64_t *__restrict__ keys,
+                                                          int64_t m, const int *__restrict__ sh,
+                                                          int npass,
+                                                          unsigned long long *__restrict__ hist) {
+  __shared__ uint32_t h[OS_MAXPASS][256];
+  for (int i = threadIdx.x; i < OS_MAXPASS * 256; i += RS_NT) (&h[0][0])[i] = 0;
+  __syncthreads();
+  int shl[OS_MAXPASS];
+#pragma unroll
+  for (int p = 0; p < OS_MAXPASS; ++p) shl[p] = p < npass ? sh[p] : 0;
+  for (int64_t i = (int64_t)blockIdx.x * RS_NT + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * RS_NT) {
+    const uint64_t k = keys[i];
+#pragma unroll
+    for (int p = 0; p < OS_MAXPASS; ++p)
+      if (p < npass) atomicAdd(&h[p][(k >> shl[p]) & 0xff], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < npass * 256; i += RS_NT)
+    if ((&h[0][0])[i]) atomicAdd(&hist[i], (unsigned long long)(&h[0][0])[i]);
+}
+
+// hist[p][d] -> exclusive digit bases (in place), one CTA of 256 threads
+__global__ void __launch_bounds__(256) k_radix_digit_bases(unsigned long long *__restrict__ hist,
+                                                           int npass) {
+  __shared__ unsigned long long s[256];
+  for (int p = 0; p < npass; ++p) {
+    s[threadIdx.x] = hist[p * 256 + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long run = 0;
+      for (int d = 0; d < 256; ++d) {
+        const unsigned long long c = s[d];
+        s[d] = run;
+        run += c;
+      }
+    }
+    __syncthreads();
+    hist[p * 256 + threadIdx.x] = s[threadIdx.x];
+    __syncthreads();
+  }
+}
+
+template <bool VALS, int IPT>
+__global__ void __launch_bounds__(RS_NT) k_radix_onesweep(
+    const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+    uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t m, int shift,
+    const unsigned long long *__restrict__ digit_base, unsigned long long *status,
+    unsigned int *ticket) {
+  __shared__ uint64_t skeys[(RS_NT * IPT)];
+  __shared__ uint32_t svals[VALS ? (RS_NT * IPT) : 1];
+  __shared__ uint32_t wcnt[RS_WARPS][256];
+  __shared__ uint32_t tstart[256];
+  __shared__ unsigned long long gbase[256];
+  __shared__ uint32_t sw[RS_NT / 32];
+  __shared__ unsigned int stile;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) stile = atomicAdd(ticket, 1u);
+  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_NT) (&wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const int64_t tile = stile;
+  const int64_t base = tile * (RS_NT * IPT) + (int64_t)wid * 32 * IPT;
+  uint64_t k[IPT];
+  uint32_t v[IPT];
+  uint32_t rank[IPT];
+  const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {           // all loads in flight before ranking
+    const int64_t idx = base + i * 32 + lane;
+    k[i] = idx < m ? keys_in[idx] : 0;
+    if (VALS) v[i] = idx < m ? vals_in[idx] : 0;
+  }
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    const bool ok = idx < m;
+    const uint32_t dg = ok ? (uint32_t)((k[i] >> shift) & 0xff) : 0x100u;
+    const unsigned peers = __match_any_sync(0xffffffffu, dg);
+    uint32_t before = 0;
+    if (ok) before = wcnt[wid][dg];
+    rank[i] = before + __popc(peers & lt);
+    __syncwarp();
+    if (ok && (peers & lt) == 0) wcnt[wid][dg] = before + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    const int dgt = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < RS_WARPS; ++w) {
+      const uint32_t c = wcnt[w][dgt];
+      wcnt[w][dgt] = run;
+      run += c;
+    }
+    uint32_t tot;
+    tstart[dgt] = block_exclusive_scan<RS_NT>(run, tot, sw);
+    // publish this tile's count, then look back for the exclusive prefix
+    volatile unsigned long long *st = status;
+    if (tile == 0) {
+      st[dgt] = OS_INC | run;
+      gbase[dgt] = digit_base[dgt];
+    } else {
+      st[tile * 256 + dgt] = OS_AGG | run;
+      // look back in windows of 16 predecessors: the window's loads are
+      // independent (in flight together), then consumed newest first
+      unsigned long long pre = 0;
+      bool done = false;
+      for (int64_t t = tile - 1; t >= 0 && !done; t -= 16) {
+        unsigned long long w[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) w[q] = t - q >= 0 ? st[(t - q) * 256 + dgt] : 0ull;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          if (done || t - q < 0) continue;
+          unsigned long long x = w[q];
+          while ((x >> 62) == 0) x = st[(t - q) * 256 + dgt];
+          pre += x & OS_VAL;
+          if ((x >> 62) == 2) done = true;
+        }
+      }
+      __threadfence();
+      st[tile * 256 + dgt] = OS_INC | (pre + run);
+      gbase[dgt] = digit_base[dgt] + pre;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const int64_t idx = base + i * 32 + lane;
+    if (idx < m) {
+      const uint32_t dg = (uint32_t)((k[i] >> shift) & 0xff);
+      const uint32_t pos = tstart[dg] + wcnt[wid][dg] + rank[i];
+      skeys[pos] = k[i];
+      if (VALS) svals[pos] = v[i];
+    }
+  }
+  __syncthreads();
+  const int64_t tile0 = tile * (RS_NT * IPT);
+  const int valid = (int)min((int64_t)(RS_NT * IPT), m - tile0);
+  for (int j = threadIdx.x; j < valid; j += RS_NT) {
+    const uint64_t key = skeys[j];
+    const uint32_t dg = (uint32_t)((key >> shift) & 0xff);
+    const unsigned long long dst = gbase[dg] + (unsigned long long)(j - (int)tstart[dg]);
+    keys_out[dst] = key;
+    if (VALS) vals_out[dst] = svals[j];
+  }
+}
+
 __host__ inline size_t radix_workspace(int64_t m, bool vals) {
   int64_t ntiles = (m + RS_TILE - 1) / RS_TILE;
   size_t b = ws_bytes(m, 8) + (vals ? ws_bytes(m, 4) : 0);
   b += ws_bytes(ntiles * 256, 4);
   b += scan_workspace(ntiles * 256);
-  return b + 1024;
+  // onesweep: status words per (pass, tile, digit), tickets, histograms, shifts
+  b += ws_bytes((size_t)OS_MAXPASS * ntiles * 256, 8) + ws_bytes(OS_MAXPASS * 256 + 64, 8);
+  return b + 2048;
+}
+
+// Onesweep LSD sort (see above); same contract as radix_sort.
+__host__ inline int radix_sort_onesweep(uint64_t *keys, uint32_t *vals, int64_t m,
+                                        const int *shifts, int npass, Arena &ar,
+                                        cudaStream_t st) {
+  if (m <= 1 || npass == 0) return EG_OK;
+  if (npass > OS_MAXPASS || m >= (1ll << 32)) return EG_ERR_UNSUPPORTED;
+  const int64_t tilek = (int64_t)RS_NT * (vals ? RS_IPT : OS_IPT);
+  const int64_t ntiles = (m + tilek - 1) / tilek;
+  uint64_t *kalt = ar.take<uint64_t>(m);
+  uint32_t *valt = vals ? ar.take<uint32_t>(m) : nullptr;
+  unsigned long long *status = ar.take<unsigned long long>((size_t)npass * ntiles * 256);
+  // [hist npass*256][tickets 16 (u32 pairs)][shifts 8 (int)]
+  unsigned long long *meta = ar.take<unsigned long long>(OS_MAXPASS * 256 + 64);
+  if (!kalt || (vals && !valt) || !status || !meta) return EG_ERR_WORKSPACE;
+  unsigned long long *hist = meta;
+  unsigned int *tickets = reinterpret_cast<unsigned int *>(meta + OS_MAXPASS * 256);
+  int *dshift = reinterpret_cast<int *>(meta + OS_MAXPASS * 256 + 32);
+  EG_CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)npass * ntiles * 256 * 8, st));
+  EG_CUDA_TRY(cudaMemsetAsync(meta, 0, (OS_MAXPASS * 256 + 32) * 8, st));
+  EG_CUDA_TRY(cudaMemcpyAsync(dshift, shifts, npass * sizeof(int), cudaMemcpyHostToDevice, st));
+  {
+    EG_PROF(PC_SORT_UPSWEEP, st);
+    const unsigned g = (unsigned)std::min<int64_t>((m + RS_NT * 16 - 1) / (RS_NT * 16),
+                                                   (int64_t)1184);
+    k_radix_hist_all<<<g, RS_NT, 0, st>>>(keys, m, dshift, npass, hist);
+    k_radix_digit_bases<<<1, 256, 0, st>>>(hist, npass);
+  }
+  EG_LAUNCH_CHECK();
+  uint64_t *ksrc = keys, *kdst = kalt;
+  uint32_t *vsrc = vals, *vdst = valt;
+  for (int p = 0; p < npass; ++p) {
+    EG_PROF(PC_SORT_DOWNSWEEP, st);
+    unsigned long long *stp = status + (size_t)p * ntiles * 256;
+    if (vals)
+      k_radix_onesweep<true, RS_IPT><<<(unsigned)ntiles, RS_NT, 0, st>>>(
+          ksrc, vsrc, kdst, vdst, m, shifts[p], hist + p * 256, stp, tickets + p);
+    else
+      k_radix_onesweep<false, OS_IPT><<<(unsigned)ntiles, RS_NT, 0, st>>>(
+          ksrc, nullptr, kdst, nullptr, m, shifts[p], hist + p * 256, stp, tickets + p);
+    EG_LAUNCH_CHECK();
+    uint64_t *t = ksrc; ksrc = kdst; kdst = t;
+    uint32_t *tv = vsrc; vsrc = vdst; vdst = tv;
+  }
+  if (ksrc != keys) {
+    EG_CUDA_TRY(cudaMemcpyAsync(keys, ksrc, m * 8, cudaMemcpyDeviceToDevice, st));
+    if (vals) EG_CUDA_TRY(cudaMemcpyAsync(vals, vsrc, m * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return EG_OK;
 }
 
 // Sort keys (and vals) by the 8-bit digits at the given shifts, least
 // significant first.  Result ends in keys/vals.
-__host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const int *shifts,
-                               int npass, Arena &ar, cudaStream_t st) {
+__host__ inline int radix_sort_classic(uint64_t *keys, uint32_t *vals, int64_t m,
+                                       const int *shifts, int npass, Arena &ar, cudaStream_t st) {
   if (m <= 1 || npass == 0) return EG_OK;
   if (m >= (1ll << 32)) return EG_ERR_UNSUPPORTED;
   int64_t ntiles = (m + RS_TILE - 1) / RS_TILE;
@@ -242,6 +460,18 @@ __host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const 
     if (vals) EG_CUDA_TRY(cudaMemcpyAsync(vals, vsrc, m * 4, cudaMemcpyDeviceToDevice, st));
   }
   return EG_OK;
+}
+
+// Production sort: onesweep up to 32M keys (fewer launches: 0.47 -> 0.33 ms
+// for config 3's 2.5M candidate keys), the three-kernel upsweep / scan /
+// downsweep passes above that (higher occupancy, faster at 2e8-1.4e9 keys:
+// configs 4 and 5).  EG_SORT_CLASSIC=0/1 forces one of them (tests).
+__host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const int *shifts,
+                               int npass, Arena &ar, cudaStream_t st) {
+  const char *e = getenv("EG_SORT_CLASSIC");
+  const bool classic = (e && *e) ? *e == '1' : m > (32ll << 20);
+  if (classic || npass > OS_MAXPASS) return radix_sort_classic(keys, vals, m, shifts, npass, ar, st);
+  return radix_sort_onesweep(keys, vals, m, shifts, npass, ar, st);
 }
 
 // Digit shifts for pair keys (i << 32 | j) with i, j < n: only the low

@@ -571,3 +571,31 @@ def test_projection_extreme_magnitudes(eg, oracle, monkeypatch, tf32):
     for rep in (1, 2):
         got = eg.project(x, eg.ProjectionSpec(64, 3, rep)).words
         np.testing.assert_array_equal(got, oracle.project_words(x, 64, 3, rep))
+
+
+@pytest.mark.parametrize("classic", ["0", "1"])
+def test_radix_sort_kernels(eg, monkeypatch, classic):
+    """Onesweep (decoupled look-back) and classic LSD passes: pair-key sort
+    and key-value sort equal numpy's stable sort on ragged sizes, including
+    skewed digits (long look-back chains) and keys with equal halves."""
+    import torch
+    from paper_0904_3151_b200 import engine
+    monkeypatch.setenv("EG_SORT_CLASSIC", classic)
+    rng = np.random.default_rng(3)
+    dev = torch.device("cuda", 0)
+    for m in (1, 2, 2047, 2048, 2049, 100_003, 1_500_000):
+        n = 1 << 21
+        i = rng.integers(0, n, m)
+        j = rng.integers(0, n, m)
+        if m > 1000:
+            i[: m // 3] = 7                     # one digit value dominates
+        keys = (i.astype(np.int64) << 32) | j
+        t = torch.from_numpy(keys.copy()).to(dev)
+        engine.sort_pair_keys(t, n)
+        np.testing.assert_array_equal(t.cpu().numpy(), np.sort(keys))
+        vals = torch.arange(m, dtype=torch.int32, device=dev)
+        t = torch.from_numpy(keys.copy()).to(dev)
+        engine.sort_keys(t, 64, vals)
+        order = np.argsort(keys, kind="stable")
+        np.testing.assert_array_equal(t.cpu().numpy(), keys[order])
+        np.testing.assert_array_equal(vals.cpu().numpy(), order.astype(np.int32))
