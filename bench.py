@@ -443,7 +443,28 @@ def main():
                 "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                 "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg, blocks), "blocks": blocks,
                 "units_per_launch": units_per_launch, "avg_launch_ms": avg_ms}
+        # the same B_sort definition at the reference's own block count
+        # (independent of the kernel used; the planned count
+        # above is the conservative figure)
+        ref_units = cfg.replicates * math.comb(cfg.blocks, cfg.mismatch)
+        ref_units_mine = len(distributed.my_units(ref_units, world, rank))
+        ach_ref = sort_bytes_per_unit(n, cfg) * ref_units_mine / (avg_ms / 1e3) / 1e9
+        roof["ref_blocks"] = {"blocks": cfg.blocks, "units": ref_units_mine,
+                              "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg),
+                              "achieved": ach_ref, "frac": ach_ref / peak}
     stage_ms = {k: v["ms"] / args.steps for k, v in kprof.items()}
+    # other stages against their own bounds (SURVEY 8(d) byte definitions)
+    other = {}
+    if not hamming and "project" in kprof and kprof["project"]["count"]:
+        W = max(1, -(-cfg.length // 64))
+        pb = 4 * n * data.shape[1] + 8 * n + 8 * n * cfg.replicates * W
+        pms = kprof["project"]["ms"] / kprof["project"]["count"]
+        other["projection"] = {"kernel": "k_project_h16 (tcgen05 kind::f16, fused norms)",
+                               "bound": "hbm", "alg_bytes": pb, "avg_launch_ms": pms,
+                               "achieved": pb / (pms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                               "frac": pb / (pms / 1e3) / 1e9 / peak}
+    if roof is not None and other:
+        roof["other_stages"] = other
 
     # -------------------------------------------------------- cpu baseline
     cpu = None

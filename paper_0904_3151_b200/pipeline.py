@@ -123,6 +123,11 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
     if norms is None and codes is None:
         # one pass over the rows: norms + flags fused into the projection
         codes, norms, bad, fix = engine.project_rows(x, params.length, params.seed, reps)
+        # the flags travel to pinned host memory behind the projection and
+        # are checked after the next synchronising call (no extra bubble)
+        bad_host = torch.empty(bad.shape, dtype=bad.dtype, pin_memory=True)
+        bad_host.copy_(bad, non_blocking=True)
+        bad = bad_host
     else:
         if norms is None:
             norms, bad = engine.row_stats_async(x)     # checked once msm_pairs syncs
