@@ -175,6 +175,12 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
                    const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
                    int32_t replicates, uint8_t *d_keep, int64_t *h_new_counts,
                    void *stream);
+/* Same, without synchronising: the survivor counts go to device memory   */
+/* d_new_counts[replicates] (valid once the stream reaches this point).   */
+int eg_xrep_filter_async(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+                         const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
+                         int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,
+                         void *stream);
 
 /* --------------------------------------------------------------------- */
 /* Grouped sort of one mask.  Replaces grouped_radix_sort                 */

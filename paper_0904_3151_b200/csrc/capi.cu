@@ -148,6 +148,19 @@ static int env_int(const char *name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
+// Small pinned host staging area per device (results read after a sync the
+// call performs anyway, so the copy does not add a synchronisation).
+static unsigned long long *pinned_small() {
+  static unsigned long long *buf[64];
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (!buf[dev] && cudaHostAlloc(&buf[dev], 4096, cudaHostAllocPortable) != cudaSuccess)
+    buf[dev] = nullptr;
+  return buf[dev];
+}
+
 static int msm_buckets(int64_t n) {
   // mean bucket size: the tuned target, but never above EG_MSM_FILL (default
   // 80%) of the small tier's capacity.  Buckets are hash-balanced (Poisson,
@@ -1013,11 +1026,19 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   EG_CUDA_TRY(cudaMemsetAsync(a.ctr, 0, (3 + 2 * (size_t)replicates) * 8, st));
   EG_CUDA_TRY(cudaMemcpyAsync(b2b_d, b2b, EG_MAX_LENGTH, cudaMemcpyHostToDevice, st));
 
+  // balanced batches of <= lay.U units; at least two when there are a few
+  // units (a sharded rank's share), so the second batch's hist / scatter
+  // overlap the first batch's grouping on the side stream
   std::vector<UnitBatch> batches;
-  for (int64_t u0 = 0; u0 < n_units; u0 += lay.U) {
+  int64_t nbatch = (n_units + lay.U - 1) / lay.U;
+  if (lay.sets == 2 && n_units >= 4)
+    nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(env_int("EG_MSM_MINBATCHES", 2),
+                                                         n_units / 2));
+  const int64_t per_batch = nbatch > 0 ? (n_units + nbatch - 1) / nbatch : lay.U;
+  for (int64_t u0 = 0; u0 < n_units; u0 += per_batch) {
     UnitBatch ub;
     memset(&ub, 0, sizeof(ub));
-    ub.count = (int)std::min<int64_t>(lay.U, n_units - u0);
+    ub.count = (int)std::min<int64_t>(per_batch, n_units - u0);
     for (int j = 0; j < ub.count; ++j) {
       const int rep = h_unit_rep[u0 + j];
       const uint64_t mb = h_unit_mask[u0 + j];
@@ -1068,6 +1089,24 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   if (hc[0] > a.out_cap) {
     set_error("eg_msm_pairs: %llu pairs exceed capacity %llu", hc[0], a.out_cap);
     return EG_ERR_CAPACITY;
+  }
+  return EG_OK;
+}
+
+int eg_xrep_filter_async(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+                         const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
+                         int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,
+                         void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (replicates < 1 || replicates > 255 || W < 1 || W > 4 || m < 0)
+    return arg_error("eg_xrep_filter: bad arguments");
+  EG_CUDA_TRY(cudaMemsetAsync(d_new_counts, 0, 8 * (size_t)replicates, st));
+  if (m > 0) {
+    unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
+    EG_PROF(PC_MISC, st);
+    k_xrep_filter<<<grid, 256, 0, st>>>(d_keys, d_reps, m, d_codes, n, W, d, replicates, d_keep,
+                                        (unsigned long long *)d_new_counts);
+    EG_LAUNCH_CHECK();
   }
   return EG_OK;
 }
@@ -1257,11 +1296,18 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
                                              metric, eps, flags, dist, bad);
   }
   EG_LAUNCH_CHECK();
+  // the out-of-range flag rides on the compaction's synchronisation
+  unsigned long long *pin = pinned_small();
+  if (pin) EG_CUDA_TRY(cudaMemcpyAsync(pin, bad, 8, cudaMemcpyDeviceToHost, st));
   int rc = compact<double>(d_keys, dist, flags, m, d_out_keys, d_out_dist, h_count, ar, st);
   if (rc) return rc;
   unsigned long long hb = 0;
-  EG_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
-  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  if (pin) {
+    hb = pin[0];
+  } else {
+    EG_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+    EG_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   if (hb != ~0ull) {
     set_error("eg_verify: candidate %llu has an index out of range", hb);
     return EG_ERR_ARG;

@@ -237,20 +237,12 @@ __global__ void __launch_bounds__(RS_NT) k_radix_hist_all(const uint64_t *__rest
 // hist[p][d] -> exclusive digit bases (in place), one CTA of 256 threads
 __global__ void __launch_bounds__(256) k_radix_digit_bases(unsigned long long *__restrict__ hist,
                                                            int npass) {
-  __shared__ unsigned long long s[256];
+  __shared__ unsigned long long sw[8];
   for (int p = 0; p < npass; ++p) {
-    s[threadIdx.x] = hist[p * 256 + threadIdx.x];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long run = 0;
-      for (int d = 0; d < 256; ++d) {
-        const unsigned long long c = s[d];
-        s[d] = run;
-        run += c;
-      }
-    }
-    __syncthreads();
-    hist[p * 256 + threadIdx.x] = s[threadIdx.x];
+    const unsigned long long v = hist[p * 256 + threadIdx.x];
+    unsigned long long tot;
+    const unsigned long long ex = block_exclusive_scan64<256>(v, tot, sw);
+    hist[p * 256 + threadIdx.x] = ex;
     __syncthreads();
   }
 }

@@ -5,8 +5,9 @@ Sharding: every output pair has exactly one owning
 first-witness rule across replicates -- so units can be split across ranks
 with disjoint outputs and no cross-rank dedup.
 
-    1. rows are split into equal shards; each rank projects its shard
-       (eg_project) and computes its row norms (eg_row_stats);
+    1. rows are split into equal shards; each rank projects its shard and
+       computes its row norms and bad-row flags in the same pass
+       (eg_project_rows); the flags are MIN-reduced over the ranks;
     2. codes and norms are all-gathered over NVLink (NCCL all_gather);
     3. the block count is planned on the gathered codes (eg_msm_plan,
        deterministic, so every rank agrees without a collective), units are
@@ -51,6 +52,16 @@ class DeviceOps:
         codes, _ = engine.project_codes(x, norms, params.length, params.seed,
                                         list(range(1, params.replicates + 1)))
         return codes
+
+    def project_rows(self, x, params):
+        """Norms, bad-row flags and codes of a row shard in one pass over
+        the rows (eg_project_rows); no host sync."""
+        codes, norms, bad, _ = engine.project_rows(x, params.length, params.seed,
+                                                   list(range(1, params.replicates + 1)))
+        return codes, norms, bad
+
+    def raise_bad(self, bad):
+        engine.raise_bad_rows(bad)
 
     def plan(self, codes, params):
         """Block count of the units (deterministic in the codes, so every
@@ -98,14 +109,28 @@ def _all_gather_rows(t: torch.Tensor, per: int, world: int) -> torch.Tensor:
 
 
 def gather_codes(codes_shard, norms_shard, n, world, rank):
-    """(reps, n_r, W) shards -> (reps, n, W) full codes + full norms."""
+    """(reps, n_r, W) shards -> (reps, n, W) full codes + full norms, in ONE
+    all-gather: each rank packs its rows as [codes of every replicate |
+    norm bits] (int64), so the collective latency is paid once."""
     lo, hi, per = row_shard(n, world, rank)
-    reps = codes_shard.shape[0]
-    full = []
-    for h in range(reps):
-        full.append(_all_gather_rows(codes_shard[h], per, world)[:n])
-    norms = _all_gather_rows(norms_shard, per, world)[:n]
-    return torch.stack(full).contiguous(), norms.contiguous()
+    reps, nr, W = codes_shard.shape
+    packed = torch.cat([codes_shard.permute(1, 0, 2).reshape(nr, reps * W),
+                        norms_shard.contiguous().view(torch.int64).reshape(nr, 1)], dim=1)
+    full = _all_gather_rows(packed, per, world)[:n]
+    codes = full[:, :reps * W].reshape(n, reps, W).permute(1, 0, 2).contiguous()
+    norms = full[:, reps * W].contiguous().view(torch.float64)
+    return codes, norms
+
+
+def global_bad_rows(bad_local: torch.Tensor, row0: int) -> torch.Tensor:
+    """(first non-finite row, first zero-norm row) of the whole pool from
+    every rank's shard flags (-1 = none): MIN over ranks of the global row
+    indices, so all ranks see the reference's first offending row."""
+    big = torch.iinfo(torch.int64).max
+    g = torch.where(bad_local >= 0, bad_local + row0, torch.full_like(bad_local, big))
+    if tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1:
+        tdist.all_reduce(g, op=tdist.ReduceOp.MIN)
+    return torch.where(g == big, torch.full_like(g, -1), g)
 
 
 def gather_edges(keys, dists, world, rank, ops, n):
@@ -117,17 +142,16 @@ def gather_edges(keys, dists, world, rank, ops, n):
     mx = max(counts) if counts else 0
     if mx == 0:
         return keys[:0], dists[:0]
-    kp = torch.cat([keys, keys.new_zeros(mx - keys.numel())])
-    dp = torch.cat([dists, dists.new_zeros(mx - dists.numel())])
-    ka = kp.new_empty(mx * world)
-    da = dp.new_empty(mx * world)
+    # keys and distance bits travel together: one all-gather
+    kd = torch.stack([keys, dists.contiguous().view(torch.int64)], dim=1)
+    kp = torch.cat([kd, kd.new_zeros((mx - keys.numel(), 2))])
+    ka = kp.new_empty((mx * world, 2))
     tdist.all_gather_into_tensor(ka, kp)
-    tdist.all_gather_into_tensor(da, dp)
     if rank != 0:
         return None, None
-    ks = torch.cat([ka[r * mx:r * mx + counts[r]] for r in range(world)])
-    ds = torch.cat([da[r * mx:r * mx + counts[r]] for r in range(world)])
-    return ops.merge(ks, ds, n)
+    ks = torch.cat([ka[r * mx:r * mx + counts[r], 0] for r in range(world)])
+    ds = torch.cat([ka[r * mx:r * mx + counts[r], 1] for r in range(world)])
+    return ops.merge(ks.contiguous(), ds.contiguous().view(torch.float64), n)
 
 
 def build_step(x, params, metric: str, world: int, rank: int, ops=None,
@@ -145,9 +169,18 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
         return {"keys": out["keys"], "dist": out["dist"], "info": out["info"]}
     lo, hi, per = row_shard(n, world, rank)
     xs = x[lo:hi]
-    norms_s = ops.norms(xs)
-    codes_s = ops.project(xs, norms_s, params)
-    codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
+    if hasattr(ops, "project_rows"):
+        # one pass over the shard (norms + flags fused into the projection);
+        # the flags are agreed over the ranks so every rank raises the same
+        # error instead of one rank leaving the collectives
+        codes_s, norms_s, bad_s = ops.project_rows(xs, params)
+        bad = global_bad_rows(bad_s, lo)
+        codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
+        ops.raise_bad(bad)
+    else:
+        norms_s = ops.norms(xs)
+        codes_s = ops.project(xs, norms_s, params)
+        codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
     from math import comb
     blocks = ops.plan(codes, params)
     units = my_units(params.replicates * comb(blocks, params.mismatch), world, rank)

@@ -245,11 +245,15 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     keys = out[:total]
     if defer:
         keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
-        newc = (ctypes_i64 * reps)()
-        check(lib.eg_xrep_filter(_p(keys), _p(rtag), total, _p(codes), n, W, d, reps, _p(keep),
-                                 ctypes_addr(newc), _stream(dev)), "xrep_filter")
+        newc = torch.empty(reps, dtype=torch.int64, device=dev)
+        check(lib.eg_xrep_filter_async(_p(keys), _p(rtag), total, _p(codes), n, W, d, reps,
+                                       _p(keep), _p(newc), _stream(dev)), "xrep_filter")
+        # the counts reach pinned host memory behind the filter; the
+        # compaction's synchronisation makes them readable
+        newc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
+        newc_host.copy_(newc, non_blocking=True)
         keys = compact_keys(keys, keep[:total])
-        new = tuple(int(newc[h]) for h in range(reps))
+        new = tuple(int(v) for v in newc_host.tolist())
     else:
         new = tuple(int(counts[2 + reps + h]) for h in range(reps))
     info = {

@@ -44,6 +44,20 @@ class OracleOps:
                  for h in range(params.replicates)]
         return torch.from_numpy(np.stack(codes).view(np.int64))
 
+    def project_rows(self, xs, params):
+        """Fused stage of DeviceOps: codes, norms, (non-finite, zero) flags."""
+        v = xs.numpy().astype(np.float64)
+        ss = (v ** 2).sum(axis=1)
+        nonfin = np.flatnonzero(~np.isfinite(ss))
+        zero = np.flatnonzero(ss == 0.0)
+        bad = torch.tensor([int(nonfin[0]) if nonfin.size else -1,
+                            int(zero[0]) if zero.size else -1], dtype=torch.int64)
+        return self.project(xs, None, params), torch.from_numpy(np.sqrt(ss)), bad
+
+    def raise_bad(self, bad):
+        from paper_0904_3151_b200 import engine
+        engine.raise_bad_rows(bad)
+
     def plan(self, codes, params):
         # the block count is a cost knob: any k' > d gives the same pairs
         return self.blocks or params.blocks
@@ -123,6 +137,40 @@ def test_two_rank_build_equals_single_process(oracle, tmp_path, blocks):
                       (k & np.uint64(0xffffffff)).astype(np.int64)], axis=1)
     np.testing.assert_array_equal(pairs, ref.pairs)
     np.testing.assert_allclose(got["dist"], ref.distances, rtol=0, atol=1e-12)
+
+
+def _bad_worker(rank, world, port, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    import paper_0904_3151_b200 as eg
+    from paper_0904_3151_b200 import distributed, workloads
+    x = workloads.planted_clusters(400, 8, 8, 20, 0.03, 5)
+    x[301] = 0.0                       # in rank 1's shard
+    x[350] = 0.0
+    params = eg.MsmParams(epsilon=0.05, gamma=1e-3, length=24, mismatch=2, blocks=4,
+                          replicates=1, seed=7)
+    try:
+        distributed.build_step(torch.from_numpy(x), params, "cosine", world, rank,
+                               ops=OracleOps(orc, x))
+        msg = "no error"
+    except eg.DataError as e:
+        msg = str(e)
+    with open(f"{out_path}.{rank}", "w") as f:
+        f.write(msg)
+    tdist.destroy_process_group()
+
+
+def test_bad_rows_raise_on_every_rank(oracle, tmp_path):
+    """A zero row in one rank's shard: every rank raises the reference's
+    DataError for the first offending global row (no rank is left waiting
+    in a collective)."""
+    out = str(tmp_path / "msg")
+    mp.spawn(_bad_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        assert open(f"{out}.{r}").read() == "row 301 has zero norm and cannot be projected"
 
 
 def test_unit_and_row_sharding_cover_exactly_once():
