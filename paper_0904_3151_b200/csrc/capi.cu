@@ -1276,7 +1276,20 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   {
   EG_PROF(PC_VERIFY, st);
   const int vu = (!x_is_f64 && dim % 4 == 0 && dim <= 128 * VER_VU) ? (dim + 127) / 128 : 0;
-  if (x_is_f64)
+  const bool narrow = !x_is_f64 && dim % 4 == 0 && dim <= 128 && !env_int("EG_VERIFY_WIDE", 0);
+  if (narrow) {
+    // eight lanes per pair, four pairs per warp step (measured: 4 lanes per
+    // pair is slower on configs 4 and 5)
+    const int lp = 8;
+    const unsigned g8 = (unsigned)std::min<int64_t>((m * lp + 255) / 256, (int64_t)num_sms() * 64);
+    const int v8 = (dim / 4 + lp - 1) / lp;
+#define EG_V8(LP, V)                                                                           \
+  k_verify8<LP, V><<<g8, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, m, metric, \
+                                       eps, flags, dist, bad)
+    if (v8 <= 1) EG_V8(8, 1); else if (v8 == 2) EG_V8(8, 2); else if (v8 == 3) EG_V8(8, 3);
+    else EG_V8(8, 4);
+#undef EG_V8
+  } else if (x_is_f64)
     k_verify<double, 0><<<grid, 256, 0, st>>>((const double *)d_x, n, dim, d_norms, d_keys, m,
                                               metric, eps, flags, dist, bad);
   else if (vu == 1)

@@ -151,4 +151,85 @@ __global__ void __launch_bounds__(256) k_verify(const TX *__restrict__ x, int64_
   }
 }
 
+// Narrow rows (fp32, dim % 4 == 0, dim <= 128): LP lanes per pair, 32 / LP
+// pairs per warp step.  Each LP-lane group walks its own contiguous run of
+// the (i, j)-sorted candidates, keeps x_i in registers across a run of equal
+// i, adds lane-local products in ascending slice order and reduces over the
+// group with a fixed butterfly (xor LP/2, ..., 1) -- one summation order for
+// every pair of a given shape, so distances stay per-pair deterministic.
+template <int LP, int VU8>
+__global__ void __launch_bounds__(256) k_verify8(const float *__restrict__ x, int64_t n, int dim,
+                                                 const double *__restrict__ norms,
+                                                 const uint64_t *__restrict__ keys, int64_t m,
+                                                 int metric, double eps,
+                                                 uint8_t *__restrict__ flags,
+                                                 double *__restrict__ dist,
+                                                 unsigned long long *__restrict__ bad) {
+  const int lane = threadIdx.x & 31, gl = lane & (LP - 1);
+  const int64_t groups = (int64_t)gridDim.x * (256 / LP);
+  const int64_t gid = ((int64_t)blockIdx.x * 256 + threadIdx.x) / LP;
+  const int d4 = dim / 4;
+  const int64_t per = (m + groups - 1) / groups;
+  const int64_t p0 = gid * per, p1 = min(m, p0 + per);
+  const int64_t steps = per;                 // uniform trip count across the warp
+  int64_t cur = -1;
+  float4 a[VU8];
+  for (int64_t t = 0; t < steps; ++t) {
+    const int64_t p = p0 + t;
+    const bool live = p < p1;
+    const uint64_t key = live ? keys[p] : 0ull;
+    const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+    const bool ok = live && i < n && j < n;
+    if (live && !ok && gl == 0) { atomicMin(bad, (unsigned long long)p); flags[p] = 0; dist[p] = 0.0; }
+    float4 b[VU8];
+    const float4 *xj = reinterpret_cast<const float4 *>(x + (ok ? j : 0) * dim);
+#pragma unroll
+    for (int u = 0; u < VU8; ++u) {
+      const int q = gl + LP * u;
+      b[u] = (ok && q < d4) ? __ldg(xj + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (ok && i != cur) {
+      const float4 *xi = reinterpret_cast<const float4 *>(x + i * dim);
+#pragma unroll
+      for (int u = 0; u < VU8; ++u) {
+        const int q = gl + LP * u;
+        a[u] = q < d4 ? __ldg(xi + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      cur = i;
+    }
+    double acc = 0.0;
+    if (ok) {
+#pragma unroll
+      for (int u = 0; u < VU8; ++u) {
+        if (gl + LP * u >= d4) break;
+        if (metric == EG_METRIC_COSINE) {
+          acc = fma((double)a[u].x, (double)b[u].x, acc);
+          acc = fma((double)a[u].y, (double)b[u].y, acc);
+          acc = fma((double)a[u].z, (double)b[u].z, acc);
+          acc = fma((double)a[u].w, (double)b[u].w, acc);
+        } else {
+          double tt;
+          tt = (double)a[u].x - (double)b[u].x; acc = fma(tt, tt, acc);
+          tt = (double)a[u].y - (double)b[u].y; acc = fma(tt, tt, acc);
+          tt = (double)a[u].z - (double)b[u].z; acc = fma(tt, tt, acc);
+          tt = (double)a[u].w - (double)b[u].w; acc = fma(tt, tt, acc);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = LP / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (ok && gl == 0) {
+      double dd;
+      if (metric == EG_METRIC_COSINE) {
+        dd = 1.0 - acc / (norms[i] * norms[j]);
+        dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
+      } else {
+        dd = sqrt(acc);
+      }
+      dist[p] = dd;
+      flags[p] = dd <= eps;
+    }
+  }
+}
+
 }  // namespace eg

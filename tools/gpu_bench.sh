@@ -1,4 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-for w in 1 8; do timeout 600 python tools/rank_sim.py --world $w --ranks 2 2>&1 | grep world=; done
-timeout 900 python bench.py --no-cpu-baseline --no-quality --e2e-steps 0 --steps 12 2> gpurun_out/b.err > gpurun_out/b.json; grep step_ms gpurun_out/b.err; python -c "
-import json; d=json.load(open('gpurun_out/b.json')); print(d['ms_per_step'], d['parity']['match'])"
+for lp in 8 4; do for c in cfg4 cfg5; do EG_VERIFY_LP=$lp timeout 900 python bench.py --config $c --no-cpu-baseline --no-quality --e2e-steps 0 --steps 3 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('lp=$lp $c', round(d['ms_per_step'],2), round(d['stage_ms'].get('verify',0),2), d['counts']['edges'])"; done; done
+EG_VERIFY_LP=4 timeout 900 python -m pytest tests -m gpu -x -q -k "cfg or exact or small" 2>&1 | tail -2
