@@ -78,12 +78,32 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
   return z;
 }
 
+// Hash of a masked key: per word half of murmur3's fmix64 (xor-shift,
+// one multiply, xor-shift): the pre-shift folds the high bits down, the
+// multiply carries every bit upward into the top bits (the MSD bucket
+// digit), the post-shift folds them into the low 32 bits (the in-bucket
+// group key h2).  Equal keys give equal hashes and h2 collisions between
+// distinct keys are removed by the exact compare, so only speed depends on
+// the mixing.  EG_HASH_FMIX=1 restores the full finaliser.
+#ifndef EG_HASH_FMIX
+#define EG_HASH_FMIX 0
+#endif
 template <int W>
 __device__ __forceinline__ uint64_t hash_key(const uint64_t (&c)[W], const uint64_t *kept,
                                              uint64_t salt) {
   uint64_t h = salt;
+#if EG_HASH_FMIX
 #pragma unroll
   for (int w = 0; w < W; ++w) h = fmix64(h ^ (c[w] & kept[w]) ^ (0x9e3779b97f4a7c15ULL * (w + 1)));
+#else
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    h ^= (c[w] & kept[w]) ^ (0x9e3779b97f4a7c15ULL * (w + 1));
+    h ^= h >> 33;
+    h *= 0xff51afd7ed558ccdULL;
+    h ^= h >> 33;
+  }
+#endif
   return h;
 }
 
