@@ -265,6 +265,21 @@ int eg_bf_hamming(const uint64_t *d_codes, int64_t n, int32_t words, int32_t d,
                   uint64_t *d_keys, int64_t cap, int64_t *h_count, void *d_workspace,
                   size_t workspace_bytes, void *stream);
 
+/* --------------------------------------------------------------------- */
+/* Edge-list text.  Replaces the formatting loop of */
+/* io.write_edges (io.py:145-158): for m <= EG_FORMAT_MAX_EDGES edges      */
+/* (keys (i << 32) | j, fp64 distances) writes "i j d.ddddddddd\n" lines   */
+/* (%.9f, round-half-even on the exact binary value, as Python's float     */
+/* formatting) back to back into d_out; *h_bytes = total bytes.  Returns   */
+/* EG_ERR_CAPACITY (with *h_bytes set, nothing written) if out_cap is too  */
+/* small, EG_ERR_UNSUPPORTED if |dist| * 1e9 >= 2^63.  Synchronises.       */
+/* --------------------------------------------------------------------- */
+#define EG_FORMAT_MAX_EDGES (1ll << 26)
+size_t eg_format_edges_workspace(int64_t m);
+int eg_format_edges(const uint64_t *d_keys, const double *d_dist, int64_t m, char *d_out,
+                    int64_t out_cap, int64_t *h_bytes, void *d_workspace,
+                    size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

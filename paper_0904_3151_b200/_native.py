@@ -86,6 +86,8 @@ def _declare(lib):
         "eg_bf_cosine_candidates": ([P, I, i64, i32, P, dbl, P, i64, P, P, sz, P], I),
         "eg_bf_hamming_workspace": ([], sz),
         "eg_bf_hamming": ([P, i64, i32, i32, P, i64, P, P, sz, P], I),
+        "eg_format_edges_workspace": ([i64], sz),
+        "eg_format_edges": ([P, P, i64, P, i64, P, P, sz, P], I),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

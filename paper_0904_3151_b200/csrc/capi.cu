@@ -16,6 +16,7 @@
 #include "plan.cuh"
 #include "project_h16.cuh"
 #include "exact.cuh"
+#include "format.cuh"
 #include "project.cuh"
 #include "project_tc.cuh"
 #include <cudaTypedefs.h>
@@ -1451,6 +1452,61 @@ int eg_bf_hamming(const uint64_t *d_codes, int64_t n, int32_t words, int32_t d, 
   EG_LAUNCH_CHECK();
   EG_CUDA_TRY(cudaMemcpyAsync(h_count, cnt, 8, cudaMemcpyDeviceToHost, st));
   EG_CUDA_TRY(cudaStreamSynchronize(st));
+  return EG_OK;
+}
+
+
+// --------------------------------------------------------- edge text
+size_t eg_format_edges_workspace(int64_t m) {
+  return ws_bytes(m + 1, 4) + scan_workspace(m + 1) + ws_bytes(1, 8) + 1024;
+}
+
+int eg_format_edges(const uint64_t *d_keys, const double *d_dist, int64_t m, char *d_out,
+                    int64_t out_cap, int64_t *h_bytes, void *d_workspace,
+                    size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  *h_bytes = 0;
+  if (m < 0 || m > EG_FORMAT_MAX_EDGES) return arg_error("eg_format_edges: 0 <= m <= 2^26");
+  if (m == 0) return EG_OK;
+  Arena ar(d_workspace, workspace_bytes);
+  uint32_t *len = ar.take<uint32_t>(m + 1);
+  unsigned long long *bad = ar.take<unsigned long long>(1);
+  if (!len || !bad) {
+    set_error("eg_format_edges: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
+  EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 8, st));
+  EG_CUDA_TRY(cudaMemsetAsync(len + m, 0, 4, st));
+  const unsigned g = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
+  k_edge_len<<<g, 256, 0, st>>>(d_keys, d_dist, m, len, bad);
+  EG_LAUNCH_CHECK();
+  int rc = scan_exclusive_u32(len, len, m + 1, ar, st);
+  if (rc) return rc;
+  unsigned long long *pin = pinned_small();
+  uint32_t total = 0;
+  unsigned long long hb = 0;
+  if (pin) {
+    EG_CUDA_TRY(cudaMemcpyAsync(pin, len + m, 4, cudaMemcpyDeviceToHost, st));
+    EG_CUDA_TRY(cudaMemcpyAsync(pin + 1, bad, 8, cudaMemcpyDeviceToHost, st));
+    EG_CUDA_TRY(cudaStreamSynchronize(st));
+    total = (uint32_t)(pin[0] & 0xffffffffull);
+    hb = pin[1];
+  } else {
+    EG_CUDA_TRY(cudaMemcpyAsync(&total, len + m, 4, cudaMemcpyDeviceToHost, st));
+    EG_CUDA_TRY(cudaMemcpyAsync(&hb, bad, 8, cudaMemcpyDeviceToHost, st));
+    EG_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  if (hb != ~0ull) {
+    set_error("eg_format_edges: distance of edge %llu is outside the %%.9f range", hb);
+    return EG_ERR_UNSUPPORTED;
+  }
+  *h_bytes = (int64_t)total;
+  if ((int64_t)total > out_cap) {
+    set_error("eg_format_edges: %u bytes exceed capacity %lld", total, (long long)out_cap);
+    return EG_ERR_CAPACITY;
+  }
+  k_edge_write<<<g, 256, 0, st>>>(d_keys, d_dist, m, len, d_out);
+  EG_LAUNCH_CHECK();
   return EG_OK;
 }
 

@@ -234,6 +234,39 @@ def gen_exact(manifest):
     manifest["exact"] = meta
 
 
+def gen_io(manifest):
+    """Edge files written by the reference's io.write_edges (io.py:145-158):
+    special distances, values at %.9f rounding boundaries, random ones,
+    large indices and Euclidean-scale distances; the bytes are the fixture."""
+    import tempfile
+    rng = np.random.default_rng(31)
+    special = [0.0, 2.0, 1.0, 0.123456789123, 5e-10, 1.5e-9, 2.5e-9, 0.0000000015,
+               0.9999999995, 1.9999999995, 0.1234567885, 0.1234567895, 1e-300, 5e-324,
+               12345.678901234, 1e9, 3.0000000005, 7.25, 0.5, 0.05]
+    m = 4000
+    d = np.concatenate([np.array(special), rng.random(m) * 2.0,
+                        rng.random(200) * 1e4, np.round(rng.random(200) * 2, 9),
+                        np.round(rng.random(200) * 2, 10) + 5e-10])
+    i = np.sort(rng.integers(0, 4_000_000_000, d.size))
+    j = i + rng.integers(1, 1000, d.size)
+    pairs = np.stack([i, j], axis=1).astype(np.int64)
+    order = np.lexsort((pairs[:, 1], pairs[:, 0]))
+    pairs, d = pairs[order], d[order]
+    keep = np.ones(len(pairs), dtype=bool)
+    keep[1:] = np.any(pairs[1:] != pairs[:-1], axis=1)
+    pairs, d = pairs[keep], d[keep]
+    edges = ref.EdgeList(pairs, d)
+    meta = {"epsilon": 0.05, "nodes": 1600000, "normalize": False, "tag": "golden"}
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "e.txt")
+        ref.write_edges(path, edges, meta)
+        blob = open(path, "rb").read()
+    np.savez_compressed(os.path.join(HERE, "io_edges.npz"), pairs=pairs, dist=d,
+                        text=np.frombuffer(blob, dtype=np.uint8))
+    manifest["io_edges"] = {"edges": int(len(pairs)), "bytes": len(blob),
+                            "sha256": hashlib.sha256(blob).hexdigest(), "meta": meta}
+
+
 def main():
     manifest = {"numpy": np.__version__, "reference": ref.__version__}
     gen_fig2(manifest)
@@ -241,6 +274,7 @@ def main():
     gen_projection(manifest)
     gen_small_build(manifest)
     gen_exact(manifest)
+    gen_io(manifest)
     # Config 1 at full size (809,648 edges).
     gen_config(manifest, "cfg1", workloads.cfg1_points(),
                {"epsilon": 0.1, "length": 32, "blocks": 8, "mismatch": 2,
@@ -267,11 +301,11 @@ def main():
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "exact":   # only the exhaustive-oracle fixtures
+    if len(sys.argv) > 1 and sys.argv[1] in ("exact", "io"):   # one fixture family only
         path = os.path.join(HERE, "manifest.json")
         with open(path) as f:
             manifest = json.load(f)
-        gen_exact(manifest)
+        {"exact": gen_exact, "io": gen_io}[sys.argv[1]](manifest)
         with open(path, "w") as f:
             json.dump(manifest, f, indent=1, sort_keys=True)
     else:

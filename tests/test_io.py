@@ -1,0 +1,106 @@
+"""Edge-list files (reference io.py:122-195): GPU formatting of write_edges
+against bytes written by the reference itself (tests/golden/io_edges.npz,
+made by make_golden.py), the host parser, and the reference's own cases
+(tests/test_io.py of the reference, restated)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+
+# ----------------------------------------------------------- host (no GPU)
+def test_read_edges_parses_reference_bytes(tmp_path, manifest):
+    from paper_0904_3151_b200 import read_edges
+    g = golden("io_edges")
+    path = tmp_path / "e.txt"
+    path.write_bytes(g["text"].tobytes())
+    edges, meta = read_edges(path)
+    np.testing.assert_array_equal(edges.pairs, g["pairs"])
+    # %.9f text: the parsed distance is within half a unit of the 9th digit
+    assert np.all(np.abs(edges.distances - g["dist"]) <= 5e-10 * (1 + 1e-9) + 1e-15 * g["dist"])
+    assert meta == manifest["io_edges"]["meta"]
+
+
+@pytest.mark.parametrize("body", [
+    "1 0 0.5\n",                  # i >= j
+    "0 1 0.5\n0 1 0.5\n",         # duplicate
+    "1 2 0.5\n0 1 0.5\n",         # out of order
+    "0 1\n",                      # missing column
+    "0 x 0.5\n",                  # not an integer
+])
+def test_read_edges_rejects_malformed(tmp_path, body):
+    from paper_0904_3151_b200 import DataError, read_edges
+    path = tmp_path / "e.txt"
+    path.write_text("# nodes=3\n" + body)
+    with pytest.raises(DataError):
+        read_edges(path)
+
+
+def test_read_edges_error_lines(tmp_path):
+    from paper_0904_3151_b200 import DataError, read_edges
+    path = tmp_path / "e.txt"
+    path.write_text("# nodes=9\n0 1 0.5\n\n2 3 0.1\n3 3 0.2\n")
+    with pytest.raises(DataError, match=r":5: need 0 <= i < j"):
+        read_edges(path)
+    path.write_text("0 1 0.5\n2 3 0.1\n2 3 0.2\n")
+    with pytest.raises(DataError, match=r":3: pairs must be sorted and unique"):
+        read_edges(path)
+
+
+# ------------------------------------------------------------------- GPU
+@pytest.fixture(scope="module")
+def eg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_0904_3151_b200 as eg
+    return eg
+
+
+@pytest.mark.gpu
+def test_write_edges_bytes_equal_reference(eg, tmp_path, manifest):
+    g = golden("io_edges")
+    path = tmp_path / "e.txt"
+    eg.write_edges(path, eg.EdgeList(g["pairs"], g["dist"]), manifest["io_edges"]["meta"])
+    assert path.read_bytes() == g["text"].tobytes()
+
+
+@pytest.mark.gpu
+def test_write_edges_from_device_and_round_trip(eg, tmp_path):
+    import torch
+    from paper_0904_3151_b200 import workloads
+    x = workloads.cfg1_points(3_000, clusters=60)
+    params = eg.MsmParams(epsilon=0.1, gamma=1e-6, length=32, mismatch=2, blocks=8,
+                          replicates=1, seed=0)
+    out = eg.build_graph_device(torch.from_numpy(x).cuda(), params)
+    p1, p2 = tmp_path / "a.txt", tmp_path / "b.txt"
+    eg.write_edges(p1, (out["keys"], out["dist"]), {"nodes": 3000})
+    g = eg.build_graph(x, params)
+    eg.write_edges(p2, g.edge_list, {"nodes": 3000})
+    assert p1.read_bytes() == p2.read_bytes()
+    back, meta = eg.read_edges(p1)
+    np.testing.assert_array_equal(back.pairs, g.edge_list.pairs)
+    assert meta == {"nodes": 3000}
+    # the stable-format case of the reference's tests
+    p3 = tmp_path / "c.txt"
+    eg.write_edges(p3, eg.EdgeList.from_rows([(0, 1, 0.123456789123)]), {"nodes": 2})
+    assert p3.read_text() == "# nodes=2\n0 1 0.123456789\n"
+    eg.write_edges(p3, eg.EdgeList(), {"nodes": 0})
+    back, meta = eg.read_edges(p3)
+    assert len(back) == 0 and meta["nodes"] == 0
+
+
+@pytest.mark.gpu
+def test_write_edges_random_doubles_match_python_format(eg, tmp_path):
+    """%.9f of arbitrary doubles (all exponents that fit, ties at the 9th
+    digit) equals Python's correctly rounded formatting."""
+    rng = np.random.default_rng(8)
+    d = np.concatenate([rng.random(3000) * 2, 10.0 ** rng.uniform(-12, 9, 3000),
+                        (rng.integers(0, 2 ** 20, 2000) + 0.5) / 1e9,      # exact-ish ties
+                        np.ldexp(rng.integers(1, 2 ** 30, 2000).astype(np.float64), -31)])
+    pairs = np.stack([np.arange(d.size), np.arange(d.size) + 1], axis=1)
+    path = tmp_path / "r.txt"
+    eg.write_edges(path, eg.EdgeList(pairs, d))
+    want = "".join(f"{i} {j} {v:.9f}\n" for (i, j), v in zip(pairs.tolist(), d.tolist()))
+    assert path.read_text() == want
