@@ -104,3 +104,57 @@ def test_write_edges_random_doubles_match_python_format(eg, tmp_path):
     eg.write_edges(path, eg.EdgeList(pairs, d))
     want = "".join(f"{i} {j} {v:.9f}\n" for (i, j), v in zip(pairs.tolist(), d.tolist()))
     assert path.read_text() == want
+
+
+# --------------------------------------------------------------- datasets
+def test_dataset_round_trip_and_reference_bytes(tmp_path):
+    """write_dataset bytes = the reference's header + float32 payload;
+    read_dataset returns the rows (reference tests/test_io.py cases)."""
+    import struct
+    from paper_0904_3151_b200 import read_dataset, write_dataset
+    rng = np.random.default_rng(1)
+    data = rng.standard_normal((37, 5)).astype(np.float32)
+    path = tmp_path / "d.bin"
+    write_dataset(path, data)
+    raw = path.read_bytes()
+    assert raw[:28] == struct.pack("<4sIQQI", b"EPGD", 1, 37, 5, 4)
+    assert raw[28:] == data.astype("<f4").tobytes()
+    np.testing.assert_array_equal(read_dataset(path).vectors, data)
+
+
+def test_dataset_csv_fallback_and_errors(tmp_path):
+    from paper_0904_3151_b200 import DataError, read_dataset, write_dataset
+    path = tmp_path / "d.csv"
+    path.write_text("1.5,2.0\n-0.25,3.0\n0.125,7.0\n")
+    back = read_dataset(path)
+    assert back.vectors.dtype == np.float32
+    np.testing.assert_array_equal(back.vectors, np.array([[1.5, 2.0], [-0.25, 3.0],
+                                                          [0.125, 7.0]], dtype=np.float32))
+    bad = tmp_path / "bad.bin"
+    bad.write_bytes(b"not a dataset at all")
+    with pytest.raises(DataError):
+        read_dataset(bad)
+    d = tmp_path / "t.bin"
+    write_dataset(d, np.ones((20, 4), np.float32))
+    d.write_bytes(d.read_bytes()[:-8])
+    with pytest.raises(DataError, match="payload"):
+        read_dataset(d)
+    with pytest.raises(DataError):
+        write_dataset(tmp_path / "n.bin", np.array([[1.0, np.nan]], dtype=np.float32))
+
+
+@pytest.mark.gpu
+def test_read_dataset_device(eg, tmp_path):
+    rng = np.random.default_rng(4)
+    data = rng.standard_normal((1000, 48)).astype(np.float32)
+    path = tmp_path / "d.bin"
+    eg.write_dataset(path, data)
+    x = eg.read_dataset_device(path)
+    assert x.is_cuda and x.dtype.is_floating_point
+    np.testing.assert_array_equal(x.cpu().numpy(), data)
+    # a corrupted payload value is caught on the device
+    raw = bytearray(path.read_bytes())
+    raw[28 + 4 * 777:28 + 4 * 778] = np.array([np.inf], dtype="<f4").tobytes()
+    path.write_bytes(bytes(raw))
+    with pytest.raises(eg.DataError, match="non-finite"):
+        eg.read_dataset_device(path)

@@ -1,2 +1,1 @@
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-timeout 600 python tools/io_bench.py 2>&1 | tail -2
