@@ -267,6 +267,21 @@ def gen_io(manifest):
                             "sha256": hashlib.sha256(blob).hexdigest(), "meta": meta}
 
 
+def gen_estimate(manifest):
+    """The reference's estimate_output_size (tuning.py:190-229) on seeded
+    cfg1- and cfg3-shaped samples."""
+    out = {}
+    for name, x, eps, pairs, seed in [
+            ("cfg1", workloads.cfg1_points(5_000, clusters=50), 0.1, 20_000, 0),
+            ("cfg3", workloads.cfg3_points(20_000, planted_rows=4_000), 0.05, 50_000, 3),
+            ("tiny", workloads.cfg1_points(40, clusters=2), 0.3, 7, 1)]:
+        e = ref.estimate_output_size(x, eps, sample_pairs=pairs, seed=seed)
+        out[name] = {"eps": eps, "sample_pairs": pairs, "seed": seed, "hits": e.hits,
+                     "total_pairs": e.total_pairs, "estimate_s": e.estimate_s,
+                     "ci": [e.ci_low, e.ci_high]}
+    manifest["estimate"] = out
+
+
 def main():
     manifest = {"numpy": np.__version__, "reference": ref.__version__}
     gen_fig2(manifest)
@@ -275,6 +290,7 @@ def main():
     gen_small_build(manifest)
     gen_exact(manifest)
     gen_io(manifest)
+    gen_estimate(manifest)
     # Config 1 at full size (809,648 edges).
     gen_config(manifest, "cfg1", workloads.cfg1_points(),
                {"epsilon": 0.1, "length": 32, "blocks": 8, "mismatch": 2,
@@ -301,11 +317,11 @@ def main():
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] in ("exact", "io"):   # one fixture family only
+    if len(sys.argv) > 1 and sys.argv[1] in ("exact", "io", "estimate"):   # one family only
         path = os.path.join(HERE, "manifest.json")
         with open(path) as f:
             manifest = json.load(f)
-        {"exact": gen_exact, "io": gen_io}[sys.argv[1]](manifest)
+        {"exact": gen_exact, "io": gen_io, "estimate": gen_estimate}[sys.argv[1]](manifest)
         with open(path, "w") as f:
             json.dump(manifest, f, indent=1, sort_keys=True)
     else:
