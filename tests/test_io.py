@@ -158,3 +158,16 @@ def test_read_dataset_device(eg, tmp_path):
     path.write_bytes(bytes(raw))
     with pytest.raises(eg.DataError, match="non-finite"):
         eg.read_dataset_device(path)
+
+
+@pytest.mark.gpu
+def test_write_edges_chunked_equals_single_call(eg, tmp_path, monkeypatch):
+    """Edge lists longer than one eg_format_edges call are written in chunks
+    with identical bytes (chunk size forced small)."""
+    g = golden("io_edges")
+    edges = eg.EdgeList(g["pairs"], g["dist"])
+    a, b = tmp_path / "a.txt", tmp_path / "b.txt"
+    eg.write_edges(a, edges, {"nodes": 7})
+    monkeypatch.setenv("EG_FORMAT_CHUNK", "997")
+    eg.write_edges(b, edges, {"nodes": 7})
+    assert a.read_bytes() == b.read_bytes()
