@@ -124,29 +124,29 @@ __global__ void __launch_bounds__(256) k_verify(const TX *__restrict__ x, int64_
         flags[p] = dd <= eps;
       }
     }
-    return;
-  }
-  for (int64_t p = wid; p < m; p += warps) {
-    const uint64_t key = keys[p];
-    const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
-    if (!(i < n && j < n)) {
-      if (lane == 0) { atomicMin(bad, (unsigned long long)p); flags[p] = 0; dist[p] = 0.0; }
-      continue;
-    }
-    double acc = 0.0;
-    accum_pair<TX>(x + i * dim, x + j * dim, dim, lane, metric, acc);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) {
-      double dd;
-      if (metric == EG_METRIC_COSINE) {
-        dd = 1.0 - acc / (norms[i] * norms[j]);
-        dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
-      } else {
-        dd = sqrt(acc);
+  } else {
+    for (int64_t p = wid; p < m; p += warps) {
+      const uint64_t key = keys[p];
+      const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+      if (!(i < n && j < n)) {
+        if (lane == 0) { atomicMin(bad, (unsigned long long)p); flags[p] = 0; dist[p] = 0.0; }
+        continue;
       }
-      dist[p] = dd;
-      flags[p] = dd <= eps;
+      double acc = 0.0;
+      accum_pair<TX>(x + i * dim, x + j * dim, dim, lane, metric, acc);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) {
+        double dd;
+        if (metric == EG_METRIC_COSINE) {
+          dd = 1.0 - acc / (norms[i] * norms[j]);
+          dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
+        } else {
+          dd = sqrt(acc);
+        }
+        dist[p] = dd;
+        flags[p] = dd <= eps;
+      }
     }
   }
 }
