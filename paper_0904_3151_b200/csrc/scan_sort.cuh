@@ -497,6 +497,11 @@ __global__ void __launch_bounds__(CP_NT) k_flag_count(const uint8_t *__restrict_
 }
 
 // Stable scatter: blocked arrangement inside each tile keeps input order.
+// Stable scatter of the flagged elements, coalesced: iteration i of a tile
+// covers elements [i * CP_NT, (i + 1) * CP_NT), a block scan per iteration
+// places them in ascending index order; fully kept tiles (the common case
+// of a verify that keeps almost every candidate) are copied straight and
+// empty tiles exit.
 template <typename V>
 __global__ void __launch_bounds__(CP_NT) k_flag_scatter(const uint64_t *__restrict__ keys,
                                                         const V *__restrict__ vals,
@@ -506,23 +511,33 @@ __global__ void __launch_bounds__(CP_NT) k_flag_scatter(const uint64_t *__restri
                                                         uint64_t *__restrict__ out_keys,
                                                         V *__restrict__ out_vals) {
   __shared__ uint32_t sw[CP_NT / 32];
-  int64_t base = (int64_t)blockIdx.x * CP_TILE + (int64_t)threadIdx.x * CP_IPT;
-  uint32_t c = 0;
-#pragma unroll
-  for (int i = 0; i < CP_IPT; ++i) {
-    int64_t idx = base + i;
-    if (idx < m && flags[idx]) ++c;
-  }
-  uint32_t tot;
-  uint32_t pos = block_exclusive_scan<CP_NT>(c, tot, sw) + tile_off[blockIdx.x];
-#pragma unroll
-  for (int i = 0; i < CP_IPT; ++i) {
-    int64_t idx = base + i;
-    if (idx < m && flags[idx]) {
-      out_keys[pos] = keys[idx];
-      if (vals) out_vals[pos] = vals[idx];
-      ++pos;
+  const int64_t base = (int64_t)blockIdx.x * CP_TILE;
+  const uint32_t t0 = tile_off[blockIdx.x], tn = tile_off[blockIdx.x + 1] - t0;
+  if (tn == 0) return;
+  const int64_t valid = min((int64_t)CP_TILE, m - base);
+  if ((int64_t)tn == valid) {
+#pragma unroll 4
+    for (int i = 0; i < CP_IPT; ++i) {
+      const int64_t k = (int64_t)i * CP_NT + threadIdx.x;
+      if (k < valid) {
+        out_keys[t0 + k] = keys[base + k];
+        if (vals) out_vals[t0 + k] = vals[base + k];
+      }
     }
+    return;
+  }
+  uint32_t run = t0;
+  for (int i = 0; i < CP_IPT; ++i) {
+    const int64_t idx = base + (int64_t)i * CP_NT + threadIdx.x;
+    const uint32_t f = (idx < m && flags[idx]) ? 1u : 0u;
+    uint32_t tot;
+    const uint32_t ex = block_exclusive_scan<CP_NT>(f, tot, sw);
+    if (f) {
+      out_keys[run + ex] = keys[idx];
+      if (vals) out_vals[run + ex] = vals[idx];
+    }
+    run += tot;
+    __syncthreads();                     // sw is reused by the next scan
   }
 }
 

@@ -1,3 +1,3 @@
-timeout 900 python bench.py --config cfg4 --no-cpu-baseline --no-quality --e2e-steps 0 --steps 3 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],1), {k: round(v,1) for k,v in d['stage_ms'].items()})"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/cfg4_launches.csv python tools/run_build.py --config cfg4 --reps 1 > /dev/null 2>&1; echo ncu=$?
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -1
+for c in cfg3 cfg4 cfg5; do timeout 900 python bench.py --config $c --no-cpu-baseline --no-quality --e2e-steps 0 --steps 4 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['ms_per_step'],3), round(d['stage_ms'].get('compact',0),3), d['counts']['edges'])"; done
