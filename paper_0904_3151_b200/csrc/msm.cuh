@@ -1182,6 +1182,8 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
   __shared__ uint64_t tmask_s[MSM_MAXT * W];
   __shared__ uint8_t b2b[EG_MAX_LENGTH];
   __shared__ uint32_t sraw, sneu;
+  __shared__ uint32_t sw_spill[MSM_SPILL_T / 32];
+  __shared__ unsigned long long sbase;
   for (int i = threadIdx.x; i < a.L; i += MSM_SPILL_T) b2b[i] = a.bit2blk[i];
   const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (unsigned long long sb = 0; sb < nspill; ++sb) {
@@ -1229,16 +1231,18 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
       __syncthreads();
       const uint32_t i = threadIdx.x;
       uint32_t my_raw = 0, my_new = 0, my_eq = 0;
+      uint32_t emask[MSM_SPILL_T / 32] = {};   // emitted partners j of this row
+      uint32_t ra = 0;
       if (ia0 + i < s) {
         const uint64_t e = ea[i];
-        const uint32_t h2 = (uint32_t)(e >> 32), ra = (uint32_t)e;
+        const uint32_t h2 = (uint32_t)(e >> 32);
+        ra = (uint32_t)e;
         uint64_t ca[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) ca[w] = __ldg(codes + (int64_t)ra * W + w);
         const uint32_t jlo = (ta == tb) ? i + 1 : 0;
         for (uint32_t j = jlo; j < MSM_SPILL_T; ++j) {
           const uint64_t f = eb[j];
-          bool emit = false;
           if (ib0 + j < s && (uint32_t)(f >> 32) == h2) {
             uint64_t cb[W];
             uint64_t kd = 0;
@@ -1251,19 +1255,35 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
               int v = pair_verdict<W>(ca, cb, ra, rb, a, tt, kept, rep, b2b);
               my_raw += v > 0;
               my_new += v == 2;
-              emit = v == 2;
-            }
-          }
-          {  // warp-aggregated emission (one global atomic per warp step)
-            const uint32_t rb = (uint32_t)f;
-            const unsigned long long slot = warp_append(emit, &a.ctr[0]);
-            if (emit && slot < a.out_cap) {
-              a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-              if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+              if (v == 2) emask[j >> 5] |= 1u << (j & 31);
             }
           }
         }
         if (count_groups && my_eq) atomicAdd(&gc[ia0 + i], my_eq);
+      }
+      // one global reservation per tile pair (a per-warp-step atomic on the
+      // shared output counter serialised giant-group buckets), then every
+      // thread writes its emitted pairs at its offset
+      uint32_t tot;
+      const uint32_t off = block_exclusive_scan<MSM_SPILL_T>(my_new, tot, sw_spill);
+      if (threadIdx.x == 0) sbase = tot ? atomicAdd(&a.ctr[0], (unsigned long long)tot) : 0ull;
+      __syncthreads();
+      if (my_new) {
+        unsigned long long slot = sbase + off;
+#pragma unroll
+        for (int q = 0; q < MSM_SPILL_T / 32; ++q) {
+          uint32_t mbits = emask[q];
+          while (mbits) {
+            const int b = __ffs(mbits) - 1;
+            mbits &= mbits - 1;
+            const uint32_t rb = (uint32_t)eb[q * 32 + b];
+            if (slot < a.out_cap) {
+              a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+              if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+            }
+            ++slot;
+          }
+        }
       }
       if (my_raw) atomicAdd(&sraw, my_raw);
       if (my_new) atomicAdd(&sneu, my_new);
