@@ -171,3 +171,41 @@ def test_write_edges_chunked_equals_single_call(eg, tmp_path, monkeypatch):
     monkeypatch.setenv("EG_FORMAT_CHUNK", "997")
     eg.write_edges(b, edges, {"nodes": 7})
     assert a.read_bytes() == b.read_bytes()
+
+
+# ------------------------------------------------------------------ pools
+@pytest.mark.parametrize("length", [1, 7, 60, 64, 65, 128, 130])
+def test_pool_round_trip_and_reference_bytes(tmp_path, length):
+    import struct
+    from paper_0904_3151_b200 import BitStringPool, read_pool, write_pool
+    rng = np.random.default_rng(length)
+    bits = (rng.random((9, length)) < 0.5).astype(np.uint8)
+    pool = BitStringPool.from_bits(bits)
+    path = tmp_path / "p.bin"
+    write_pool(path, pool)
+    raw = path.read_bytes()
+    row_bytes = -(-length // 8)
+    assert raw[:24] == struct.pack("<4sIQQ", b"EPGP", 1, 9, length)
+    assert len(raw) == 24 + 9 * row_bytes
+    # byte b of a row holds bits 8b..8b+7, bit t at position t % 8
+    packed = np.packbits(bits, axis=1, bitorder="little")
+    assert raw[24:] == packed.tobytes()
+    back = read_pool(path)
+    assert back.length == length
+    np.testing.assert_array_equal(back.words, pool.words)
+
+
+def test_pool_rejects_padding_and_magic(tmp_path):
+    from paper_0904_3151_b200 import BitStringPool, DataError, read_pool, write_pool
+    rng = np.random.default_rng(5)
+    pool = BitStringPool.from_bits((rng.random((4, 60)) < 0.5).astype(np.uint8))
+    path = tmp_path / "p.bin"
+    write_pool(path, pool)
+    raw = bytearray(path.read_bytes())
+    raw[-1] |= 0xF0
+    path.write_bytes(bytes(raw))
+    with pytest.raises(DataError, match="padding"):
+        read_pool(path)
+    path.write_bytes(b"EPGX" + b"\x00" * 40)
+    with pytest.raises(DataError):
+        read_pool(path)
