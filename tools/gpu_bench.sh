@@ -1,2 +1,4 @@
-for kb in 128 160 212; do EG_HIST_SMEM_KB=$kb timeout 900 python bench.py --no-cpu-baseline --no-quality --e2e-steps 0 --steps 8 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); print('kb=$kb', round(d['ms_per_step'],3), round(d['stage_ms']['msm_stage'],3), d['parity']['match'])"; done
+timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py --no-cpu-baseline --e2e-steps 1 --steps 5 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3), d['parity']['match'], d['quality']['recall'])"
