@@ -43,6 +43,8 @@ extern "C" {
 /* Largest string length / block count the enumeration kernels support. */
 #define EG_MAX_LENGTH 256
 #define EG_MAX_BLOCKS 64
+/* replicates a pair tag can name (d_out_rep is uint16)                   */
+#define EG_MAX_REPLICATES 65535
 
 const char *eg_last_error(void);
 int eg_version(void);
@@ -163,7 +165,7 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k,
 int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
                  int32_t replicates, const int32_t *h_block_bounds, int32_t k,
                  int32_t d, const int32_t *h_unit_rep, const uint64_t *h_unit_mask,
-                 int64_t n_units, uint64_t *d_out_keys, uint8_t *d_out_rep,
+                 int64_t n_units, uint64_t *d_out_keys, uint16_t *d_out_rep,
                  int64_t capacity, int64_t *h_counts, void *d_workspace,
                  size_t workspace_bytes, void *stream);
 
@@ -171,13 +173,13 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
 /* pairs emitted by eg_msm_pairs with d_out_rep: d_keep[p] = 1 iff the     */
 /* pair's Hamming distance exceeds d in every replicate before its own.   */
 /* h_new_counts[replicates] receives the survivors per replicate.         */
-int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+int eg_xrep_filter(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
                    const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
                    int32_t replicates, uint8_t *d_keep, int64_t *h_new_counts,
                    void *stream);
 /* Same, without synchronising: the survivor counts go to device memory   */
 /* d_new_counts[replicates] (valid once the stream reaches this point).   */
-int eg_xrep_filter_async(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+int eg_xrep_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
                          const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
                          int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,
                          void *stream);

@@ -462,3 +462,48 @@ void or_cosine_dist(const double *x, int64_t n, int32_t dim, const int64_t *pair
         dist[p] = dd;
     }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Exhaustive Hamming pairs, digest form: exact.py:99-121 (brute_force_     */
+/* hamming) restated for subsets whose answer is too large to hold as a     */
+/* pair list (config 4's 50k-member clusters: ~1.6e9 pairs).  Every pair    */
+/* (a<b) of the rows with popcount(xor) <= d contributes key = (ids[a] <<   */
+/* 32 | ids[b]) (ids: sorted global row ids) through an order-independent   */
+/* digest: out[0] = count, out[1] = sum of mix(key) mod 2^64, out[2] = xor  */
+/* of mix(key).  mix = splitmix64's finaliser.                             */
+/* ------------------------------------------------------------------------ */
+static inline uint64_t or_mix(uint64_t z)
+{
+    z ^= z >> 30; z *= 0xbf58476d1ce4e5b9ULL;
+    z ^= z >> 27; z *= 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return z;
+}
+
+void or_bf_hamming_digest(const uint64_t *words, const int64_t *ids, int64_t n, int32_t W,
+                          int32_t d, uint64_t *out, int32_t threads)
+{
+    uint64_t cnt = 0, sum = 0, xr = 0;
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#pragma omp parallel for schedule(dynamic, 64) reduction(+:cnt, sum) reduction(^:xr)
+#endif
+    for (int64_t a = 0; a < n; ++a) {
+        const uint64_t *wa = words + a * W;
+        const uint64_t ia = (uint64_t)ids[a] << 32;
+        for (int64_t b = a + 1; b < n; ++b) {
+            const uint64_t *wb = words + b * W;
+            int32_t dist = 0;
+            for (int32_t w = 0; w < W; ++w) dist += __builtin_popcountll(wa[w] ^ wb[w]);
+            if (dist <= d) {
+                const uint64_t m = or_mix(ia | (uint64_t)ids[b]);
+                ++cnt;
+                sum += m;
+                xr ^= m;
+            }
+        }
+    }
+    out[0] = cnt;
+    out[1] = sum;
+    out[2] = xr;
+}

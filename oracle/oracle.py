@@ -62,6 +62,8 @@ def _load():
     lib.or_free.argtypes = [P]
     lib.or_first_witness.argtypes = [P, i64, P, i32, i32, i32, P]
     lib.or_cosine_dist.argtypes = [P, i64, i32, P, i64, P, i32]
+    lib.or_bf_hamming_digest.argtypes = [P, P, i64, i32, i32, P, i32]
+    lib.or_bf_hamming_digest.restype = None
     _lib = lib
     return lib
 
@@ -170,6 +172,31 @@ def brute_force_hamming(words, d):
     if not chunks:
         return np.empty((0, 2), dtype=np.int64)
     return np.vstack(chunks).astype(np.int64)
+
+
+def bf_hamming_digest(words, ids, d, threads=0):
+    """exact.py:99-121 in digest form (see or_bf_hamming_digest): (count,
+    sum of mix(key) mod 2^64, xor of mix(key)) over all pairs a < b of the
+    rows with popcount(xor) <= d, keys built from the global ``ids``."""
+    words = np.ascontiguousarray(words, dtype=np.uint64)
+    if words.ndim == 1:
+        words = words.reshape(-1, 1)
+    ids = np.ascontiguousarray(ids, dtype=np.int64)
+    out = np.zeros(3, dtype=np.uint64)
+    _load().or_bf_hamming_digest(_ptr(words), _ptr(ids), words.shape[0], words.shape[1], d,
+                                 _ptr(out), threads)
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def mix_digest(keys) -> tuple:
+    """The same digest over uint64 pair keys (i << 32 | j), numpy side."""
+    z = np.asarray(keys).view(np.uint64).copy()
+    z ^= z >> np.uint64(30)
+    z *= np.uint64(0xbf58476d1ce4e5b9)
+    z ^= z >> np.uint64(27)
+    z *= np.uint64(0x94d049bb133111eb)
+    z ^= z >> np.uint64(31)
+    return int(z.size), int(z.sum(dtype=np.uint64)), int(np.bitwise_xor.reduce(z)) if z.size else 0
 
 
 def first_witness(pairs, earlier_words, d):

@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -86,17 +87,39 @@ static int arg_error(const char *msg) {
 }
 
 static int num_sms() {
-  static int cached = 0;
-  if (!cached) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
-      cached = 148;
+  static int cached[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!cached[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v < 1)
+      v = 148;
+    cached[dev] = v;
   }
-  return cached;
+  return cached[dev];
 }
 
 static int env_int(const char *name, int dflt);
+
+// Dynamic shared-memory opt-in.  The attribute lives in the device context,
+// so the record of what was already set is kept per (device, kernel): a
+// process that builds on cuda:0 and then on cuda:1 sets it on both.
+static cudaError_t smem_optin(const void *func, size_t bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void *>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t &have = done[std::make_pair(dev, func)];
+  if (bytes <= have) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+#define EG_SMEM_OPTIN(func, bytes) EG_CUDA_TRY(smem_optin((const void *)(func), (size_t)(bytes)))
 
 // ------------------------------------------------------------ projection
 static int project_tn(int cols) {
@@ -238,33 +261,11 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
   const size_t smem_medium = sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>);
   a.gcnt_min = MediumCfg<W>::CAP;
   const size_t smem_tsort = (size_t)MSM_TILE * 8 + (size_t)lay.B * 4;
-  static size_t set_tsort = 0;
-  if (lay.tiled && smem_tsort > set_tsort) {
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_tsort<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_tsort));
-    set_tsort = smem_tsort;
-  }
-  static size_t set_hist = 0, set_scatter = 0;
-  static bool set_fixed = false;
-  if (smem_hist > set_hist) {
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_hist<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_hist));
-    set_hist = smem_hist;
-  }
-  if (smem_scatter > set_scatter) {
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_scatter<W>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_scatter));
-    set_scatter = smem_scatter;
-  }
-  if (!set_fixed) {
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_group<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_group));
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_medium<W>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_medium));
-    set_fixed = true;
-  }
+  if (lay.tiled) EG_SMEM_OPTIN(k_msm_tsort<W>, smem_tsort);
+  EG_SMEM_OPTIN(k_msm_hist<W>, smem_hist);
+  EG_SMEM_OPTIN(k_msm_scatter<W>, smem_scatter);
+  EG_SMEM_OPTIN(k_msm_group<W>, smem_group);
+  EG_SMEM_OPTIN(k_msm_medium<W>, smem_medium);
   const unsigned tiles = (unsigned)((a.n + MSM_TILE - 1) / MSM_TILE);
   const unsigned spill_grid = (unsigned)num_sms() * 8;
   // Two scratch sets on two streams: the caller's stream runs hist / scan /
@@ -527,33 +528,18 @@ static int run_band_fixup(const void *d_x, int32_t dim, const double *d_r, int64
                      COLLECT_NT, 0, st>>>(unc, n, W, length, replicates, items, cnt, cap);
     if (env_int("EG_FIXUP_LIST", 0)) {   // thread-per-entry variant (comparison)
       const size_t fxs = fixl_smem(cols);
-      static size_t fixl_set = 0;
-      if (fxs > 48 * 1024 && fxs > fixl_set) {
-        EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_list,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fxs));
-        fixl_set = fxs;
-      }
+      EG_SMEM_OPTIN(k_fixup_list, fxs);
       k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
           (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
     } else {
       const size_t fws = (size_t)(FIXW_NT / 32) * dim * 8;
-      static size_t fixw_set = 0;
-      if (fws > 48 * 1024 && fws > fixw_set) {
-        EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_warp,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)fws));
-        fixw_set = fws;
-      }
+      EG_SMEM_OPTIN(k_fixup_warp, fws);
       k_fixup_warp<<<(unsigned)num_sms() * 8, FIXW_NT, fws, st>>>(
           (const float *)d_x, dim, d_r, n, length, W, d_codes, items, cnt, cap,
           env_int("EG_FIXUP_FORCE_SEQ", 0));
     }
     const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
-    if (fsm > 48 * 1024)
-      EG_CUDA_TRY(cudaFuncSetAttribute(k_fixup_bits,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)fsm));
+    EG_SMEM_OPTIN(k_fixup_bits, fsm);
     const unsigned fg = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
     k_fixup_bits<<<fg, 256, fsm, st>>>((const float *)d_x, n, dim, d_r, length, W,
                                        replicates, d_codes, unc, cnt, cap);
@@ -643,12 +629,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
                                            (budget - no * ob) / H16_XSLOT);
       if (nx < 2) return arg_error("eg_project: too many direction columns for the f16 path");
       const size_t smem = nx * H16_XSLOT + no * ob + sizeof(H16Bars) + 1024;
-      static size_t h16_smem_set = 0;
-      if (smem > h16_smem_set) {
-        EG_CUDA_TRY(cudaFuncSetAttribute(k_project_h16,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        h16_smem_set = smem;
-      }
+      EG_SMEM_OPTIN(k_project_h16, smem);
       {
         EG_PROF(PC_PROJECT, st);
         k_project_h16<<<grid, H16_THREADS, smem, st>>>(
@@ -664,12 +645,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
       const size_t sbytes = tc2_stage_bytes(npad);
       const int nstages = (int)std::min<size_t>(env_int("EG_TC2_STAGES", 4), ((size_t)212 << 10) / sbytes);
       const size_t smem = nstages * sbytes + sizeof(Tc2Bars) + 1024;
-      static size_t tc2_smem_set = 0;
-      if (smem > tc2_smem_set) {
-        EG_CUDA_TRY(cudaFuncSetAttribute(k_project_tc2,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tc2_smem_set = smem;
-      }
+      EG_SMEM_OPTIN(k_project_tc2, smem);
       uint64_t *unc = ar.take<uint64_t>((size_t)replicates * n * W);
       if (!unc) {
         set_error("eg_project: workspace too small");
@@ -690,12 +666,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
                             cnt, cap, d_fixups, st);
     } else {
       const size_t smem = 2 * tc_stage_bytes(npad) + sizeof(TcSmem) + 1024;
-      static size_t tc_smem_set = 0;
-      if (smem > tc_smem_set) {
-        EG_CUDA_TRY(cudaFuncSetAttribute(k_project_tc,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        tc_smem_set = smem;
-      }
+      EG_SMEM_OPTIN(k_project_tc, smem);
       EG_PROF(PC_PROJECT, st);
       k_project_tc<<<grid, TC_NT, smem, st>>>((const float *)d_x, n, dim, img, cols, npad,
                                               d_norms, d_rnorm, tc_tau(dim), length, W, d_codes,
@@ -881,8 +852,7 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     EG_PROF(PC_MISC, st);
 #define EG_PLAN_CASE(WW)                                                                     \
   case WW:                                                                                   \
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_msm_plan<WW>,                                         \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    EG_SMEM_OPTIN(k_msm_plan<WW>, smem);                                                     \
     k_msm_plan<WW><<<P, PLAN_NT, smem, st>>>(d_codes, n, d_samp, d_kept, d_pairs, d_max);    \
     break;
     switch (W) {
@@ -948,7 +918,7 @@ size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates) {
 int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t replicates,
                  const int32_t *h_block_bounds, int32_t k, int32_t d, const int32_t *h_unit_rep,
                  const uint64_t *h_unit_mask, int64_t n_units, uint64_t *d_out_keys,
-                 uint8_t *d_out_rep, int64_t capacity, int64_t *h_counts, void *d_workspace,
+                 uint16_t *d_out_rep, int64_t capacity, int64_t *h_counts, void *d_workspace,
                  size_t workspace_bytes, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 1 || n >= (1ll << 32)) return arg_error("eg_msm_pairs: need 1 <= n < 2^32");
@@ -956,7 +926,8 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
     return arg_error("eg_msm_pairs: length outside [1, 256]");
   if (!(0 <= d && d < k && k <= length) || k > EG_MAX_BLOCKS)
     return arg_error("eg_msm_pairs: need 0 <= d < k <= min(length, 64)");
-  if (replicates < 1) return arg_error("eg_msm_pairs: replicates < 1");
+  if (replicates < 1 || replicates > EG_MAX_REPLICATES)
+    return arg_error("eg_msm_pairs: replicates outside [1, 65535] (the pair tag is 16 bits)");
   const int W = (length + 63) / 64;
   if (h_block_bounds[0] != 0 || h_block_bounds[k] != length)
     return arg_error("eg_msm_pairs: block bounds must span [0, length]");
@@ -1094,12 +1065,12 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   return EG_OK;
 }
 
-int eg_xrep_filter_async(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+int eg_xrep_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
                          const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
                          int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,
                          void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (replicates < 1 || replicates > 255 || W < 1 || W > 4 || m < 0)
+  if (replicates < 1 || replicates > EG_MAX_REPLICATES || W < 1 || W > 4 || m < 0)
     return arg_error("eg_xrep_filter: bad arguments");
   EG_CUDA_TRY(cudaMemsetAsync(d_new_counts, 0, 8 * (size_t)replicates, st));
   if (m > 0) {
@@ -1112,11 +1083,12 @@ int eg_xrep_filter_async(const uint64_t *d_keys, const uint8_t *d_reps, int64_t 
   return EG_OK;
 }
 
-int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
+int eg_xrep_filter(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
                    const uint64_t *d_codes, int64_t n, int32_t W, int32_t d, int32_t replicates,
                    uint8_t *d_keep, int64_t *h_new_counts, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (replicates < 1 || replicates > 255) return arg_error("eg_xrep_filter: replicates outside [1, 255]");
+  if (replicates < 1 || replicates > EG_MAX_REPLICATES)
+    return arg_error("eg_xrep_filter: replicates outside [1, 65535]");
   // per-device counter block, allocated once: a stream-ordered allocation
   // here released its pool at every synchronise and stalled some calls by
   // tens of ms.  The mutex covers the call up to its final synchronise.
@@ -1125,7 +1097,7 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint8_t *d_reps, int64_t m,
   std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   EG_CUDA_TRY(cudaGetDevice(&dev));
-  if (!small[dev]) EG_CUDA_TRY(cudaMalloc(&small[dev], 8 * 256));
+  if (!small[dev]) EG_CUDA_TRY(cudaMalloc(&small[dev], 8 * (size_t)EG_MAX_REPLICATES));
   unsigned long long *nc = small[dev];
   EG_CUDA_TRY(cudaMemsetAsync(nc, 0, 8 * (size_t)replicates, st));
   if (m > 0) {
@@ -1403,12 +1375,7 @@ int eg_bf_cosine_candidates(const void *d_x, int x_is_f64, int64_t n, int32_t di
   const size_t budget = ((size_t)220 << 10) - sizeof(BfBars) - 1024;
   const int nb = (int)std::min<size_t>(BF_MAXSTAGES, (budget - nkc * BF_ACHUNK) / BF_BSTAGE);
   const size_t smem = nkc * BF_ACHUNK + nb * BF_BSTAGE + sizeof(BfBars) + 1024;
-  static size_t bf_smem_set = 0;
-  if (smem > bf_smem_set) {
-    EG_CUDA_TRY(cudaFuncSetAttribute(k_bf_cosine_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    bf_smem_set = smem;
-  }
+  EG_SMEM_OPTIN(k_bf_cosine_tc, smem);
   const int64_t ti = (n + BF_BM - 1) / BF_BM;
   const unsigned grid = (unsigned)std::min<int64_t>(ti, (int64_t)num_sms());
   {

@@ -91,7 +91,7 @@ struct MsmArgs {
   int gcnt_min;                  // spilled buckets above this size count groups
   int hist_smem;                  // dynamic shared memory of k_msm_hist (bytes)
   int scatter_staged;             // 1: k_msm_scatter reorders runs in smem
-  uint8_t *out_rep;              // non-null: emit raw pairs tagged with their
+  uint16_t *out_rep;             // non-null: emit raw pairs tagged with their
                                  // replicate; the cross-replicate rule runs
                                  // later in k_xrep_filter (off the group
                                  // kernels' critical path)
@@ -889,7 +889,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
           slot = __shfl_sync(active, slot, leader) + __popc(smask & ((1u << lane) - 1u));
           if (spill && slot < a.out_cap) {
             a.out_keys[slot] = key;
-            if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+            if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
           }
         }
       }
@@ -912,7 +912,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
             const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
             if (slot < a.out_cap) {
               a.out_keys[slot] = key;
-              if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+              if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
             }
           }
         }
@@ -953,7 +953,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     for (uint32_t i = threadIdx.x; i < nst; i += NT) {
       if (base + i < a.out_cap) {
         a.out_keys[base + i] = S.outbuf()[i];
-        if (a.out_rep) a.out_rep[base + i] = (uint8_t)rep;
+        if (a.out_rep) a.out_rep[base + i] = (uint16_t)rep;
       }
     }
     __syncthreads();
@@ -1282,7 +1282,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
             const uint32_t rb = (uint32_t)eb[q * 32 + b];
             if (slot < a.out_cap) {
               a.out_keys[slot] = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-              if (a.out_rep) a.out_rep[slot] = (uint8_t)rep;
+              if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
             }
             ++slot;
           }
@@ -1320,12 +1320,13 @@ __global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
 // Deferred form of the fold in pipeline.py:286-314: a raw pair of replicate
 // h survives iff its Hamming distance exceeds d in every replicate g < h.
 // Counts survivors per replicate (per_replicate_new).
-__global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint8_t *__restrict__ reps,
+constexpr int XREP_SMEM_REPS = 1024;   // replicates counted in shared memory
+__global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint16_t *__restrict__ reps,
                               int64_t m, const uint64_t *__restrict__ codes, int64_t n, int W,
                               int d, int nreps, uint8_t *__restrict__ keep,
                               unsigned long long *__restrict__ new_counts) {
-  __shared__ unsigned int cnt[256];
-  for (int i = threadIdx.x; i < nreps && i < 256; i += blockDim.x) cnt[i] = 0;
+  __shared__ unsigned int cnt[XREP_SMEM_REPS];
+  for (int i = threadIdx.x; i < nreps && i < XREP_SMEM_REPS; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -1340,10 +1341,13 @@ __global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint8_t *
       ok = pc > d;
     }
     keep[p] = ok;
-    if (ok) atomicAdd(&cnt[h], 1u);
+    if (ok) {
+      if (h < XREP_SMEM_REPS) atomicAdd(&cnt[h], 1u);
+      else atomicAdd(&new_counts[h], 1ull);
+    }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < nreps && i < 256; i += blockDim.x)
+  for (int i = threadIdx.x; i < nreps && i < XREP_SMEM_REPS; i += blockDim.x)
     if (cnt[i]) atomicAdd(&new_counts[i], (unsigned long long)cnt[i]);
 }
 

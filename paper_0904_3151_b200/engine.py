@@ -229,7 +229,7 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     defer = reps > 1       # cross-replicate rule in a separate streaming pass
     while True:
         out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
-        rtag = torch.empty(max(capacity, 1), dtype=torch.uint8, device=dev) if defer else None
+        rtag = torch.empty(max(capacity, 1), dtype=torch.int16, device=dev) if defer else None
         rc = lib.eg_msm_pairs(_p(codes), n, length, reps, bb.ctypes.data, k, d, ur.ctypes.data,
                               um.ctypes.data, len(ur), _p(out), _p(rtag), capacity,
                               ctypes_addr(counts), _p(ws), ws.numel(), _stream(dev))

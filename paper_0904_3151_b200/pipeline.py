@@ -120,22 +120,31 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
     bad = None
     fix = None
     reps = list(range(1, params.replicates + 1))
+    flags_ready = None
     if norms is None and codes is None:
         # one pass over the rows: norms + flags fused into the projection
         codes, norms, bad, fix = engine.project_rows(x, params.length, params.seed, reps)
-        # the flags travel to pinned host memory behind the projection and
-        # are checked after the next synchronising call (no extra bubble)
+    else:
+        if norms is None:
+            norms, bad = engine.row_stats_async(x)
+        if codes is None:
+            codes, fix = engine.project_codes(x, norms, params.length, params.seed, reps)
+    if bad is not None:
+        # the flags travel to pinned host memory behind the projection; they
+        # are checked before any unit runs (zero-norm / NaN rows share the
+        # all-zero code and would form one giant group), after the plan's own
+        # synchronisation when it makes one
         bad_host = torch.empty(bad.shape, dtype=bad.dtype, pin_memory=True)
         bad_host.copy_(bad, non_blocking=True)
         bad = bad_host
-    else:
-        if norms is None:
-            norms, bad = engine.row_stats_async(x)     # checked once msm_pairs syncs
-        if codes is None:
-            codes, fix = engine.project_codes(x, norms, params.length, params.seed, reps)
+        flags_ready = torch.cuda.Event()
+        flags_ready.record()
     ev[1].record()
     if blocks is None:
         blocks = engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
+    if flags_ready is not None:
+        flags_ready.synchronize()
+        engine.raise_bad_rows(bad)
     bounds = _bounds(params.length, blocks)
     if units is None:
         ureps, umasks = engine.units_for(range(params.replicates), blocks, params.mismatch)
@@ -143,8 +152,6 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
         ureps, umasks = units
     keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, ureps, umasks)
     info["blocks"] = blocks
-    if bad is not None:
-        engine.raise_bad_rows(bad)
     ev[2].record()
     engine.sort_pair_keys(keys, n)
     ev[3].record()
@@ -236,7 +243,12 @@ def filter_exact(data, candidates, epsilon: float, block_pairs: int = 1 << 20, *
         pairs = candidates.array
     else:
         pairs = np.asarray(candidates, dtype=np.int64).reshape(-1, 2)
-    rows = data.vectors if isinstance(data, VectorDataset) else data
+    if isinstance(data, torch.Tensor):
+        rows = data
+    else:
+        # the reference validates through as_dataset (pipeline.py:197): list
+        # input is accepted, a non-finite row raises DataError
+        rows = data.vectors if isinstance(data, VectorDataset) else VectorDataset(data).vectors
     n = rows.shape[0]
     if pairs.size and (pairs.min() < 0 or pairs.max() >= n):
         raise IndexError("candidate index out of range")
@@ -245,7 +257,9 @@ def filter_exact(data, candidates, epsilon: float, block_pairs: int = 1 << 20, *
     dev = engine.require_device(device)
     with torch.cuda.device(dev):
         x = engine.as_device_rows(rows, dev)
-        norms, _, _ = engine.row_stats(x)
+        norms, nonfinite, _ = engine.row_stats(x)
+        if nonfinite != -1:
+            raise DataError(f"row {nonfinite} has a non-finite entry")
         keys = torch.from_numpy(engine.pairs_to_keys(pairs)).to(dev)
         engine.sort_pair_keys(keys, n)
         ek, ed = engine.verify(x, norms, keys, _metric_id(metric), epsilon)

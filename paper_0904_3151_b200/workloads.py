@@ -97,11 +97,13 @@ def cfg3_points(n: int = 1_600_000, dim: int = 384, planted_rows: int | None = N
 
 
 def cfg4_points(n: int = 4_000_000, dim: int = 128, largest: int = 50_000,
-                subset: int | None = None, seed: int = 0) -> np.ndarray:
+                subset: int | None = None, seed: int = 0, labels: bool = False):
     """Config 4: rank-size Zipf(1.2) clusters (sigma 0.05) plus N(0,I) singletons.
 
     Cluster r has floor(largest * r^-1.2) members (kept when >= 2); rows are
     normalised in float64, permuted, optionally row-subsampled, cast to f32.
+    ``labels=True`` also returns each row's cluster rank (0 = largest, -1 =
+    singleton); the random stream is the same either way.
     """
     rng = np.random.default_rng(seed)
     ranks = np.arange(1, 100_000, dtype=np.float64)
@@ -116,25 +118,38 @@ def cfg4_points(n: int = 4_000_000, dim: int = 128, largest: int = 50_000,
              + 0.05 * rng.standard_normal((m, dim)))
     x[m:] = rng.standard_normal((n - m, dim))
     x = _normalise64(x)
-    x = x[rng.permutation(n)]
+    perm = rng.permutation(n)
+    x = x[perm]
+    lab = None
+    if labels:
+        lab = np.full(n, -1, dtype=np.int64)
+        lab[:m] = np.repeat(np.arange(sizes.size), sizes)
+        lab = lab[perm]
     if subset is not None:
-        x = x[np.sort(rng.choice(n, subset, replace=False))]
-    return x.astype(np.float32)
+        sel = np.sort(rng.choice(n, subset, replace=False))
+        x = x[sel]
+        lab = lab[sel] if labels else None
+    x = x.astype(np.float32)
+    return (x, lab) if labels else x
 
 
 def cfg5_points(n: int = 20_000_000, dim: int = 128, clusters: int = 1_000_000,
-                seed: int = 0) -> np.ndarray:
-    """Config 5: Gaussian clusters (sigma 0.05) normalised per 2^20-row block."""
+                seed: int = 0, labels: bool = False):
+    """Config 5: Gaussian clusters (sigma 0.05) normalised per 2^20-row block.
+    ``labels=True`` also returns each row's cluster id (same random stream)."""
     rng = np.random.default_rng(seed)
     centres = rng.standard_normal((clusters, dim), dtype=np.float32)
     out = np.empty((n, dim), dtype=np.float32)
+    labs = np.empty(n, dtype=np.int64) if labels else None
     for lo in range(0, n, 1 << 20):
         rows = min(1 << 20, n - lo)
         lab = rng.integers(0, clusters, rows)
         blk = centres[lab] + 0.05 * rng.standard_normal((rows, dim), dtype=np.float32)
         blk /= np.linalg.norm(blk, axis=1, keepdims=True)
         out[lo:lo + rows] = blk
-    return out
+        if labels:
+            labs[lo:lo + rows] = lab
+    return (out, labs) if labels else out
 
 
 def planted_clusters(n, dim, clusters, cluster_size, spread, seed):
@@ -151,3 +166,24 @@ def planted_clusters(n, dim, clusters, cluster_size, spread, seed):
     planted = planted + spread * rng.standard_normal(planted.shape)
     background = rng.standard_normal((n - clusters * cluster_size, dim))
     return np.vstack([planted, background]).astype(np.float32)
+
+
+def restricted_subset(labels: np.ndarray, clusters, extra: int = 20_000,
+                      seed: int = 4321) -> np.ndarray:
+    """Sorted row subset S for restricted-subset parity:
+    every member of the given clusters plus ``extra`` seeded random rows.
+    The Hamming pair set is a pairwise predicate, so (pairs of the full
+    build) restricted to S x S must equal the pairs enumerated on pool[S]."""
+    rng = np.random.default_rng(seed)
+    n = labels.shape[0]
+    pick = rng.choice(n, min(extra, n), replace=False)
+    members = np.nonzero(np.isin(labels, np.asarray(list(clusters), dtype=np.int64)))[0]
+    return np.unique(np.concatenate([members, pick])).astype(np.int64)
+
+
+def largest_clusters(labels: np.ndarray, count: int) -> list:
+    """Ids of the ``count`` most populous clusters (ties: smaller id first)."""
+    lab = labels[labels >= 0]
+    sizes = np.bincount(lab)
+    order = np.argsort(-sizes, kind="stable")
+    return [int(c) for c in order[:count]]

@@ -128,3 +128,53 @@ def test_cfg3_small_build(oracle, manifest):
     assert res.per_replicate_raw == tuple(rec["per_replicate_raw"])
     assert res.per_replicate_new == tuple(rec["per_replicate_new"])
     assert oracle.pair_digest(res.pairs) == rec["pairs_sha256"]
+
+
+def test_bf_hamming_digest_matches_pair_list(oracle):
+    """The digest form of the exhaustive Hamming join (used for the config-4
+    full-scale restriction) agrees with the pinned pair list."""
+    g = golden("exact")
+    words = g["ham_rand_words"]
+    ids = np.arange(words.shape[0], dtype=np.int64) * 3 + 5     # any increasing ids
+    for d in (0, 1, 3):
+        pairs = g[f"ham_rand_d{d}_pairs"]
+        keys = (ids[pairs[:, 0]].astype(np.uint64) << np.uint64(32)) | ids[pairs[:, 1]].astype(np.uint64)
+        assert oracle.bf_hamming_digest(words, ids, d) == oracle.mix_digest(keys)
+
+
+def _full_fixture(name):
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "full", f"{name}.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.slow
+def test_oracle_cfg4_ten_percent_vs_reference(oracle):
+    """The C oracle pinned against the reference's own config-4 answer at a
+    10% row sample (400k rows, 13.9M edges; tests/golden/full)."""
+    rec = _full_fixture("cfg4_10")
+    x = workloads.cfg4_points(4_000_000, subset=400_000)
+    g = oracle.build_graph(x, 0.08, 64, 2, 16, 1, 0, keep_codes=True)
+    assert oracle.words_digest(g.codes[0]) == rec["codes_sha256"][0]
+    assert list(g.per_replicate_raw) == rec["per_replicate_raw"]
+    assert g.candidate_count == rec["candidate_count"]
+    assert not rec["band"]["pairs"]
+    assert oracle.pair_digest(g.pairs) == rec["edges_sha256"]
+    assert abs(float(np.sum(g.distances)) - rec["distance_sum"]) <= 1e-12 * len(g.distances)
+
+
+@pytest.mark.slow
+def test_oracle_cfg4_full_subset_vs_reference(oracle):
+    """SURVEY.md 8(c) restriction at full config 4: the oracle's
+    enumerate_pairs on pool[S] equals the reference's (whole clusters 3-5 +
+    20k random rows of the n=4M input)."""
+    rec = _full_fixture("cfg4_full")["subset_mid"]
+    x, lab = workloads.cfg4_points(labels=True)
+    S = workloads.restricted_subset(lab, rec["clusters"], rec["extra"], rec["seed"])
+    assert oracle.words_digest(S) == rec["rows_sha256"]
+    w = oracle.project_words(x[S], 64, 0, 1)
+    assert oracle.words_digest(w) == rec["codes_sha256"][0]
+    pairs, _ = oracle.enumerate_pairs(w, 64, oracle.block_partition(64, 16), 2)
+    assert oracle.pair_digest(S[pairs]) == rec["raw_sha256"][0]
