@@ -278,6 +278,35 @@ def test_lsh_only_matches_reference(eg, manifest):
     np.testing.assert_array_equal(graph.edge_list.pairs, g["lsh_edges"])
 
 
+def test_lsh_only_default_300_replicates(eg, oracle):
+    """build_graph_lsh_only's default replicates=300 (pipeline.py:383-408;
+    the reference's test_acceptance.py calls it so): replicate tags wider
+    than 8 bits, counts and edges equal to the oracle's d=0, k=1 build."""
+    g = golden("small_build")
+    graph = eg.build_graph_lsh_only(g["x"], 0.05, 1e-3)
+    assert graph.params.replicates == 300
+    ref = oracle.build_graph(g["x"], 0.05, graph.params.length, 0, 1, 300, 0)
+    assert graph.stats.per_replicate_raw == ref.per_replicate_raw
+    assert graph.stats.per_replicate_new == ref.per_replicate_new
+    np.testing.assert_array_equal(graph.edge_list.pairs, ref.pairs)
+
+
+def test_bad_rows_rejected_before_enumeration(eg):
+    """Many zero / NaN rows share the all-zero code: the DataError must come
+    before the units run (no giant-group enumeration)."""
+    import time
+    params = eg.MsmParams(0.05, 1e-3, 32, 2, 8, 2, 0)
+    x = np.random.default_rng(3).standard_normal((200_000, 16)).astype(np.float32)
+    x[1000:150_000] = 0.0
+    t0 = time.perf_counter()
+    with pytest.raises(eg.DataError, match="row 1000 has zero norm"):
+        eg.build_graph(x, params)
+    x[1000:150_000] = np.nan
+    with pytest.raises(eg.DataError, match="row 1000 has a non-finite entry"):
+        eg.build_graph(x, params)
+    assert time.perf_counter() - t0 < 30
+
+
 def test_build_edge_cases(eg):
     params = eg.MsmParams(0.05, 1e-3, 24, 2, 4, 2, 7)
     with pytest.raises(eg.DataError):
