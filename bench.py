@@ -48,16 +48,17 @@ def peaks():
 
 
 def make_inputs(name: str):
+    """(rows, cluster labels or None) of the full configuration."""
     if name == "cfg1":
-        return workloads.cfg1_points()
+        return workloads.cfg1_points(), None
     if name == "cfg2":
-        return workloads.cfg2_words()
+        return workloads.cfg2_words(), None
     if name == "cfg3":
-        return workloads.cfg3_points()
+        return workloads.cfg3_points(), None
     if name == "cfg4":
-        return workloads.cfg4_points()
+        return workloads.cfg4_points(labels=True)
     if name == "cfg5":
-        return workloads.cfg5_points()
+        return workloads.cfg5_points(labels=True)
     raise ValueError(name)
 
 
@@ -101,22 +102,98 @@ def sort_bytes_per_unit(n: int, cfg, blocks: int | None = None) -> int:
     return n * (8 * W + kb * 2 * (kb + 4))
 
 
-# Output counts of the reference's own CPU build at the full configs,
-# measured during the survey.
-REFERENCE_COUNTS = {
-    "cfg1": {"edges": 809_648, "candidates": 809_654},
-    "cfg2": {"edges": 500_000, "candidates": 500_000},
-    "cfg3": {"edges": 244_617, "candidates": 2_478_622, "raw": [1_942_637, 311_325, 713_791]},
-}
+# Parity of the timed build against the REFERENCE's own answer on the same
+# seeded input (untimed, after the timed region).  The answers are digests
+# the reference produced in the build container (tests/golden/make_golden
+# *.py): the full edge set for configs 1-3, and for configs 4-5 the SURVEY
+# 8(c) restriction of the full-scale build to a seeded subset S of whole
+# clusters + 20k random rows (the reference cannot run at n = 4M / 20M).
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
-def parity_vs_reference(config: str, counts):
-    ref = REFERENCE_COUNTS.get(config)
-    if not ref or not counts:
+def _fixture(name):
+    path = os.path.join(ROOT, "tests", "golden", "full", f"{name}.json")
+    if not os.path.exists(path):
         return None
-    got = {k: (list(counts[k]) if isinstance(counts.get(k), (list, tuple)) else counts.get(k))
-           for k in ref}
-    return {"reference": ref, "match": got == ref, "source": "SURVEY.md section 6 [measured]"}
+    with open(path) as f:
+        return json.load(f)
+
+
+def _edges_core_sha(pairs, rec):
+    band = {tuple(p) for p in rec["band"]["pairs"]}
+    if band:
+        pairs = pairs[np.array([tuple(p) not in band for p in pairs.tolist()], dtype=bool)]
+    return _sha(pairs)
+
+
+def _restrict(keys, rows, n):
+    import torch
+    ins = torch.zeros(n, dtype=torch.bool, device=keys.device)
+    ins[torch.from_numpy(rows).to(keys.device)] = True
+    out = []
+    for lo in range(0, keys.numel(), 1 << 27):
+        k = keys[lo:lo + (1 << 27)]
+        out.append(k[ins[k >> 32] & ins[k & 0xFFFFFFFF]])
+    return torch.cat(out) if out else keys[:0]
+
+
+def parity_vs_reference(config: str, last, labels, n):
+    if not last or last.get("keys") is None:
+        return None
+    from paper_0904_3151_b200 import engine
+    keys = last["keys"]
+    info = last.get("info") or {}
+    res = {"source": "reference epsgraph 0.1.0 run on the same seeded input "
+                     "(tests/golden/full, tests/golden/manifest.json)"}
+    checks = {}
+    if config == "cfg1":
+        with open(os.path.join(ROOT, "tests", "golden", "manifest.json")) as f:
+            rec = json.load(f)["cfg1"]
+        pairs = engine.keys_to_pairs(keys.cpu().numpy())
+        checks["edges_sha256"] = _sha(pairs) == rec["pairs_sha256"]
+        checks["counts"] = (list(info.get("raw") or []) == rec["per_replicate_raw"])
+        res["kind"] = "full edge-set digest"
+    elif config == "cfg2":
+        rec = _fixture("cfg2")
+        pairs = engine.keys_to_pairs(keys.cpu().numpy())
+        checks["pairs_sha256"] = _sha(pairs) == rec["pairs_sha256"]
+        res["kind"] = "full pair-set digest (10.5M words)"
+    elif config == "cfg3":
+        rec = _fixture("cfg3")
+        pairs = engine.keys_to_pairs(keys.cpu().numpy())
+        checks["edges_sha256"] = _edges_core_sha(pairs, rec) == rec["edges_core_sha256"]
+        checks["raw_new"] = (list(info.get("raw") or []) == rec["per_replicate_raw"] and
+                             list(info.get("new") or []) == rec["per_replicate_new"])
+        if last.get("candidates") is not None:
+            cand = engine.keys_to_pairs(last["candidates"].cpu().numpy())
+            checks["candidates_sha256"] = _sha(cand) == rec["candidates_sha256"]
+        if last.get("codes") is not None:
+            c = last["codes"]
+            checks["codes_sha256"] = all(
+                _sha(c[h].cpu().numpy()) == rec["codes_sha256"][h] for h in range(c.shape[0]))
+        res["kind"] = "full digests: edges, candidate union, codes, raw/new counts"
+    elif config in ("cfg4", "cfg5") and labels is not None:
+        from paper_0904_3151_b200 import workloads
+        rec = _fixture("cfg4_full" if config == "cfg4" else "cfg5_full")
+        subs = ["subset_mid"] if config == "cfg4" else ["subset", "subset_wide"]
+        for key in subs:
+            sub = rec[key]
+            cl = sub.get("clusters") or workloads.largest_clusters(labels, sub["clusters_top"])
+            S = workloads.restricted_subset(labels, cl, sub["extra"], sub["seed"])
+            pairs = engine.keys_to_pairs(_restrict(keys, S, n).cpu().numpy())
+            checks[f"{key}_edges_sha256"] = _edges_core_sha(pairs, sub) == sub["edges_core_sha256"]
+            if last.get("candidates") is not None:
+                cand = engine.keys_to_pairs(_restrict(last["candidates"], S, n).cpu().numpy())
+                checks[f"{key}_candidates_sha256"] = _sha(cand) == sub["candidates_sha256"]
+        res["kind"] = ("SURVEY 8(c) restriction of the full-scale build to seeded subsets "
+                       "(whole clusters + 20k random rows) vs the reference on pool[S]")
+    else:
+        return None
+    res["checks"] = checks
+    res["match"] = all(checks.values())
+    return res
 
 
 # ------------------------------------------------------------------ clocks
@@ -188,44 +265,63 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference
+CPU_SAMPLE_ROWS = {"cfg1": 20_000, "cfg2": 10_500_000, "cfg3": 1_600_000, "cfg4": 400_000,
+                   "cfg5": 500_000}
+
+
 def run_reference(args, rank, world):
+    """The reference algorithm on the host cores (the C restatement in
+    oracle/, pinned to the reference's own outputs at these shapes): for
+    configs 1-3 the FULL workload of our arm (same n, same params); configs
+    4-5 on the CPU-feasible samples SURVEY 8(d) names.  The oracle has no
+    JIT, so warm-up runs on a 1% sample; the timed steps stop once ~120 s
+    of CPU time is spent (at least one full step), and the line says how
+    many ran."""
     if rank != 0:
         return
     from oracle import oracle
     oracle.build()
     cfg = CONFIGS[args.config]
-    rows = args.cpu_sample_rows
+    rows = args.cpu_sample_rows or CPU_SAMPLE_ROWS[args.config]
     x = sample_inputs(args.config, rows)
     cores = os.cpu_count() or 1
     n = x.shape[0]
 
-    def step():
+    def step(xx):
         if cfg.metric == "hamming":
-            oracle.enumerate_pairs(x, 64, oracle.block_partition(64, cfg.blocks), cfg.mismatch,
+            oracle.enumerate_pairs(xx, 64, oracle.block_partition(64, cfg.blocks), cfg.mismatch,
                                    threads=cores)
         else:
             eps = cfg.epsilon if cfg.metric == "cosine" else cfg.epsilon ** 2 / 2.0
-            oracle.build_graph(x, eps, cfg.length, cfg.mismatch, cfg.blocks, cfg.replicates,
+            oracle.build_graph(xx, eps, cfg.length, cfg.mismatch, cfg.blocks, cfg.replicates,
                                cfg.seed, threads=cores)
 
+    xw = x[: max(2, n // 100)]
     for _ in range(args.warmup):
-        step()
+        step(xw)
     times = []
+    budget = float(os.environ.get("EG_REFERENCE_BUDGET_S", "120"))
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        step()
+        step(x)
         times.append(time.perf_counter() - t0)
+        if sum(times) > budget:
+            break
     sec = sum(times) / len(times)
     value = n / sec
-    sample = (f"{args.config} generator at n={n} rows (full params), C oracle port "
-              f"(reference algorithm, oracle/), {cores} threads; points/s of that sample")
     full_n = make_inputs_rows(args.config)
+    same = n == full_n
+    sample = (f"{args.config} generator at n={n} rows ({'the full workload' if same else 'sample'}"
+              f", full params), C oracle port of the reference algorithm (oracle/, pinned to "
+              f"the reference's outputs), {cores} threads; {len(times)} timed step(s)")
     cfgb = config_block(args, cfg, full_n, world)
     cfgb["parallelism"] = f"CPU oracle, {cores} threads (rank 0 only)"
     cfgb["cpu_sample_rows"] = n
+    cfgb["same_config"] = same
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": cfgb,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
@@ -256,7 +352,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
-    ap.add_argument("--cpu-sample-rows", type=int, default=400_000)
+    ap.add_argument("--cpu-sample-rows", type=int, default=0,
+                    help="rows of the CPU-baseline sample (default: per config, CPU_SAMPLE_ROWS)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-quality", action="store_true",
@@ -285,7 +382,7 @@ def main():
         tdist.init_process_group("nccl", device_id=dev)
     cfg = CONFIGS[args.config]
     params = params_for(cfg, eg)
-    data = make_inputs(args.config)
+    data, labels = make_inputs(args.config)
     n = data.shape[0]
     hamming = cfg.metric == "hamming"
     if hamming:
@@ -471,8 +568,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import oracle
         oracle.build()
-        rows = args.cpu_sample_rows
-        xs = sample_inputs(args.config, rows)
+        rows = args.cpu_sample_rows or CPU_SAMPLE_ROWS[args.config]
+        xs = data if rows == n else sample_inputs(args.config, rows)
         cores = os.cpu_count() or 1
         t0 = time.perf_counter()
         if hamming:
@@ -498,7 +595,7 @@ def main():
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
             "cpu_baseline": cpu, "stage_ms": stage_ms, "quality": quality,
             "counts": distributed.last_counts(last),
-            "parity": parity_vs_reference(args.config, distributed.last_counts(last)),
+            "parity": parity_vs_reference(args.config, last, labels, n),
         }
         print(json.dumps(out), flush=True)
     if world > 1:

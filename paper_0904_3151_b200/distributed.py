@@ -166,7 +166,8 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
     if world == 1 and not force_dist:
         from .pipeline import build_graph_device
         out = build_graph_device(x, params, metric=metric)
-        return {"keys": out["keys"], "dist": out["dist"], "info": out["info"]}
+        return {"keys": out["keys"], "dist": out["dist"], "info": out["info"],
+                "candidates": out["candidates"], "codes": out["codes"]}
     lo, hi, per = row_shard(n, world, rank)
     xs = x[lo:hi]
     if hasattr(ops, "project_rows"):
