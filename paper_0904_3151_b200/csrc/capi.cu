@@ -258,6 +258,7 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
       staged ? (size_t)MSM_TILE * 10 + (size_t)lay.B * 12 : (size_t)lay.B * 8;
   const size_t smem_group =
       sizeof(HGroupSmem<W, SmallCfg<W>::CAP, SmallCfg<W>::NT, SmallCfg<W>::MDIV>);
+
   const size_t smem_medium = sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>);
   a.gcnt_min = MediumCfg<W>::CAP;
   const size_t smem_tsort = (size_t)MSM_TILE * 8 + (size_t)lay.B * 4;

@@ -48,6 +48,12 @@ constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to thi
 constexpr uint32_t MSM_PAIR_SPLIT = EG_PAIR_SPLIT;  // small-tier buckets with more pairs -> medium
 
 constexpr int MSM_MAXT = 4;             // tail blocks of the O(1) canonical test
+#ifndef EG_TAIL_REGS
+#define EG_TAIL_REGS 0   // 1: tail masks in registers (measured slower: register pressure)
+#endif
+#ifndef EG_SMALL_GDIV
+#define EG_SMALL_GDIV 2  // small tier: at most CAP/4 groups per bucket (smem for 5 CTAs/SM)
+#endif
 
 struct UnitBatch {
   int count;
@@ -436,16 +442,38 @@ struct TailTest {
       sm[i] = wl < wh ? (wh - wl == 64 ? ~0ull : ((1ull << (wh - wl)) - 1ull)) << wl : 0ull;
     }
   }
+#if EG_TAIL_REGS
+  uint64_t r[MSM_MAXT * W];        // register copy of the tail masks
+  // after the barrier that follows load(): uniform registers for the pair loop
+  __device__ __forceinline__ void fetch() {
+#pragma unroll
+    for (int i = 0; i < MSM_MAXT * W; ++i) r[i] = m[i];
+  }
+#else
+  __device__ __forceinline__ void fetch() {}
+#endif
   __device__ __forceinline__ bool ok(const uint64_t (&x)[W], int pc, const uint8_t *b2b, int k,
                                      int d) const {
     if (nt > MSM_MAXT) return canonical_mask<W>(x, b2b, k, d) == maskbits;
     if (nt > pc) return false;       // every tail block needs a differing bit
+#if EG_TAIL_REGS
+#pragma unroll
+    for (int t = 0; t < MSM_MAXT; ++t) {
+      if (t < nt) {
+        uint64_t any = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) any |= x[w] & r[t * W + w];
+        if (!any) return false;
+      }
+    }
+#else
     for (int t = 0; t < nt; ++t) {
       uint64_t any = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) any |= x[w] & m[t * W + w];
       if (!any) return false;
     }
+#endif
     return true;
   }
 };
@@ -550,7 +578,8 @@ __device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia,
 // groups.
 template <int CAP, int MDIV>
 struct MemberCap {
-  static constexpr uint32_t M = CAP / MDIV, G = CAP / MDIV / 2;
+  static constexpr uint32_t M = CAP / MDIV,
+                            G = CAP / MDIV / 2 / (MDIV == EG_SMALL_MDIV && CAP < 4096 ? EG_SMALL_GDIV : 1);
 };
 
 template <int W, int CAP, int NT, int MDIV = 1>
@@ -843,6 +872,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   TailTest<W> tt;
   tt.load(ub, u, S.tmask);
   __syncthreads();
+  tt.fetch();
   uint32_t my_raw = 0, my_new = 0;
   // Each thread takes a contiguous range of the flattened pair index and
   // walks it incrementally (one group lookup + triangular decode per thread).
@@ -986,7 +1016,7 @@ template <int W>
 #define EG_SMALL_NT 256
 #endif
 #ifndef EG_SMALL_MINCTAS
-#define EG_SMALL_MINCTAS 4
+#define EG_SMALL_MINCTAS 5   // cfg3 group kernel 2.75 -> 2.60 ms (4 -> 5 CTAs/SM)
 #endif
 struct SmallCfg {               // one CTA per bucket, several CTAs per SM
   static constexpr int CAP = W <= 2 ? EG_SMALL_CAP : EG_SMALL_CAP / 2;
@@ -1232,6 +1262,7 @@ __global__ void __launch_bounds__(MSM_SPILL_T) k_msm_spill(const __grid_constant
         }
       }
       __syncthreads();
+      tt.fetch();
       const uint32_t i = threadIdx.x;
       uint32_t my_raw = 0, my_new = 0, my_eq = 0;
       uint32_t emask[MSM_SPILL_T / 32] = {};   // emitted partners j of this row

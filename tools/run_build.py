@@ -22,7 +22,7 @@ ap.add_argument("--reps", type=int, default=2)
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 params = bench.params_for(cfg, eg)
-data = bench.make_inputs(args.config)
+data, _ = bench.make_inputs(args.config)
 dev = torch.device("cuda", 0)
 if cfg.metric == "hamming":
     import numpy as np
