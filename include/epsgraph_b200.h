@@ -47,6 +47,17 @@ extern "C" {
 #define EG_MAX_REPLICATES 65535
 
 const char *eg_last_error(void);
+
+/* Path overrides for tests and tuning (the product never reads the       */
+/* environment).  Names: "project_path" (0 auto, 1 SIMT, 2 kind::tf32,    */
+/* 3 unfused norms, 4 non-TMA tensor-core kernel), "fixup_force_seq",     */
+/* "fixup_cap" (> 0 caps the band-entry list: overflow path),            */
+/* "msm_blocks" (> 0 forces the block count, -1 keeps the reference's),   */
+/* "msm_streams" (1 or 2), "verify_wide", "sort_path" (-1 auto, 0         */
+/* onesweep, 1 classic).  EG_ERR_ARG for an unknown name or value.        */
+/* Process-wide; not synchronised with calls in flight.                   */
+int eg_set_option(const char *name, long long value);
+void eg_reset_options(void);
 int eg_version(void);
 /* Number of SMs of the current device (for host-side sizing). */
 int eg_device_sm_count(void);

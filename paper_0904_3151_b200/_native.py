@@ -55,6 +55,8 @@ def _declare(lib):
     I = ctypes.c_int
     sig = {
         "eg_last_error": ([], ctypes.c_char_p),
+        "eg_set_option": ([ctypes.c_char_p, ctypes.c_longlong], I),
+        "eg_reset_options": ([], None),
         "eg_version": ([], I),
         "eg_device_sm_count": ([], I),
         "eg_launch_count": ([], ctypes.c_longlong),
@@ -148,6 +150,24 @@ class Profile:
             if cnt[c]:
                 out[self.lib.eg_profile_class_name(c).decode()] = {"ms": ms[c], "count": int(cnt[c])}
         return out
+
+
+class options:
+    """Context manager for the library's path overrides (eg_set_option):
+    ``with options(project_path=1): ...`` -- tests use it to reach the
+    alternative kernels; the defaults are restored on exit."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            check(lib().eg_set_option(k.encode(), int(v)), f"option {k}")
+        return self
+
+    def __exit__(self, *exc):
+        lib().eg_reset_options()
+        return False
 
 
 def launch_count() -> int:

@@ -100,7 +100,10 @@ static int num_sms() {
   return cached[dev];
 }
 
-static int env_int(const char *name, int dflt);
+Options &options() {
+  static Options o;
+  return o;
+}
 
 // Dynamic shared-memory opt-in.  The attribute lives in the device context,
 // so the record of what was already set is kept per (device, kernel): a
@@ -137,7 +140,7 @@ static double projection_tau(int dim) {
 static unsigned long long fixup_cap(int64_t n, int cols) {
   unsigned long long c = (unsigned long long)n * cols / 32;
   c = c < (1ull << 20) ? (1ull << 20) : c;
-  const int forced = env_int("EG_FIXUP_CAP", 0);   // tests: force the overflow path
+  const long long forced = options().fixup_cap;   // tests: force the overflow path
   return forced > 0 && (unsigned long long)forced < c ? (unsigned long long)forced : c;
 }
 
@@ -167,10 +170,6 @@ static void dispatch_project(int tn, const TX *x, int64_t n, int dim, const floa
 }
 
 // ------------------------------------------------------------------ MSM
-static int env_int(const char *name, int dflt) {
-  const char *v = getenv(name);
-  return (v && *v) ? atoi(v) : dflt;
-}
 
 // Small pinned host staging area per device (results read after a sync the
 // call performs anyway, so the copy does not add a synchronisation).
@@ -186,12 +185,11 @@ static unsigned long long *pinned_small() {
 }
 
 static int msm_buckets(int64_t n) {
-  // mean bucket size: the tuned target, but never above EG_MSM_FILL (default
-  // 80%) of the small tier's capacity.  Buckets are hash-balanced (Poisson,
-  // sd = sqrt(mean)), so the few that overflow go to the medium tier.
-  const double fill = env_int("EG_MSM_FILL", 80) / 100.0;
-  const int64_t cap_mean = (int64_t)(fill * SmallCfg<1>::CAP);
-  const int64_t tgt = std::min<int64_t>(env_int("EG_MSM_TARGET", MSM_TARGET), cap_mean);
+  // mean bucket size: the tuned target, but never above 80% of the small
+  // tier's capacity.  Buckets are hash-balanced (Poisson, sd = sqrt(mean)),
+  // so the few that overflow go to the medium tier.
+  const int64_t cap_mean = (int64_t)(0.8 * SmallCfg<1>::CAP);
+  const int64_t tgt = std::min<int64_t>(MSM_TARGET, cap_mean);
   int64_t b = (n + tgt - 1) / tgt;
   if (b < 1) b = 1;
   return (int)std::min<int64_t>(b, (int64_t)1 << MSM_MAX_LGB);
@@ -202,12 +200,11 @@ static int msm_batch_units(int64_t n) {
   int64_t per = n * 12;
   int64_t u = per > 0 ? (int64_t)(2ll << 30) / per : MSM_MAXU;
   if (u < 1) u = 1;
-  const int cap = std::max(1, std::min(MSM_MAXU, env_int("EG_MSM_UNITS", MSM_MAXU)));
-  return (int)(u > cap ? cap : u);
+  return (int)(u > MSM_MAXU ? MSM_MAXU : u);
 }
 
 struct MsmLayout {
-  int lgB, B, U, sets, tiled, ntiles;
+  int lgB, B, U, sets;
   size_t bytes;
 };
 
@@ -217,11 +214,7 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   l.lgB = ilog2_ceil((uint64_t)l.B);
   l.U = msm_batch_units(n);
   // two scratch sets: batch i+1's hist/scatter overlap batch i's grouping
-  l.sets = env_int("EG_MSM_STREAMS", 2) >= 2 ? 2 : 1;
-  // tile-local partition when every tile holds >= 4 rows per bucket and the
-  // group kernel can stage the per-tile segment table
-  l.ntiles = (int)((n + MSM_TILE - 1) / MSM_TILE);
-  l.tiled = env_int("EG_MSM_TILED", 0) && l.B * 4 <= MSM_TILE && l.ntiles <= 2048;
+  l.sets = options().msm_streams >= 2 ? 2 : 1;
   size_t b = 0;
   b += ws_bytes((size_t)l.U * l.B, 4);            // counts
   b += ws_bytes((size_t)l.U * (l.B + 1), 4);      // starts
@@ -232,11 +225,6 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   b += ws_bytes(3 + 2 * (size_t)reps, 8);         // counters
   b += ws_bytes((size_t)l.U * (l.B + 1) * 9, 4);  // spill list (<= 3 entries/bucket)
   b += ws_bytes(1, 8);                            // spill counter
-  if (l.tiled) {
-    b += ws_bytes((size_t)l.U * (l.B + 1) * l.ntiles, 2);   // tile bucket offsets
-    b += ws_bytes((size_t)l.U * n, 8);                      // spilled bucket copies
-    b += ws_bytes(1, 8);
-  }
   l.bytes = (b + 4096) * l.sets;
   return l;
 }
@@ -261,8 +249,6 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
 
   const size_t smem_medium = sizeof(HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>);
   a.gcnt_min = MediumCfg<W>::CAP;
-  const size_t smem_tsort = (size_t)MSM_TILE * 8 + (size_t)lay.B * 4;
-  if (lay.tiled) EG_SMEM_OPTIN(k_msm_tsort<W>, smem_tsort);
   EG_SMEM_OPTIN(k_msm_hist<W>, smem_hist);
   EG_SMEM_OPTIN(k_msm_scatter<W>, smem_scatter);
   EG_SMEM_OPTIN(k_msm_group<W>, smem_group);
@@ -308,22 +294,17 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     x.gcnt_min = a.gcnt_min;
     if (two && bi >= 2) EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_done[dev][si], 0));
     dim3 g1(tiles, ub.count);
-    if (lay.tiled) {
+    {
+      EG_PROF(PC_MSM_HIST, st);
+      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(x, ub);
+    }
+    {
+      EG_PROF(PC_MSM_SCAN, st);
+      k_msm_scan<<<ub.count, 1024, 0, st>>>(x);
+    }
+    {
       EG_PROF(PC_MSM_SCATTER, st);
-      k_msm_tsort<W><<<g1, MSM_SC_NT, smem_tsort, st>>>(x, ub);
-    } else {
-      {
-        EG_PROF(PC_MSM_HIST, st);
-        k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(x, ub);
-      }
-      {
-        EG_PROF(PC_MSM_SCAN, st);
-        k_msm_scan<<<ub.count, 1024, 0, st>>>(x);
-      }
-      {
-        EG_PROF(PC_MSM_SCATTER, st);
-        k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(x, ub);
-      }
+      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(x, ub);
     }
     if (two) {
       EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][si], st));
@@ -369,6 +350,22 @@ using namespace eg;
 extern "C" {
 
 const char *eg_last_error(void) { return g_err; }
+
+int eg_set_option(const char *name, long long value) {
+  if (!name) return arg_error("eg_set_option: null name");
+  Options &o = options();
+  if (!strcmp(name, "project_path") && value >= 0 && value <= 4) o.project_path = (int)value;
+  else if (!strcmp(name, "fixup_force_seq")) o.fixup_force_seq = value != 0;
+  else if (!strcmp(name, "fixup_cap") && value >= 0) o.fixup_cap = value;
+  else if (!strcmp(name, "msm_blocks") && value >= -1 && value <= EG_MAX_BLOCKS) o.msm_blocks = (int)value;
+  else if (!strcmp(name, "msm_streams") && (value == 1 || value == 2)) o.msm_streams = (int)value;
+  else if (!strcmp(name, "verify_wide")) o.verify_wide = value != 0;
+  else if (!strcmp(name, "sort_path") && value >= -1 && value <= 1) o.sort_path = (int)value;
+  else return arg_error("eg_set_option: unknown option or value out of range");
+  return EG_OK;
+}
+
+void eg_reset_options(void) { options() = Options(); }
 
 long long eg_launch_count(void) { return g_launches.load(); }
 
@@ -527,17 +524,12 @@ static int run_band_fixup(const void *d_x, int32_t dim, const double *d_r, int64
     k_collect_bits<<<(unsigned)std::min<int64_t>((words + per - 1) / per,
                                                  (int64_t)num_sms() * 8),
                      COLLECT_NT, 0, st>>>(unc, n, W, length, replicates, items, cnt, cap);
-    if (env_int("EG_FIXUP_LIST", 0)) {   // thread-per-entry variant (comparison)
-      const size_t fxs = fixl_smem(cols);
-      EG_SMEM_OPTIN(k_fixup_list, fxs);
-      k_fixup_list<<<(unsigned)num_sms() * 4, FIXL_NT, fxs, st>>>(
-          (const float *)d_x, dim, d_r, cols, n, length, W, d_codes, items, cnt, cap);
-    } else {
+    {
       const size_t fws = (size_t)(FIXW_NT / 32) * dim * 8;
       EG_SMEM_OPTIN(k_fixup_warp, fws);
       k_fixup_warp<<<(unsigned)num_sms() * 8, FIXW_NT, fws, st>>>(
           (const float *)d_x, dim, d_r, n, length, W, d_codes, items, cnt, cap,
-          env_int("EG_FIXUP_FORCE_SEQ", 0));
+          options().fixup_force_seq);
     }
     const size_t fsm = (size_t)8 * dim * 8;   // 8 warps x dim doubles
     EG_SMEM_OPTIN(k_fixup_bits, fsm);
@@ -581,12 +573,12 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
   EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
   FixupList fl{cnt, items, cap};
   const int npad = (cols + 15) / 16 * 16;
-  const bool use_tc = !x_is_f64 && dim % 4 == 0 && npad <= TC_MAXN &&
-                      !env_int("EG_PROJECT_SIMT", 0);
+  const int path = options().project_path;
+  const bool use_tc = !x_is_f64 && dim % 4 == 0 && npad <= TC_MAXN && path != 1;
   CUtensorMap xmap;
-  const bool tma_ok = use_tc && !env_int("EG_PROJECT_TC1", 0) &&
+  const bool tma_ok = use_tc && path != 4 &&
                       make_x_tensor_map(&xmap, d_x, n, dim);
-  const bool fuse = d_bad && tma_ok && !env_int("EG_PROJECT_UNFUSED", 0);
+  const bool fuse = d_bad && tma_ok && path != 3;
   if (d_bad && !fuse) {   // norms first, then the projection reads them
     int rc = eg_row_stats(d_x, x_is_f64, n, dim, d_norms, d_bad, st);
     if (rc) return rc;
@@ -606,9 +598,9 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
     EG_LAUNCH_CHECK();
     const int64_t ntiles = (n + TC_M - 1) / TC_M;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
-    const int h16_no = std::max(2, std::min(H16_MAXSLOTS, env_int("EG_H16_OSLOTS", 2)));
-    const int h16_npad = std::max(npad, std::min(TC_MAXN, env_int("EG_H16_NPAD", 0)) / 16 * 16);
-    const bool h16 = tma_ok && !env_int("EG_PROJECT_TF32", 0) && h16_fits(h16_npad, h16_no);
+    const int h16_no = 2;
+    const int h16_npad = npad;
+    const bool h16 = tma_ok && path != 2 && h16_fits(h16_npad, h16_no);
     if (h16) {
       // kind::f16 (2-term fp16 splits): the production path for fp32 rows
       double *colscale = ar.take<double>(TC_MAXN);
@@ -626,8 +618,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
       const size_t ob = h16_oslot_bytes(h16_npad);
       const int no = h16_no;
       const size_t budget = ((size_t)220 << 10) - sizeof(H16Bars) - 1024;
-      const int nx = (int)std::min<size_t>(env_int("EG_H16_XSLOTS", H16_MAXSLOTS),
-                                           (budget - no * ob) / H16_XSLOT);
+      const int nx = (int)std::min<size_t>(H16_MAXSLOTS, (budget - no * ob) / H16_XSLOT);
       if (nx < 2) return arg_error("eg_project: too many direction columns for the f16 path");
       const size_t smem = nx * H16_XSLOT + no * ob + sizeof(H16Bars) + 1024;
       EG_SMEM_OPTIN(k_project_h16, smem);
@@ -636,7 +627,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
         k_project_h16<<<grid, H16_THREADS, smem, st>>>(
             xmap, n, dim, himg, colscale, cols, h16_npad, nx, no, d_norms, d_rnorm, h16_tau(dim),
             length, W, d_codes, unc, g_tc_debug, fuse ? d_norms : nullptr,
-            fuse ? (unsigned long long *)d_bad : nullptr, env_int("EG_TC_EXP", 0));
+            fuse ? (unsigned long long *)d_bad : nullptr);
       }
       EG_LAUNCH_CHECK();
       return run_band_fixup(d_x, dim, d_r, n, length, W, replicates, cols, d_codes, unc, items,
@@ -644,7 +635,7 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
     }
     if (tma_ok) {
       const size_t sbytes = tc2_stage_bytes(npad);
-      const int nstages = (int)std::min<size_t>(env_int("EG_TC2_STAGES", 4), ((size_t)212 << 10) / sbytes);
+      const int nstages = (int)std::min<size_t>(4, ((size_t)212 << 10) / sbytes);
       const size_t smem = nstages * sbytes + sizeof(Tc2Bars) + 1024;
       EG_SMEM_OPTIN(k_project_tc2, smem);
       uint64_t *unc = ar.take<uint64_t>((size_t)replicates * n * W);
@@ -657,7 +648,6 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
         k_project_tc2<<<grid, TC2_THREADS, smem, st>>>(xmap, n, dim, img, cols, npad, nstages,
                                                        d_norms, d_rnorm, tc_tau(dim), length, W,
                                                        d_codes, unc, g_tc_debug,
-                                                       env_int("EG_TC_EXP", 0),
                                                        fuse ? d_norms : nullptr,
                                                        fuse ? (unsigned long long *)d_bad
                                                             : nullptr);
@@ -735,10 +725,6 @@ static void plan_kept(int length, int kk, uint64_t dropped_blocks, uint64_t kept
   }
 }
 
-static double env_double(const char *name, double dflt) {
-  const char *v = getenv(name);
-  return (v && *v) ? atof(v) : dflt;
-}
 
 constexpr int PLAN_REF_MAX = 4096;     // reference masks probed for the oversize check
 constexpr int PLAN_PER_K = 12;         // masks probed per candidate block count
@@ -762,7 +748,7 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   *h_k_out = k;
   if (h_cost) h_cost[0] = h_cost[1] = 0;
   const int kmax = std::min(length, EG_MAX_BLOCKS);
-  const int forced = env_int("EG_MSM_BLOCKS", 0);
+  const int forced = options().msm_blocks;
   if (forced > 0) {
     if (forced > d && forced <= kmax) *h_k_out = forced;
     return EG_OK;
@@ -880,8 +866,8 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   } else if (oversized_fraction * SR < 200 || rmax >= 0.5 * oversized_fraction * SR) {
     return EG_OK;
   }
-  const double ce = env_double("EG_PLAN_CE_PS", 18.5) * 1e-12;   // per row per unit
-  const double cp = env_double("EG_PLAN_CP_PS", 3.0) * 1e-12;    // per visited pair
+  const double ce = 18.5e-12;   // s per row per unit (measured, cfg3)
+  const double cp = 3.0e-12;    // s per visited in-group pair
   const double scale = S > 1 ? (double)n * (double)(n - 1) / ((double)S * (double)(S - 1)) : 0;
   double best = -1, ref_cost = -1;
   int best_k = k;
@@ -892,9 +878,6 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     for (; p < P && probe_k[p] == kk; ++p, ++cnt) sum += (double)pairs[p];
     const double est_pairs = sum / cnt * scale;
     const double cost = comb_sat(kk, d) * ((double)n * ce + est_pairs * cp);
-    if (env_int("EG_PLAN_DEBUG", 0))
-      fprintf(stderr, "eg_msm_plan: k'=%d units=%.0f est_pairs/mask=%.4g cost=%.3f ms\n", kk,
-              comb_sat(kk, d), est_pairs, cost * 1e3);
     if (kk == k) ref_cost = cost;
     if (best < 0 || cost < best) {
       best = cost;
@@ -977,18 +960,6 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
     x.gcnt = ar.take<uint32_t>((size_t)lay.U * n);
     x.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 9);
     x.spill_ctr = ar.take<unsigned long long>(1);
-    x.tiled = lay.tiled;
-    x.ntiles = lay.ntiles;
-    if (lay.tiled) {
-      x.toff = ar.take<uint16_t>((size_t)lay.U * (lay.B + 1) * lay.ntiles);
-      x.toff_ro = x.toff;
-      x.sel = ar.take<uint64_t>((size_t)lay.U * n);
-      x.sel_ctr = ar.take<unsigned long long>(1);
-      if (!x.toff || !x.sel || !x.sel_ctr) {
-        set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
-        return EG_ERR_WORKSPACE;
-      }
-    }
     if (!x.counts || !x.starts || !x.cursor || !x.elems || !x.gcnt || !x.spill || !x.spill_ctr) {
       set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
       return EG_ERR_WORKSPACE;
@@ -1005,8 +976,7 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   std::vector<UnitBatch> batches;
   int64_t nbatch = (n_units + lay.U - 1) / lay.U;
   if (lay.sets == 2 && n_units >= 4)
-    nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(env_int("EG_MSM_MINBATCHES", 2),
-                                                         n_units / 2));
+    nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(2, n_units / 2));
   const int64_t per_batch = nbatch > 0 ? (n_units + nbatch - 1) / nbatch : lay.U;
   for (int64_t u0 = 0; u0 < n_units; u0 += per_batch) {
     UnitBatch ub;
@@ -1250,7 +1220,7 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   {
   EG_PROF(PC_VERIFY, st);
   const int vu = (!x_is_f64 && dim % 4 == 0 && dim <= 128 * VER_VU) ? (dim + 127) / 128 : 0;
-  const bool narrow = !x_is_f64 && dim % 4 == 0 && dim <= 128 && !env_int("EG_VERIFY_WIDE", 0);
+  const bool narrow = !x_is_f64 && dim % 4 == 0 && dim <= 128 && !options().verify_wide;
   if (narrow) {
     // eight lanes per pair, four pairs per warp step (measured: 4 lanes per
     // pair is slower on configs 4 and 5)

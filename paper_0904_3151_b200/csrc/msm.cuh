@@ -85,13 +85,6 @@ struct MsmArgs {
   unsigned long long *ctr;       // [0] emitted, [1] max group, [2] unused,
                                  // [3..3+reps) raw, [3+reps..) new
   unsigned long long *spill_ctr; // [0] entries on this scratch set's spill list
-  // tile-local mode (k_msm_tsort): each tile's rows are bucket-sorted in
-  // place; toff[u][b][tile] = start of bucket b inside tile (b = 0..B)
-  int tiled, ntiles;
-  const uint16_t *toff_ro;
-  uint16_t *toff;
-  uint64_t *sel;                 // contiguous copies of spilled buckets
-  unsigned long long *sel_ctr;
   uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
   int64_t spill_cap;
   int gcnt_min;                  // spilled buckets above this size count groups
@@ -303,88 +296,6 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
     const uint32_t b = sbk[j];
     el[gbase[b] + (j - tstart[b])] = stage[j];
   }
-}
-
-// ------------------------------------------------------------- 1'-3'
-// Tile-local partition (replaces hist + scan + scatter when the tiles hold
-// several rows per bucket): each CTA hashes its 8192-row tile under one
-// unit's mask, sorts the tile by bucket in shared memory and writes it back
-// contiguously (fully coalesced), plus the tile's bucket offsets
-// toff[u][b][tile].  No global histogram, no global atomics.
-template <int W>
-__global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_tsort(const __grid_constant__ MsmArgs a,
-                                                            const __grid_constant__ UnitBatch ub) {
-  extern __shared__ __align__(16) unsigned char smts[];
-  const int u = blockIdx.y;
-  const int B = a.B;
-  uint64_t *stage = reinterpret_cast<uint64_t *>(smts);                    // [MSM_TILE]
-  uint32_t *hist = reinterpret_cast<uint32_t *>(stage + MSM_TILE);       // [B]
-  __shared__ uint32_t sw[MSM_SC_NT / 32];
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
-    a.spill_ctr[0] = 0;
-    a.sel_ctr[0] = 0;
-  }
-  for (int i = threadIdx.x; i < B; i += MSM_SC_NT) hist[i] = 0;
-  __syncthreads();
-  const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
-  const unsigned long long *kept = ub.kept[u];
-  const uint64_t salt = ub.salt[u];
-  const int64_t base = (int64_t)blockIdx.x * MSM_TILE;
-  constexpr int IPT = MSM_TILE / MSM_SC_NT;
-  uint32_t br[IPT], h2[IPT];
-  {
-    // all code loads first (the smem atomics below would otherwise
-    // serialise one load latency per item)
-    uint64_t c[IPT][W];
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
-      if (row < a.n) load_code<W>(codes, row, c[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
-      if (row < a.n) {
-        const uint64_t h = hash_key<W>(c[i], (const uint64_t *)kept, salt);
-        const uint32_t b = bucket_of(h, B);
-        h2[i] = (uint32_t)h;
-        br[i] = (b << 13) | atomicAdd(&hist[b], 1u);
-      }
-    }
-  }
-  __syncthreads();
-  {  // tile-local bucket starts; published as toff[u][b][tile]
-    const int per = (B + MSM_SC_NT - 1) / MSM_SC_NT;
-    uint32_t loc = 0;
-    for (int q = 0; q < per; ++q) {
-      const int b = threadIdx.x * per + q;
-      if (b < B) loc += hist[b];
-    }
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan<MSM_SC_NT>(loc, tot, sw);
-    uint16_t *to = a.toff + (int64_t)u * (B + 1) * a.ntiles + blockIdx.x;
-    for (int q = 0; q < per; ++q) {
-      const int b = threadIdx.x * per + q;
-      if (b < B) {
-        const uint32_t c = hist[b];
-        hist[b] = run;
-        to[(int64_t)b * a.ntiles] = (uint16_t)run;
-        run += c;
-      }
-    }
-    if (threadIdx.x == 0) to[(int64_t)B * a.ntiles] = (uint16_t)tot;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const int64_t row = base + (int64_t)i * MSM_SC_NT + threadIdx.x;
-    if (row < a.n)
-      stage[hist[br[i] >> 13] + (br[i] & 0x1fffu)] = ((uint64_t)h2[i] << 32) | (uint64_t)row;
-  }
-  __syncthreads();
-  uint64_t *el = a.elems + (int64_t)u * a.n + base;
-  const int valid = (int)min((int64_t)MSM_TILE, a.n - base);
-  for (int j = threadIdx.x; j < valid; j += MSM_SC_NT) el[j] = stage[j];
 }
 
 // ------------------------------------------------------- pair predicate
@@ -642,7 +553,6 @@ template <int W, int CAP, int NT, int MDIV>
 __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
                                                const MsmArgs &a, const UnitBatch &ub, int u,
                                                const uint64_t *el, uint32_t s,
-                                               bool el_in_smem,
                                                uint32_t pair_limit = 0xffffffffu) {
   constexpr int PT = CAP / NT;
   constexpr uint32_t MCAP = HGroupSmem<W, CAP, NT, MDIV>::MCAP;
@@ -656,7 +566,6 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     const uint32_t i = threadIdx.x + j * NT;
     e[j] = i < s ? el[i] : 0ull;
   }
-  if (el_in_smem) __syncthreads();   // the stage overlays the table
 #if EG_GROUP_FILTER
   // 2. atomic-free singleton filter: every row writes its local index into
   //    a slot chosen by the high bits of h2 (plain stores, last writer
@@ -991,13 +900,12 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   return true;
 }
 
-// Rows of a spill-list entry: a contiguous bucket of elems[u] (classic
-// mode) or a contiguous copy in sel (tile-local mode).
+// Rows of a spill-list entry: a contiguous bucket of elems[u].
 __device__ __forceinline__ const uint64_t *spill_elems(const MsmArgs &a, int u, uint32_t s0) {
-  return a.tiled ? a.sel + s0 : a.elems + (int64_t)u * a.n + s0;
+  return a.elems + (int64_t)u * a.n + s0;
 }
 __device__ __forceinline__ uint32_t *spill_gcnt(const MsmArgs &a, int u, uint32_t s0) {
-  return a.tiled ? a.gcnt + s0 : a.gcnt + (int64_t)u * a.n + s0;
+  return a.gcnt + (int64_t)u * a.n + s0;
 }
 
 // Spill-list routing.  Tag bit 31: re-queued by the small tier (member room
@@ -1042,77 +950,10 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
   const int u = blockIdx.y;
   const int b = blockIdx.x;
   const int B = a.B;
-  uint32_t s0 = 0, s = 0;
-  const uint64_t *src = nullptr;
-  bool in_smem = false;
-  if (!a.tiled) {
-    const uint32_t *st = a.starts + (int64_t)u * (B + 1);
-    s0 = st[b];
-    s = st[b + 1] - s0;
-    src = a.elems + (int64_t)u * a.n + s0;
-  } else {
-    // gather the bucket's segment from every tile (tile-local mode)
-    const int nt = a.ntiles;
-    const uint16_t *tb = a.toff_ro + ((int64_t)u * (B + 1) + b) * nt;
-    const uint16_t *te = tb + nt;
-    uint32_t *segstart = reinterpret_cast<uint32_t *>(S.big + CAP * 8);   // after the stage
-    uint16_t *seglo = reinterpret_cast<uint16_t *>(segstart + nt + 1);
-    constexpr int SP = 8;   // tiles per thread (nt <= SP * NT)
-    uint32_t lens[SP];
-    uint32_t loc = 0;
-#pragma unroll
-    for (int q = 0; q < SP; ++q) {
-      const int t = threadIdx.x * SP + q;
-      lens[q] = 0;
-      if (t < nt) {
-        const uint16_t lo = tb[t];
-        lens[q] = (uint32_t)te[t] - lo;
-        seglo[t] = lo;
-        loc += lens[q];
-      }
-    }
-    unsigned long long tot64;
-    unsigned long long run = block_exclusive_scan64<NT>(loc, tot64, S.sw);
-#pragma unroll
-    for (int q = 0; q < SP; ++q) {
-      const int t = threadIdx.x * SP + q;
-      if (t < nt) segstart[t] = (uint32_t)run;
-      run += lens[q];
-    }
-    s = (uint32_t)tot64;
-    if (s < 2) return;
-    __syncthreads();
-    uint64_t *dst;
-    if (s > CAP) {   // spilled: contiguous copy for the tier kernels
-      if (threadIdx.x == 0) S.ncand = (uint32_t)atomicAdd(a.sel_ctr, (unsigned long long)s);
-      __syncthreads();
-      s0 = S.ncand;
-      dst = a.sel + s0;
-    } else {
-      dst = reinterpret_cast<uint64_t *>(S.big);
-      in_smem = true;
-    }
-    const uint64_t *elu = a.elems + (int64_t)u * a.n;
-    if (threadIdx.x == 0) segstart[nt] = s;
-    __syncthreads();
-    // gather: thread per tile segment (~MSM_TILE/B contiguous rows each);
-    // the unrolled loads of a segment are independent and issued together
-    for (int t = threadIdx.x; t < nt; t += NT) {
-      const uint32_t o = segstart[t], len = segstart[t + 1] - o;
-      const uint64_t *sp = elu + (int64_t)t * MSM_TILE + seglo[t];
-      uint32_t k = 0;
-      for (; k + 8 <= len; k += 8) {
-        uint64_t v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = sp[k + q];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) dst[o + k + q] = v[q];
-      }
-      for (; k < len; ++k) dst[o + k] = sp[k];
-    }
-    __syncthreads();
-    src = dst;
-  }
+  const uint32_t *st = a.starts + (int64_t)u * (B + 1);
+  const uint32_t s0 = st[b];
+  const uint32_t s = st[b + 1] - s0;
+  const uint64_t *src = a.elems + (int64_t)u * a.n + s0;
   if (s < 2) return;
   if (s > CAP) {
     if (threadIdx.x == 0) {
@@ -1130,30 +971,12 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
     return;
   }
   for (int i = threadIdx.x; i < a.L; i += NT) S.b2b[i] = a.bit2blk[i];
-  const bool ok = process_bucket(S, a, ub, u, src, s, in_smem, MSM_PAIR_SPLIT);
+  const bool ok = process_bucket(S, a, ub, u, src, s, MSM_PAIR_SPLIT);
   if (!ok) {
     // grouped rows exceed the member capacity, or the groups hold more than
     // MSM_PAIR_SPLIT pairs: hand the bucket to the medium tier (any size up
     // to its own capacity; 512 threads per bucket, off the small tier's
     // critical path)
-    if (a.tiled) {   // the smem stage is gone: re-gather into sel
-      if (threadIdx.x == 0) S.ncand = (uint32_t)atomicAdd(a.sel_ctr, (unsigned long long)s);
-      __syncthreads();
-      s0 = S.ncand;
-      const int nt = a.ntiles;
-      const uint16_t *tb = a.toff_ro + ((int64_t)u * (B + 1) + b) * nt;
-      const uint16_t *te = tb + nt;
-      const uint64_t *elu = a.elems + (int64_t)u * a.n;
-      // sequential re-gather (rare path): thread 0 walks the segments
-      if (threadIdx.x == 0) {
-        uint32_t o = s0;
-        for (int t = 0; t < nt; ++t) {
-          const uint16_t lo = tb[t], hi = te[t];
-          for (uint32_t i = lo; i < hi; ++i) a.sel[o++] = elu[(int64_t)t * MSM_TILE + i];
-        }
-      }
-      __syncthreads();
-    }
     if (threadIdx.x == 0) {
       const unsigned long long slot = atomicAdd(&a.spill_ctr[0], 1ull);
       if ((int64_t)slot < a.spill_cap) {
@@ -1184,7 +1007,7 @@ __global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
       continue;
     const int u = (int)(tag & 0x3fffffffu);
     const uint32_t s0 = a.spill[sb * 3 + 1];
-    if (!process_bucket(S, a, ub, u, spill_elems(a, u, s0), s, false)) {
+    if (!process_bucket(S, a, ub, u, spill_elems(a, u, s0), s)) {
       // still too many grouped rows: the tile kernel takes it
       if ((int64_t)s * 4 > a.n) {
         uint32_t *g = spill_gcnt(a, u, s0);

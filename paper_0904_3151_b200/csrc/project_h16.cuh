@@ -150,9 +150,7 @@ __global__ void __launch_bounds__(H16_THREADS, 1) k_project_h16(
     const double *__restrict__ colscale, int cols, int npad, int nx, int no,
     const double *__restrict__ xnorm, const double *__restrict__ rnorm, double tau, int L, int W,
     uint64_t *__restrict__ codes, uint64_t *__restrict__ unc_bits, float *__restrict__ dbg,
-    double *__restrict__ norms_out, unsigned long long *__restrict__ bad, int exp_flags) {
-  // exp_flags (timing experiments only; codes are wrong when set):
-  // 1 = no epilogue work, 4 = no MMAs, 16 = directions loaded once
+    double *__restrict__ norms_out, unsigned long long *__restrict__ bad) {
   const bool fuse = norms_out != nullptr;
   extern __shared__ __align__(1024) unsigned char h16_smem_raw[];
   unsigned char *smem = h16_smem_raw + ((1024u - (smem_u32(h16_smem_raw) & 1023u)) & 1023u);
@@ -227,10 +225,6 @@ __global__ void __launch_bounds__(H16_THREADS, 1) k_project_h16(
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int kc = 0; kc < nkc; ++kc, p.next(no)) {
           mbar_wait(&B.ofree[p.s], p.ph ^ 1);
-          if ((exp_flags & 16) && (tile != blockIdx.x || kc >= no)) {
-            mbar_arrive(&B.rfull[p.s]);      // experiment: directions loaded once
-            continue;
-          }
           mbar_expect_tx(&B.rfull[p.s], rbytes);
           bulk_load(oring + p.s * ob, img + (int64_t)kc * 2 * npad * H16_BK, rbytes,
                     &B.rfull[p.s]);
@@ -255,7 +249,7 @@ __global__ void __launch_bounds__(H16_THREADS, 1) k_project_h16(
           const uint32_t a_h = acol + 64 * p.s, a_l = a_h + 32;
           const uint32_t b_h = smem_u32(oring + p.s * ob), b_l = b_h + npad * 128;
 #pragma unroll
-          for (int j = 0; j < ((exp_flags & 4) ? 0 : H16_BK / 16); ++j) {
+          for (int j = 0; j < H16_BK / 16; ++j) {
             const uint32_t o = j * 32;   // K=16 fp16 = 32 B along the 128 B row
             umma_f16_ts(dcol, a_h + 8 * j, umma_desc_sw128(b_h + o), idesc, (kc | j) ? 1u : 0u);
             umma_f16_ts(dcol, a_h + 8 * j, umma_desc_sw128(b_l + o), idesc, 1u);
@@ -358,7 +352,7 @@ __global__ void __launch_bounds__(H16_THREADS, 1) k_project_h16(
       // replicate / word boundaries into the row's code words
       uint64_t word = 0, uword = 0;
       int h = 0, tb = 0;                // (replicate, bit) of column c0
-      for (int c0 = 0; c0 < ((exp_flags & 1) ? 0 : cols); c0 += 32) {
+      for (int c0 = 0; c0 < cols; c0 += 32) {
         uint32_t accv[32];
         tmem_ld32(tmem + b * acc + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, accv);
         float ca[32], cb[32];

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
     const __grid_constant__ CUtensorMap xmap, int64_t n, int dim, const float *__restrict__ img,
     int cols, int npad, int nstages, const double *__restrict__ xnorm,
     const double *__restrict__ rnorm, double tau, int L, int W, uint64_t *__restrict__ codes,
-    uint64_t *__restrict__ unc_bits, float *__restrict__ dbg, int exp_flags,
+    uint64_t *__restrict__ unc_bits, float *__restrict__ dbg,
     double *__restrict__ norms_out, unsigned long long *__restrict__ bad) {
   // norms_out != nullptr: the converters also produce the fp64 row norms
   // (sequential fma over ascending q, as k_row_stats) and the bad-row flags,
@@ -426,11 +426,9 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
           const uint32_t use = it / nstages;
           mbar_wait(&B.empty[s], (use & 1) ^ 1);
           unsigned char *st = smem + s * sb;
-          const bool load_r = !(exp_flags & 4) || use == 0;
-          mbar_expect_tx(&B.full[s], xbytes + (load_r ? rbytes : 0));
+          mbar_expect_tx(&B.full[s], xbytes + rbytes);
           tma_load_2d(st, &xmap, kc * TC_BK, (int)(tile * TC_M), &B.full[s]);
-          if (load_r)
-            bulk_load(st + 2 * xbytes, img + (int64_t)kc * 2 * npad * TC_BK, rbytes, &B.full[s]);
+          bulk_load(st + 2 * xbytes, img + (int64_t)kc * 2 * npad * TC_BK, rbytes, &B.full[s]);
         }
       }
     }
@@ -481,10 +479,10 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
         float *xh = reinterpret_cast<float *>(smem + s * sb);
         float *xl = xh + TC_M * TC_BK;
 #pragma unroll
-        for (int cc = 0; cc < ((exp_flags & 2) ? 0 : 4); ++cc) {
+        for (int cc = 0; cc < 4; ++cc) {
           const uint32_t off = sw128_off(row, half * 4 + (uint32_t)cc) / 4;
           const float4 v = *reinterpret_cast<const float4 *>(xh + off);
-          if (fuse && !(exp_flags & 8)) {   // OOB columns are TMA zero-fill: fma(0, 0, s) == s
+          if (fuse) {   // OOB columns are TMA zero-fill: fma(0, 0, s) == s
             s0 = fma((double)v.x, (double)v.x, s0);
             s1 = fma((double)v.y, (double)v.y, s1);
             s2 = fma((double)v.z, (double)v.z, s2);
@@ -501,7 +499,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       if (fuse) {
         const uint32_t b = t & 1, buse = t >> 1;
         mbar_wait(&B.normempty[b], (buse & 1) ^ 1);
-        B.xss[b][half][row] = (exp_flags & 8) ? 0.5 : (s0 + s1) + (s2 + s3);
+        B.xss[b][half][row] = (s0 + s1) + (s2 + s3);
         mbar_arrive(&B.normfull[b]);
       }
     }
@@ -536,7 +534,7 @@ __global__ void __launch_bounds__(TC2_THREADS, 1) k_project_tc2(
       // become two 32-bit masks (one predicated OR per column); the masks
       // are then cut at replicate / word boundaries into the row's code
       // words (a word is stored, not OR-ed, when it completes).
-      const int ncols = (exp_flags & 1) ? 0 : cols;
+      const int ncols = cols;
       uint64_t word = 0, uword = 0;
       int h = 0, t = 0;                 // (replicate, bit) of column c0
       for (int c0 = 0; c0 < ncols; c0 += 32) {
@@ -645,62 +643,6 @@ __global__ void __launch_bounds__(COLLECT_NT) k_collect_bits(
   }
 }
 
-// Exact recompute of listed band entries, one thread per entry.  The
-// direction matrix is staged through shared memory in 32-wide q chunks
-// (shared by the CTA's 256 entries), each thread streams its own row with
-// 16-byte loads issued a whole chunk ahead, and adds the separately rounded
-// products in ascending q -- the reference's sequential fp64 sum
-// (lsh.py:107-112).  Positive sums set the code bit (atomicOr: two entries
-// may share a word).
-constexpr int FIXL_NT = 256, FIXL_QC = 32;
-__host__ __device__ inline size_t fixl_smem(int cols) { return (size_t)(FIXL_QC + 1) * cols * 8; }
-__global__ void __launch_bounds__(FIXL_NT) k_fixup_list(
-    const float *__restrict__ x, int dim, const double *__restrict__ r, int cols, int64_t n,
-    int L, int W, uint64_t *__restrict__ codes, const unsigned long long *__restrict__ items,
-    const unsigned long long *__restrict__ count, unsigned long long cap) {
-  extern __shared__ double rs[];                    // [cols][FIXL_QC + 1]
-  const unsigned long long total = min(*count, cap);
-  for (unsigned long long e0 = (unsigned long long)blockIdx.x * FIXL_NT; e0 < total;
-       e0 += (unsigned long long)gridDim.x * FIXL_NT) {
-    const unsigned long long ei = e0 + threadIdx.x;
-    const bool mine = ei < total;
-    const unsigned long long it = mine ? items[ei] : 0ull;
-    const int64_t row = (int64_t)(it >> 32);
-    const int c = (int)(it & 0xffffffffu);
-    const float4 *xr = reinterpret_cast<const float4 *>(x + row * dim);
-    double acc = 0.0;
-    for (int q0 = 0; q0 < dim; q0 += FIXL_QC) {
-      const int qn = min(FIXL_QC, dim - q0);        // multiple of 4
-      float4 xv[FIXL_QC / 4];
-#pragma unroll
-      for (int j = 0; j < FIXL_QC / 4; ++j)
-        xv[j] = (mine && 4 * j < qn) ? __ldg(xr + q0 / 4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
-      __syncthreads();                               // previous chunk consumed
-      for (int i = threadIdx.x; i < cols * FIXL_QC; i += FIXL_NT) {
-        const int cc = i / FIXL_QC, qq = i - cc * FIXL_QC;
-        rs[cc * (FIXL_QC + 1) + qq] = qq < qn ? __ldg(r + (int64_t)cc * dim + q0 + qq) : 0.0;
-      }
-      __syncthreads();
-      if (mine) {
-#pragma unroll
-        for (int j = 0; j < FIXL_QC / 4; ++j) {
-          if (4 * j >= qn) break;
-          const double *rq = rs + c * (FIXL_QC + 1) + 4 * j;
-          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].x, rq[0]));
-          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].y, rq[1]));
-          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].z, rq[2]));
-          acc = __dadd_rn(acc, __dmul_rn((double)xv[j].w, rq[3]));
-        }
-      }
-    }
-    if (mine && acc > 0.0) {
-      const int h = c / L, t = c - h * L;
-      atomicOr((unsigned long long *)&codes[((int64_t)h * n + row) * W + (t >> 6)],
-               1ull << (t & 63));
-    }
-  }
-}
-
 // Band entries, one warp per entry (the production fix-up).  The lanes form
 // the entry's separately rounded products x_q * r_q (__dmul_rn, as the
 // reference), add them in a fixed tree and also add S = sum |x_q r_q|.  The
@@ -774,7 +716,7 @@ __global__ void __launch_bounds__(FIXW_NT) k_fixup_warp(
 }
 
 // Exact recompute of the band entries flagged in the bitmap (same layout as
-// the codes) -- the overflow path of k_collect_bits/k_fixup_list (exits at
+// the codes) -- the overflow path of k_collect_bits/k_fixup_warp (exits at
 // once unless the list overflowed).  One warp per 32 rows: lanes compute the
 // separately rounded products of one entry in parallel (coalesced row
 // reads), lane 0 adds them in ascending q (lsh.py:107-112).

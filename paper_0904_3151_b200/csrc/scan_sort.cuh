@@ -457,11 +457,11 @@ __host__ inline int radix_sort_classic(uint64_t *keys, uint32_t *vals, int64_t m
 // Production sort: onesweep up to 32M keys (fewer launches: 0.47 -> 0.33 ms
 // for config 3's 2.5M candidate keys), the three-kernel upsweep / scan /
 // downsweep passes above that (higher occupancy, faster at 2e8-1.4e9 keys:
-// configs 4 and 5).  EG_SORT_CLASSIC=0/1 forces one of them (tests).
+// configs 4 and 5).  The sort_path option forces one of them (tests).
 __host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const int *shifts,
                                int npass, Arena &ar, cudaStream_t st) {
-  const char *e = getenv("EG_SORT_CLASSIC");
-  const bool classic = (e && *e) ? *e == '1' : m > (32ll << 20);
+  const int forced = options().sort_path;
+  const bool classic = forced >= 0 ? forced == 1 : m > (32ll << 20);
   if (classic || npass > OS_MAXPASS) return radix_sort_classic(keys, vals, m, shifts, npass, ar, st);
   return radix_sort_onesweep(keys, vals, m, shifts, npass, ar, st);
 }

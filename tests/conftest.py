@@ -28,6 +28,18 @@ def golden(name):
     return np.load(os.path.join(GOLDEN, f"{name}.npz"))
 
 
+@pytest.fixture
+def native_options():
+    """Set library path overrides (eg_set_option) for one test; reset after."""
+    from paper_0904_3151_b200 import _native
+
+    def set_options(**kw):
+        for k, v in kw.items():
+            _native.check(_native.lib().eg_set_option(k.encode(), int(v)), f"option {k}")
+    yield set_options
+    _native.lib().eg_reset_options()
+
+
 @pytest.fixture(scope="session")
 def oracle():
     from oracle import oracle as orc

@@ -201,12 +201,11 @@ def test_projection_vs_oracle_large(eg, oracle):
 
 
 @pytest.mark.parametrize("simt", ["0", "1"])
-def test_projection_fixup_overflow_path(eg, oracle, monkeypatch, simt):
+def test_projection_fixup_overflow_path(eg, oracle, native_options, simt):
     """A tiny band-list capacity forces the overflow recompute (bitmap path on
     the tensor cores, full recompute on the SIMT path): codes still exact."""
     from paper_0904_3151_b200 import workloads
-    monkeypatch.setenv("EG_FIXUP_CAP", "64")
-    monkeypatch.setenv("EG_PROJECT_SIMT", simt)
+    native_options(fixup_cap=64, project_path=1 if simt == "1" else 0)
     x = workloads.cfg3_points(6_000, planted_rows=600)
     got = eg.project(x, eg.ProjectionSpec(48, 0, 1)).words
     np.testing.assert_array_equal(got, oracle.project_words(x, 48, 0, 1))
@@ -319,16 +318,15 @@ def test_build_edge_cases(eg):
         eg.build_graph(x, params)
 
 
-@pytest.mark.parametrize("env", [{}, {"EG_PROJECT_UNFUSED": "1"}, {"EG_PROJECT_SIMT": "1"},
-                                 {"EG_FIXUP_FORCE_SEQ": "1"}, {"EG_FIXUP_LIST": "1"}])
-def test_fused_norms_and_flags(eg, oracle, monkeypatch, env):
+@pytest.mark.parametrize("env", [{}, {"project_path": 3}, {"project_path": 1},
+                                 {"fixup_force_seq": 1}, {"project_path": 2}])
+def test_fused_norms_and_flags(eg, oracle, native_options, env):
     """eg_project_rows: norms accumulated inside the tensor-core projection
     are bit-identical to k_row_stats' (unfused and SIMT paths), codes equal
     the oracle's, and the bad-row flags give the reference's errors."""
     import torch
     from paper_0904_3151_b200 import engine, workloads
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    native_options(**env)
     x = workloads.cfg3_points(5_000, planted_rows=500)
     xd = torch.from_numpy(x).cuda()
     codes, norms, bad, _ = engine.project_rows(xd, 48, 0, [1, 2])
@@ -420,14 +418,14 @@ def _tc_tau(dim, tf32):
 @pytest.mark.parametrize("tf32", [False, True])
 @pytest.mark.parametrize("n,dim,length,reps", [(20000, 384, 48, 3), (7000, 100, 64, 2),
                                                (5000, 128, 64, 1), (3000, 64, 32, 1)])
-def test_tc_projection_error_band(eg, oracle, monkeypatch, n, dim, length, reps, tf32):
+def test_tc_projection_error_band(eg, oracle, native_options, n, dim, length, reps, tf32):
     """The tensor-core projection's raw accumulator (kind::f16 2-term fp16
-    splits by default, kind::tf32 3xTF32 with EG_PROJECT_TF32=1) stays well
+    splits by default, kind::tf32 3xTF32 with project_path=2) stays well
     inside the certified band it uses to decide signs; signs equal the
     oracle."""
     import torch
     from paper_0904_3151_b200 import _native, engine
-    monkeypatch.setenv("EG_PROJECT_TF32", "1" if tf32 else "0")
+    native_options(project_path=2 if tf32 else 0)
     rng = np.random.default_rng(n + dim)
     x = rng.standard_normal((n, dim)).astype(np.float32)
     x[: n // 4] = np.abs(x[: n // 4])          # skewed rows like config 3
@@ -457,14 +455,12 @@ def test_tc_projection_error_band(eg, oracle, monkeypatch, n, dim, length, reps,
         np.testing.assert_array_equal(codes[h].cpu().numpy().view(np.uint64), want)
 
 
-@pytest.mark.parametrize("env", [{"EG_MSM_TILED": "1"}, {"EG_MSM_STREAMS": "1"},
-                                 {"EG_MSM_TILED": "1", "EG_MSM_STREAMS": "1"}])
-def test_msm_launch_variants(eg, oracle, manifest, monkeypatch, env):
-    """The tile-local partition (k_msm_tsort) and the single-stream schedule
-    give the same pair sets as the defaults."""
+@pytest.mark.parametrize("env", [{"msm_streams": 1}, {"msm_streams": 1, "sort_path": 1}])
+def test_msm_launch_variants(eg, oracle, manifest, native_options, env):
+    """The single-stream schedule gives the same pair sets as the default
+    two-stream overlap."""
     from paper_0904_3151_b200 import workloads
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    native_options(**env)
     words = workloads.cfg2_words(200_000, 10_000)
     got = eg.build_graph_hamming(eg.BitStringPool(words, 64).partitioned(8), 2)
     assert oracle.pair_digest(got.array) == manifest["cfg2_small"]["pairs_sha256"]
@@ -503,11 +499,11 @@ def test_sharded_path_over_nccl_single_rank(eg, oracle):
 
 
 @pytest.mark.parametrize("blocks", [4, 5, 7, 9, 16, 48])
-def test_forced_block_counts_same_pairs(eg, oracle, manifest, monkeypatch, blocks):
+def test_forced_block_counts_same_pairs(eg, oracle, manifest, native_options, blocks):
     """The pair set does not depend on the block count the units run with
     (hamming_join.py:300-375): every forced k' > d reproduces the
     reference-k pairs, per-replicate raw/new counts and edges."""
-    monkeypatch.setenv("EG_MSM_BLOCKS", str(blocks))
+    native_options(msm_blocks=blocks)
     rng = np.random.default_rng(blocks)
     n, length, k, d = 5000, 48, 12, 3
     base = (rng.random((n // 3, length)) < 0.3).astype(np.uint8)
@@ -567,11 +563,11 @@ def test_block_plan_keeps_reference_when_oversized(eg, caplog):
 
 
 @pytest.mark.parametrize("blocks", [4, 5, 6])
-def test_coarse_blocks_all_tiers_deterministic(eg, oracle, monkeypatch, blocks):
+def test_coarse_blocks_all_tiers_deterministic(eg, oracle, native_options, blocks):
     """Coarse forced block counts on skewed bits send buckets through every
     tier (small, pair-heavy -> medium, giant -> tiles); the pair set must
     equal the oracle's and be identical run to run."""
-    monkeypatch.setenv("EG_MSM_BLOCKS", str(blocks))
+    native_options(msm_blocks=blocks)
     rng = np.random.default_rng(blocks + 100)
     n, length, k, d = 50_000, 48, 12, 3
     bits = (rng.random((n, length)) < 0.8).astype(np.uint8)
@@ -585,12 +581,12 @@ def test_coarse_blocks_all_tiers_deterministic(eg, oracle, monkeypatch, blocks):
 
 
 @pytest.mark.parametrize("tf32", ["0", "1"])
-def test_projection_extreme_magnitudes(eg, oracle, monkeypatch, tf32):
+def test_projection_extreme_magnitudes(eg, oracle, native_options, tf32):
     """Rows outside the fp16 range of the kind::f16 split: entries >= 2^15
     (the row goes to the exact fix-up whole), rows of tiny magnitude (fp16
     subnormals: the absolute floor of the band) and mixed-scale rows --
     codes still bit-exact with the oracle."""
-    monkeypatch.setenv("EG_PROJECT_TF32", tf32)
+    native_options(project_path=2 if tf32 == "1" else 0)
     rng = np.random.default_rng(7)
     x = rng.standard_normal((4000, 96)).astype(np.float32)
     x[:500] *= np.float32(1e5)                         # fp16 overflow
@@ -603,13 +599,13 @@ def test_projection_extreme_magnitudes(eg, oracle, monkeypatch, tf32):
 
 
 @pytest.mark.parametrize("classic", ["0", "1"])
-def test_radix_sort_kernels(eg, monkeypatch, classic):
+def test_radix_sort_kernels(eg, native_options, classic):
     """Onesweep (decoupled look-back) and classic LSD passes: pair-key sort
     and key-value sort equal numpy's stable sort on ragged sizes, including
     skewed digits (long look-back chains) and keys with equal halves."""
     import torch
     from paper_0904_3151_b200 import engine
-    monkeypatch.setenv("EG_SORT_CLASSIC", classic)
+    native_options(sort_path=int(classic))
     rng = np.random.default_rng(3)
     dev = torch.device("cuda", 0)
     for m in (1, 2, 2047, 2048, 2049, 100_003, 1_500_000):

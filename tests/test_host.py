@@ -151,3 +151,27 @@ def test_workload_generators_shapes():
     x = workloads.cfg3_points(1000)
     assert x.shape == (1000, 384) and x.dtype == np.float32
     np.testing.assert_allclose(np.linalg.norm(x, axis=1), 1.0, rtol=1e-5)
+
+
+def test_library_reads_no_environment():
+    """Path choices come from eg_set_option only: the product library does
+    not import getenv (no environment knobs switch kernels)."""
+    import subprocess
+    _native.build()
+    und = subprocess.run(["nm", "-D", "--undefined-only", _native.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "getenv" not in und
+
+
+def test_options_api_validates_names():
+    lib = _native.lib()
+    assert lib.eg_set_option(b"no_such_option", 1) == _native.EG_ERR_ARG
+    assert lib.eg_set_option(b"project_path", 9) == _native.EG_ERR_ARG
+    assert lib.eg_set_option(b"msm_streams", 1) == _native.EG_OK
+    lib.eg_reset_options()
+    with _native.options(sort_path=1):
+        pass
+    import pytest
+    with pytest.raises(ValueError):
+        with _native.options(bogus=1):
+            pass

@@ -168,7 +168,8 @@ def test_write_edges_chunked_equals_single_call(eg, tmp_path, monkeypatch):
     edges = eg.EdgeList(g["pairs"], g["dist"])
     a, b = tmp_path / "a.txt", tmp_path / "b.txt"
     eg.write_edges(a, edges, {"nodes": 7})
-    monkeypatch.setenv("EG_FORMAT_CHUNK", "997")
+    from paper_0904_3151_b200 import io as egio
+    monkeypatch.setattr(egio, "FORMAT_CHUNK", 997)
     eg.write_edges(b, edges, {"nodes": 7})
     assert a.read_bytes() == b.read_bytes()
 

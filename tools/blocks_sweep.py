@@ -1,4 +1,4 @@
-"""Device time of the MSM stage per forced block count (EG_MSM_BLOCKS).
+"""Device time of the MSM stage per forced block count (option msm_blocks).
 
     python tools/blocks_sweep.py --config cfg3 --blocks 6,8,10,12,auto
 """
@@ -25,7 +25,7 @@ ap.add_argument("--reps", type=int, default=2)
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 params = bench.params_for(cfg, eg)
-data = bench.make_inputs(args.config)
+data, _ = bench.make_inputs(args.config)
 dev = torch.device("cuda", 0)
 if cfg.metric == "hamming":
     x = torch.from_numpy(data.view(np.int64)).to(dev).reshape(1, -1, 1)
@@ -42,7 +42,7 @@ def step():
 prof = _native.Profile()
 ref = None
 for b in args.blocks.split(","):
-    os.environ["EG_MSM_BLOCKS"] = "0" if b == "auto" else b
+    _native.lib().eg_set_option(b"msm_blocks", 0 if b == "auto" else int(b))
     step()
     best = None
     for _ in range(args.reps):

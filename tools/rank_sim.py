@@ -28,7 +28,7 @@ ap.add_argument("--ranks", type=int, default=3)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 params = bench.params_for(cfg, eg)
-x = torch.from_numpy(bench.make_inputs(a.config)).cuda()
+x = torch.from_numpy(bench.make_inputs(a.config)[0]).cuda()
 n = x.shape[0]
 ops = distributed.DeviceOps()
 full_codes, _ = engine.project_codes(x, engine.validate_rows(x), params.length, params.seed,

@@ -1,6 +1,6 @@
 """Time only the fused projection (eg_project_rows) on cfg3-shaped data.
 
-    EG_TC_EXP=<flags> python tools/tc_proj.py   (1 = no epilogue, 2 = no convert, 4 = R once)
+    python tools/tc_proj.py
 """
 import os
 import sys
@@ -28,4 +28,4 @@ for i in range(5):
     ms = {k: round(v["ms"], 3) for k, v in p.items()}
     if best is None or ms.get("project", 1e9) < best.get("project", 1e9):
         best = ms
-print("EXP", os.environ.get("EG_TC_EXP", "0"), best, "fixups", int(fix.item()), flush=True)
+print("projection ms", best, "fixups", int(fix.item()), flush=True)

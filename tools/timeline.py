@@ -25,7 +25,7 @@ ap.add_argument("--quiet", action="store_true")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 params = bench.params_for(cfg, eg)
-x = torch.from_numpy(bench.make_inputs(args.config)).cuda()
+x = torch.from_numpy(bench.make_inputs(args.config)[0]).cuda()
 marks = []
 
 
