@@ -166,13 +166,22 @@ size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates);
 /* n < 65536, or when C(k,d) > 4096.  Blocks of every k' follow the       */
 /* reference partition (first L % k' blocks one bit wider).  Synchronous. */
 /* h_cost (optional, 2 doubles): modelled ms of the chosen and of k.      */
-/* EG_MSM_BLOCKS env: >0 forces that k', <0 forces k.                      */
+/* Option "msm_blocks" (eg_set_option): >0 forces that k', -1 forces k.    */
 /* --------------------------------------------------------------------- */
 size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d);
 int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k,
                 int32_t d, double oversized_fraction, int32_t *h_k_out,
                 double *h_cost, void *d_workspace, size_t workspace_bytes,
                 void *stream);
+/* Output-size estimate for eg_msm_pairs' capacity: pairs with Hamming    */
+/* <= d among a strided sample of min(n, 8192) rows of (up to 4 of) the   */
+/* replicates, scaled by n(n-1)/(S(S-1)) and replicates/probed.            */
+/* h_estimate[0] = point estimate of the raw pairs (all replicates),      */
+/* h_estimate[1] = ~4-sigma upper bound (+10 %).  Workspace >= 256 bytes. */
+/* Synchronous.                                                           */
+int eg_msm_estimate_pairs(const uint64_t *d_codes, int64_t n, int32_t W,
+                          int32_t replicates, int32_t d, double *h_estimate,
+                          void *d_workspace, size_t workspace_bytes, void *stream);
 int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
                  int32_t replicates, const int32_t *h_block_bounds, int32_t k,
                  int32_t d, const int32_t *h_unit_rep, const uint64_t *h_unit_mask,
@@ -195,18 +204,32 @@ int eg_xrep_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t
                          int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,
                          void *stream);
 
+/* Full-code Hamming filter for pairs enumerated on a code prefix         */
+/* (lengths above EG_MAX_LENGTH: the MSM runs on the first 256 bits, a    */
+/* superset of the answer): d_keep[p] = popcount over all W words of the  */
+/* pair's replicate codes <= d (replicate from d_reps, or 0 when null);   */
+/* d_raw_counts[replicates] (device) counts the survivors per replicate.  */
+/* Asynchronous.                                                          */
+int eg_hamming_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
+                            const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
+                            int32_t replicates, uint8_t *d_keep, uint64_t *d_raw_counts,
+                            void *stream);
+
 /* --------------------------------------------------------------------- */
 /* Grouped sort of one mask.  Replaces grouped_radix_sort                 */
-/* (hamming_join.py:275-297): d_perm[n] is a permutation of rows in which */
-/* equal masked keys are contiguous; h_groups receives the group count    */
-/* and d_bounds[0..groups] the run offsets.  Order is deterministic but   */
-/* (like the reference's) not lexicographic.                              */
+/* (hamming_join.py:275-297) with the reference's exact permutation: the  */
+/* kept bits are chunked chunk_bits wide MSB first (masked_key_table,     */
+/* bitpool.py:224-253) and applied last chunk first as stable counting    */
+/* passes with buckets in first-seen order (_counting_pass, :52-82).      */
+/* d_perm[n] receives the permutation, d_bounds[0..groups] the run        */
+/* offsets (groups+1 values), *h_groups the group count.  Synchronous.    */
 /* --------------------------------------------------------------------- */
-size_t eg_grouped_sort_workspace(int64_t n, int32_t length);
+size_t eg_grouped_sort_workspace(int64_t n, int32_t chunk_bits);
 int eg_grouped_sort(const uint64_t *d_codes, int64_t n, int32_t length,
                     const int32_t *h_block_bounds, int32_t k, uint64_t mask_bits,
-                    uint32_t *d_perm, int64_t *d_bounds, int64_t *h_groups,
-                    void *d_workspace, size_t workspace_bytes, void *stream);
+                    int32_t chunk_bits, uint32_t *d_perm, int64_t *d_bounds,
+                    int64_t *h_groups, void *d_workspace, size_t workspace_bytes,
+                    void *stream);
 
 /* --------------------------------------------------------------------- */
 /* Cross-replicate first witness for externally supplied pair sets.       */

@@ -71,11 +71,13 @@ def _declare(lib):
         "eg_msm_workspace": ([i64, i32, i32], sz),
         "eg_msm_plan_workspace": ([i32, i32, i32], sz),
         "eg_msm_plan": ([P, i64, i32, i32, i32, dbl, P, P, P, sz, P], I),
+        "eg_msm_estimate_pairs": ([P, i64, i32, i32, i32, P, P, sz, P], I),
         "eg_msm_pairs": ([P, i64, i32, i32, P, i32, i32, P, P, i64, P, P, i64, P, P, sz, P], I),
         "eg_xrep_filter": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),
         "eg_xrep_filter_async": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),
+        "eg_hamming_filter_async": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),
         "eg_grouped_sort_workspace": ([i64, i32], sz),
-        "eg_grouped_sort": ([P, i64, i32, P, i32, ctypes.c_uint64, P, P, P, P, sz, P], I),
+        "eg_grouped_sort": ([P, i64, i32, P, i32, ctypes.c_uint64, i32, P, P, P, P, sz, P], I),
         "eg_first_witness": ([P, i64, P, i32, i32, i32, P, P], I),
         "eg_sort_workspace": ([i64, I], sz),
         "eg_sort_keys": ([P, P, i64, i32, P, sz, P], I),

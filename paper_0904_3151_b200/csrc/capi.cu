@@ -893,6 +893,39 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   return EG_OK;
 }
 
+// ------------------------------------------------------- output estimate
+int eg_msm_estimate_pairs(const uint64_t *d_codes, int64_t n, int32_t W, int32_t replicates,
+                          int32_t d, double *h_estimate, void *d_workspace,
+                          size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!h_estimate || n < 0 || W < 1 || W > 4 || replicates < 1 || d < 0)
+    return arg_error("eg_msm_estimate_pairs: bad arguments");
+  h_estimate[0] = h_estimate[1] = 0.0;
+  if (n < 2) return EG_OK;
+  Arena ar(d_workspace, workspace_bytes);
+  unsigned long long *cnt = ar.take<unsigned long long>(1);
+  if (!cnt) return EG_ERR_WORKSPACE;
+  const int S = (int)std::min<int64_t>(n, EST_SAMPLE);
+  const int probed = std::min(replicates, EST_MAXREPS);
+  const int nt = (S + EST_T - 1) / EST_T;
+  EG_CUDA_TRY(cudaMemsetAsync(cnt, 0, 8, st));
+  {
+    EG_PROF(PC_MISC, st);
+    k_est_pairs<<<dim3((unsigned)(nt * (nt + 1) / 2), (unsigned)probed), EST_T, 0, st>>>(
+        d_codes, n, W, S, d, cnt);
+  }
+  EG_LAUNCH_CHECK();
+  unsigned long long c = 0;
+  EG_CUDA_TRY(cudaMemcpyAsync(&c, cnt, 8, cudaMemcpyDeviceToHost, st));
+  EG_CUDA_TRY(cudaStreamSynchronize(st));
+  const double scale = S > 1 ? (double)n * (double)(n - 1) / ((double)S * (double)(S - 1)) : 1.0;
+  const double per_rep = (double)replicates / (double)probed;
+  h_estimate[0] = (double)c * scale * per_rep;
+  // ~4 sigma upper bound (sampled pairs ~ Poisson) plus 10 %
+  h_estimate[1] = 1.1 * ((double)c + 4.0 * sqrt((double)c) + 4.0) * scale * per_rep;
+  return EG_OK;
+}
+
 // ------------------------------------------------------------------ MSM
 size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates) {
   (void)length;
@@ -1041,7 +1074,7 @@ int eg_xrep_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t
                          int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,
                          void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
-  if (replicates < 1 || replicates > EG_MAX_REPLICATES || W < 1 || W > 4 || m < 0)
+  if (replicates < 1 || replicates > EG_MAX_REPLICATES || W < 1 || m < 0)
     return arg_error("eg_xrep_filter: bad arguments");
   EG_CUDA_TRY(cudaMemsetAsync(d_new_counts, 0, 8 * (size_t)replicates, st));
   if (m > 0) {
@@ -1085,60 +1118,105 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
   return EG_OK;
 }
 
+// ---------------------------------------------------- full-code filter
+int eg_hamming_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
+                            const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
+                            int32_t replicates, uint8_t *d_keep, uint64_t *d_raw_counts,
+                            void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (replicates < 1 || replicates > EG_MAX_REPLICATES || W < 1 || m < 0 || d < 0)
+    return arg_error("eg_hamming_filter: bad arguments");
+  EG_CUDA_TRY(cudaMemsetAsync(d_raw_counts, 0, 8 * (size_t)replicates, st));
+  if (m > 0) {
+    unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
+    EG_PROF(PC_MISC, st);
+    k_hamming_filter<<<grid, 256, 0, st>>>(d_keys, d_reps, m, d_codes, n, W, d, replicates,
+                                           d_keep, (unsigned long long *)d_raw_counts);
+    EG_LAUNCH_CHECK();
+  }
+  return EG_OK;
+}
+
 // --------------------------------------------------------- grouped sort
-size_t eg_grouped_sort_workspace(int64_t n, int32_t length) {
-  (void)length;
-  return ws_bytes(n, 8) * 2 + ws_bytes(n, 1) + radix_workspace(n, true) + compact_workspace(n) +
-         4096;
+size_t eg_grouped_sort_workspace(int64_t n, int32_t chunk_bits) {
+  const int cb = chunk_bits < 1 ? 1 : (chunk_bits > 24 ? 24 : chunk_bits);
+  return ws_bytes(n, 8) + 2 * ws_bytes(n, 4) + ws_bytes(n, 1) + ws_bytes(n, 8) +
+         ws_bytes((size_t)1 << cb, 4) + ws_bytes(EG_MAX_LENGTH, 4) +
+         radix_workspace(n, true) + compact_workspace(n) + 4096;
 }
 
 int eg_grouped_sort(const uint64_t *d_codes, int64_t n, int32_t length,
-                    const int32_t *h_block_bounds, int32_t k, uint64_t mask_bits, uint32_t *d_perm,
-                    int64_t *d_bounds, int64_t *h_groups, void *d_workspace,
-                    size_t workspace_bytes, void *stream) {
+                    const int32_t *h_block_bounds, int32_t k, uint64_t mask_bits,
+                    int32_t chunk_bits, uint32_t *d_perm, int64_t *d_bounds, int64_t *h_groups,
+                    void *d_workspace, size_t workspace_bytes, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 1 || n >= (1ll << 32)) return arg_error("eg_grouped_sort: need 1 <= n < 2^32");
   if (length < 1 || length > EG_MAX_LENGTH || k < 1 || k > length || k > EG_MAX_BLOCKS)
     return arg_error("eg_grouped_sort: bad length/k");
+  if (chunk_bits < 1 || chunk_bits > 24) return arg_error("chunk_bits must be in [1, 24]");
   const int W = (length + 63) / 64;
+  // kept bit positions in ascending order (bitpool._kept_positions)
+  std::vector<int32_t> cols;
   UnitBatch ub;
   memset(&ub, 0, sizeof(ub));
   ub.count = 1;
-  for (int t = 0; t < length; ++t) ub.kept[0][t >> 6] |= 1ull << (t & 63);
-  for (int b = 0; b < k; ++b)
-    if (mask_bits >> b & 1)
-      for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t)
-        ub.kept[0][t >> 6] &= ~(1ull << (t & 63));
+  for (int b = 0; b < k; ++b) {
+    if (mask_bits >> b & 1) continue;
+    for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t) {
+      cols.push_back(t);
+      ub.kept[0][t >> 6] |= 1ull << (t & 63);
+    }
+  }
+  const int ncols = (int)cols.size();
   Arena ar(d_workspace, workspace_bytes);
-  uint64_t *keyw = ar.take<uint64_t>(n);
-  uint64_t *idx = ar.take<uint64_t>(n);
+  uint64_t *key = ar.take<uint64_t>(n);
+  uint32_t *val = ar.take<uint32_t>(n);
+  uint32_t *vbuf = ar.take<uint32_t>(n);
   uint8_t *flags = ar.take<uint8_t>(n);
-  if (!keyw || !idx || !flags) return EG_ERR_WORKSPACE;
+  uint64_t *idx = ar.take<uint64_t>(n);
+  uint32_t *first = ar.take<uint32_t>((size_t)1 << chunk_bits);
+  int32_t *d_cols = ar.take<int32_t>(EG_MAX_LENGTH);
+  if (!key || !val || !vbuf || !flags || !idx || !first || !d_cols) {
+    set_error("eg_grouped_sort: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
   const unsigned grid = (unsigned)std::min<int64_t>((n + 255) / 256, 4096);
   {
     EG_PROF(PC_MISC, st);
     k_iota<<<grid, 256, 0, st>>>(d_perm, n);
   }
   EG_LAUNCH_CHECK();
+  if (ncols == 0) {   // every block masked: one group
+    int64_t b2[2] = {0, n};
+    EG_CUDA_TRY(cudaMemcpyAsync(d_bounds, b2, 16, cudaMemcpyHostToDevice, st));
+    EG_CUDA_TRY(cudaStreamSynchronize(st));
+    *h_groups = 1;
+    return EG_OK;
+  }
+  EG_CUDA_TRY(cudaMemcpyAsync(d_cols, cols.data(), (size_t)ncols * 4, cudaMemcpyHostToDevice, st));
+  const int nch = (ncols + chunk_bits - 1) / chunk_bits;
+  int shifts[8], np = 0;
+  for (int sft = 0; sft < ilog2_ceil((uint64_t)std::max<int64_t>(n, 2)); sft += 8) shifts[np++] = sft;
   size_t mark = ar.used;
-  for (int w = W - 1; w >= 0; --w) {
-    const uint64_t kw = ub.kept[0][w];
-    if (!kw) continue;
+  for (int c = nch - 1; c >= 0; --c) {   // last chunk first (hamming_join.py:267)
+    EG_CUDA_TRY(cudaMemsetAsync(first, 0xff, ((size_t)1 << chunk_bits) * 4, st));
     {
       EG_PROF(PC_MISC, st);
-      k_masked_word<<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, w, kw, keyw);
+      k_chunk_first<<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, d_cols, c * chunk_bits,
+                                          chunk_bits, ncols, first, vbuf);
+      k_chunk_rank<<<grid, 256, 0, st>>>(vbuf, first, d_perm, n, key, val);
     }
     EG_LAUNCH_CHECK();
-    int shifts[8], np = 0;
-    for (int s = 0; s < 64; s += 8)
-      if ((kw >> s) & 0xff) shifts[np++] = s;
     ar.used = mark;
-    int rc = radix_sort(keyw, d_perm, n, shifts, np, ar, st);
+    int rc = radix_sort(key, val, n, shifts, np, ar, st);
     if (rc) return rc;
+    EG_CUDA_TRY(cudaMemcpyAsync(d_perm, val, (size_t)n * 4, cudaMemcpyDeviceToDevice, st));
   }
   ar.used = mark;
-  EG_PROF(PC_MISC, st);
-  k_group_flags<4><<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, ub, flags, idx);
+  {
+    EG_PROF(PC_MISC, st);
+    k_group_flags<4><<<grid, 256, 0, st>>>(d_codes, d_perm, n, W, ub, flags, idx);
+  }
   EG_LAUNCH_CHECK();
   int64_t groups = 0;
   int rc = compact<uint32_t>(idx, (const uint32_t *)nullptr, flags, n, (uint64_t *)d_bounds,

@@ -1205,6 +1205,38 @@ __global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint16_t 
     if (cnt[i]) atomicAdd(&new_counts[i], (unsigned long long)cnt[i]);
 }
 
+// ------------------------------------------------------ full-code filter
+// Pairs enumerated on a code prefix (strings longer than the kernels' 256
+// bits, see engine.msm_candidates) are a superset of the answer; keep[p] =
+// popcount of the FULL codes of the pair's replicate <= d, and raw[h]
+// counts the survivors per replicate.
+__global__ void k_hamming_filter(const uint64_t *__restrict__ keys, const uint16_t *__restrict__ reps,
+                                 int64_t m, const uint64_t *__restrict__ codes, int64_t n, int W,
+                                 int d, int nreps, uint8_t *__restrict__ keep,
+                                 unsigned long long *__restrict__ raw) {
+  __shared__ unsigned int cnt[XREP_SMEM_REPS];
+  for (int i = threadIdx.x; i < nreps && i < XREP_SMEM_REPS; i += blockDim.x) cnt[i] = 0;
+  __syncthreads();
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[p];
+    const int64_t i = (int64_t)(key >> 32), j = (int64_t)(key & 0xffffffffu);
+    const int h = reps ? reps[p] : 0;
+    const uint64_t *c = codes + (int64_t)h * n * W;
+    int pc = 0;
+    for (int w = 0; w < W && pc <= d; ++w) pc += __popcll(__ldg(c + i * W + w) ^ __ldg(c + j * W + w));
+    const bool ok = pc <= d;
+    keep[p] = ok;
+    if (ok) {
+      if (h < XREP_SMEM_REPS) atomicAdd(&cnt[h], 1u);
+      else atomicAdd(&raw[h], 1ull);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nreps && i < XREP_SMEM_REPS; i += blockDim.x)
+    if (cnt[i]) atomicAdd(&raw[i], (unsigned long long)cnt[i]);
+}
+
 // ------------------------------------------------------ first witness
 __global__ void k_first_witness(const uint64_t *__restrict__ keys, int64_t m,
                                 const uint64_t *const *__restrict__ pools, int npools, int W,
@@ -1224,17 +1256,55 @@ __global__ void k_first_witness(const uint64_t *__restrict__ keys, int64_t m,
 }
 
 // ------------------------------------------------------- grouped sort API
-__global__ void k_masked_word(const uint64_t *__restrict__ codes, const uint32_t *__restrict__ perm,
-                              int64_t n, int W, int w, uint64_t kept, uint64_t *__restrict__ out) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = codes[(int64_t)perm[i] * W + w] & kept;
-}
-
+// grouped_radix_sort (hamming_join.py:275-297) reproduced pass for pass:
+// the masked key is split into chunk_bits-wide chunks, MSB first
+// (masked_key_table, bitpool.py:224-253), and the chunks are applied last to
+// first, each as a stable counting pass whose buckets are laid out in
+// FIRST-SEEN order (_counting_pass, hamming_join.py:52-82).  On the device a
+// pass is: chunk value of every position + atomicMin of the position into a
+// per-value table (= the bucket's first occurrence), then a stable LSD radix
+// sort of the permutation by that first occurrence.
 __global__ void k_iota(uint32_t *__restrict__ p, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = (uint32_t)i;
+}
+
+__device__ __forceinline__ uint32_t chunk_value(const uint64_t *__restrict__ codes, int64_t row,
+                                                int W, const int32_t *__restrict__ cols, int c0,
+                                                int cb, int ncols) {
+  uint32_t v = 0;
+  for (int q = 0; q < cb; ++q) {
+    const int ci = c0 + q;
+    uint32_t bit = 0;
+    if (ci < ncols) {
+      const int t = cols[ci];
+      bit = (uint32_t)(codes[row * W + (t >> 6)] >> (t & 63)) & 1u;
+    }
+    v = (v << 1) | bit;        // zero padding at the low end of the last chunk
+  }
+  return v;
+}
+
+__global__ void k_chunk_first(const uint64_t *__restrict__ codes, const uint32_t *__restrict__ perm,
+                              int64_t n, int W, const int32_t *__restrict__ cols, int c0, int cb,
+                              int ncols, uint32_t *__restrict__ first, uint32_t *__restrict__ vbuf) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = chunk_value(codes, perm[p], W, cols, c0, cb, ncols);
+    vbuf[p] = v;
+    atomicMin(&first[v], (uint32_t)p);
+  }
+}
+
+__global__ void k_chunk_rank(const uint32_t *__restrict__ vbuf, const uint32_t *__restrict__ first,
+                             const uint32_t *__restrict__ perm, int64_t n,
+                             uint64_t *__restrict__ key, uint32_t *__restrict__ val) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    key[p] = first[vbuf[p]];
+    val[p] = perm[p];
+  }
 }
 
 template <int WMAX>

@@ -91,4 +91,50 @@ __global__ void __launch_bounds__(PLAN_NT) k_msm_plan(const uint64_t *__restrict
   }
 }
 
+// ------------------------------------------------------- output estimate
+// Pairs with popcount(c_a ^ c_b) <= d among a strided sample of S rows of
+// each probed replicate (the MSM output restricted to the sample), for the
+// output-capacity estimate of eg_msm_estimate_pairs.  Grid: (tile pairs,
+// replicates); 256-row tiles staged in shared memory.
+constexpr int EST_SAMPLE = 8192, EST_T = 256, EST_MAXREPS = 4;
+__global__ void __launch_bounds__(EST_T) k_est_pairs(const uint64_t *__restrict__ codes, int64_t n,
+                                                     int W, int S, int d,
+                                                     unsigned long long *__restrict__ out) {
+  __shared__ uint64_t tb[EST_T * 4];
+  __shared__ unsigned long long red[EST_T / 32];
+  const int nt = (S + EST_T - 1) / EST_T;
+  // tile pair (ta <= tb) of the upper triangle, row-major
+  int ta = 0, rem = blockIdx.x;
+  while (rem >= nt - ta) { rem -= nt - ta; ++ta; }
+  const int tbi = ta + rem;
+  const uint64_t *cr = codes + (int64_t)blockIdx.y * n * W;
+  auto row_of = [&](int s) { return (int64_t)((double)s * (double)n / (double)S); };
+  for (int i = threadIdx.x; i < EST_T * W; i += EST_T) {
+    const int s = tbi * EST_T + i / W;
+    tb[i] = s < S ? cr[row_of(s) * W + i % W] : 0ull;
+  }
+  uint64_t a[4] = {0, 0, 0, 0};
+  const int sa = ta * EST_T + threadIdx.x;
+  if (sa < S)
+    for (int w = 0; w < W; ++w) a[w] = cr[row_of(sa) * W + w];
+  __syncthreads();
+  unsigned long long c = 0;
+  if (sa < S) {
+    const int j0 = ta == tbi ? threadIdx.x + 1 : 0;
+    for (int j = j0; j < EST_T && tbi * EST_T + j < S; ++j) {
+      int pc = 0;
+      for (int w = 0; w < W; ++w) pc += __popcll(a[w] ^ tb[j * W + w]);
+      c += pc <= d;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < EST_T / 32; ++i) t += red[i];
+    if (t) atomicAdd(out, t);
+  }
+}
+
 }  // namespace eg

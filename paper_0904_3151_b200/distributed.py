@@ -66,16 +66,11 @@ class DeviceOps:
     def plan(self, codes, params):
         """Block count of the units (deterministic in the codes, so every
         rank holding the gathered codes picks the same one)."""
-        return engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
+        return engine.plan_blocks(codes, params.length, params.blocks, params.mismatch)
 
     def candidates(self, codes, params, units, blocks):
-        from .bitpool import block_partition
-        bounds = block_partition(params.length, blocks)
-        reps, masks = engine.units_for(range(params.replicates), blocks, params.mismatch)
-        sel = np.asarray(units, dtype=np.int64)
-        keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch,
-                                      reps[sel], masks[sel])
-        return keys, info
+        return engine.msm_candidates(codes, params.length, params.blocks, params.mismatch,
+                                     blocks=blocks, select=lambda total: units)
 
     def sort(self, keys, n):
         return engine.sort_pair_keys(keys, n)
@@ -184,7 +179,7 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
         codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
     from math import comb
     blocks = ops.plan(codes, params)
-    units = my_units(params.replicates * comb(blocks, params.mismatch), world, rank)
+    units = my_units(params.replicates * comb(blocks, max(0, params.mismatch)), world, rank)
     keys, info = ops.candidates(codes, params, units, blocks)
     info = dict(info, blocks=blocks)
     keys = ops.sort(keys, n)
@@ -195,15 +190,9 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
 
 def hamming_step(codes, params, world: int, rank: int):
     """Config 2: enumerate_pairs over resident words, units sharded."""
-    from .bitpool import block_partition
     n = codes.shape[1]
-    blocks = engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
-    bounds = block_partition(params.length, blocks)
-    reps, masks = engine.units_for([0], blocks, params.mismatch)
-    sel = np.asarray(my_units(len(reps), world, rank), dtype=np.int64)
-    keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, reps[sel],
-                                  masks[sel])
-    info["blocks"] = blocks
+    keys, info = engine.msm_candidates(codes, params.length, params.blocks, params.mismatch,
+                                       select=lambda total: my_units(total, world, rank))
     engine.sort_pair_keys(keys, n)
     if world > 1:
         dummy = torch.zeros(keys.numel(), dtype=torch.float64, device=keys.device)
@@ -219,3 +208,143 @@ def last_counts(res):
     return {"candidates": info.get("emitted"), "raw": info.get("raw"), "new": info.get("new"),
             "edges": int(keys.numel()) if keys is not None else None,
             "max_group": info.get("max_group"), "blocks": info.get("blocks")}
+
+
+# ------------------------------------------------ one process, many devices
+def _device_list(devices):
+    if isinstance(devices, int):
+        if devices < 1:
+            raise ValueError("devices must be >= 1")
+        return [torch.device("cuda", i) for i in range(devices)]
+    out = []
+    for d in devices:
+        dev = torch.device("cuda", d) if isinstance(d, int) else torch.device(d)
+        if dev.type != "cuda" or dev.index is None:
+            raise ValueError(f"devices must name CUDA devices with an index, got {d!r}")
+        out.append(dev)
+    if not out:
+        raise ValueError("devices must not be empty")
+    return out
+
+
+def build_on_devices(rows, params, metric: str, devices):
+    """The sharded build of ``build_step`` driven from ONE process over
+    several devices (``build_graph(..., devices=)``): row
+    shards projected on their devices, codes and norms gathered by peer
+    copies, the block count planned once, (replicate, mask) units dealt
+    cyclically over the shards, each shard's candidates sorted and verified
+    on its device, and the sorted edge runs merged on the first device.
+
+    ``devices`` is a count or a list of CUDA devices; a device may appear
+    more than once (its shards then run one after another on it), which is
+    how one GPU exercises the multi-device path.  Every pair has exactly one
+    owning unit and a per-pair-deterministic distance, so the result is the
+    same for any device list (the mirror of the reference's thread-count
+    contract, tests/test_pipeline.py:130-135)."""
+    from concurrent.futures import ThreadPoolExecutor
+    from math import comb
+
+    from .pipeline import _metric_id
+    devs = _device_list(devices)
+    world = len(devs)
+    distinct = list(dict.fromkeys(devs))
+    n = rows.shape[0]
+    reps_ids = list(range(1, params.replicates + 1))
+
+    def on(dev, fn):
+        with torch.cuda.device(dev):
+            out = fn()
+            torch.cuda.current_stream(dev).synchronize()
+            return out
+
+    def run(fn_by_shard):
+        """fn_by_shard(s) for every shard, shards of one device in order,
+        devices concurrently (ctypes and torch release the GIL)."""
+        results = [None] * world
+
+        def work(dev):
+            for s in range(world):
+                if devs[s] == dev:
+                    results[s] = on(dev, lambda: fn_by_shard(s))
+        with ThreadPoolExecutor(max_workers=len(distinct)) as ex:
+            list(ex.map(work, distinct))
+        return results
+
+    # rows on every device (one H2D per device from host memory, else a peer copy)
+    src = rows if isinstance(rows, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(rows))
+    if src.device.type == "cpu" and not src.is_pinned() and len(distinct) > 1:
+        src = src.pin_memory()
+    xs = {}
+
+    def put(dev):
+        xs[dev] = on(dev, lambda: engine.as_device_rows(src, dev))
+    with ThreadPoolExecutor(max_workers=len(distinct)) as ex:
+        list(ex.map(put, distinct))
+
+    # 1. projection of the row shards (norms and bad-row flags in the same pass)
+    shards = [row_shard(n, world, s) for s in range(world)]
+    proj = run(lambda s: engine.project_rows(xs[devs[s]][shards[s][0]:shards[s][1]],
+                                             params.length, params.seed, reps_ids))
+    # first offending row over all shards (reference order: non-finite, then zero norm)
+    flags = []
+    for s, (codes_s, norms_s, bad_s, _) in enumerate(proj):
+        b = bad_s.cpu().tolist()
+        flags.append([v + shards[s][0] if v >= 0 else -1 for v in b])
+    from .errors import DataError
+    nonfinite = [f[0] for f in flags if f[0] >= 0]
+    zero = [f[1] for f in flags if f[1] >= 0]
+    if nonfinite:
+        raise DataError(f"row {min(nonfinite)} has a non-finite entry")
+    if zero:
+        raise DataError(f"row {min(zero)} has zero norm and cannot be projected")
+
+    # 2. codes and norms of all rows on every device (peer copies)
+    full = {}
+
+    def gather(dev):
+        def f():
+            codes = torch.cat([p[0].to(dev, non_blocking=True) for p in proj], dim=1)
+            norms = torch.cat([p[1].to(dev, non_blocking=True) for p in proj])
+            return codes, norms
+        full[dev] = on(dev, f)
+    with ThreadPoolExecutor(max_workers=len(distinct)) as ex:
+        list(ex.map(gather, distinct))
+
+    # 3. one plan (deterministic in the codes) for every shard
+    blocks = on(devs[0], lambda: engine.plan_blocks(full[devs[0]][0], params.length,
+                                                    params.blocks, params.mismatch))
+    ops = DeviceOps()
+    total_units = params.replicates * comb(blocks, params.mismatch)
+
+    def shard_build(s):
+        dev = devs[s]
+        codes, norms = full[dev]
+        units = my_units(total_units, world, s)
+        if not units:
+            empty = torch.empty(0, dtype=torch.int64, device=dev)
+            return empty, empty.to(torch.float64), None
+        keys, info = ops.candidates(codes, params, units, blocks)
+        keys = ops.sort(keys, n)
+        ek, ed = engine.verify(xs[dev], norms, keys, _metric_id(metric), params.epsilon)
+        return ek, ed, info
+    parts = run(shard_build)
+
+    # 4. merge the sorted per-shard edge runs on the first device
+    def merge():
+        dev = devs[0]
+        ks = torch.cat([p[0].to(dev) for p in parts])
+        ds = torch.cat([p[1].to(dev) for p in parts])
+        return ops.merge(ks, ds, n)
+    keys, dist = on(devs[0], merge)
+    infos = [p[2] for p in parts if p[2] is not None]
+    reps = params.replicates
+    info = {
+        "emitted": sum(i["emitted"] for i in infos),
+        "max_group": max([i["max_group"] for i in infos] or [0]),
+        "raw": tuple(sum(i["raw"][h] for i in infos) for h in range(reps)),
+        "new": tuple(sum(i["new"][h] for i in infos) for h in range(reps)),
+        "blocks": blocks,
+        "reference_blocks": all(i.get("reference_blocks", False) for i in infos) and bool(infos),
+        "devices": [str(d) for d in devs],
+    }
+    return {"keys": keys, "dist": dist, "info": info}

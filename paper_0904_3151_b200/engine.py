@@ -208,25 +208,39 @@ _last_plan: dict = {}
 
 
 def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps, unit_masks,
-              capacity: int | None = None):
-    """Run the MSM units; returns (keys tensor, counts dict)."""
+              capacity: int | None = None, full_codes: torch.Tensor | None = None):
+    """Run the MSM units; returns (keys tensor, counts dict).
+
+    ``full_codes`` (strings longer than the kernels' EG_MAX_LENGTH bits):
+    ``codes`` is then a prefix view of them; the units emit the pairs within
+    Hamming d on the prefix (a superset), which are filtered by the full
+    codes' Hamming distance before the cross-replicate rule (also on the
+    full codes)."""
     dev = codes.device
     reps, n, W = codes.shape
     k = len(block_bounds) - 1
     if length > _native.MAX_LENGTH or k > _native.MAX_BLOCKS:
-        raise NotImplementedError(
-            f"enumeration kernels support length <= {_native.MAX_LENGTH} and "
-            f"k <= {_native.MAX_BLOCKS} (got length={length}, k={k})")
+        raise ValueError(f"eg_msm_pairs runs on <= {_native.MAX_LENGTH} bits and <= "
+                         f"{_native.MAX_BLOCKS} blocks (msm_candidates maps larger ones)")
     lib = _native.lib()
     bb = np.ascontiguousarray(block_bounds, dtype=np.int32)
     ur = np.ascontiguousarray(unit_reps, dtype=np.int32)
     um = np.ascontiguousarray(unit_masks, dtype=np.uint64)
-    hint_key = (n, length, k, d, reps, len(ur))
+    hint_key = (n, length, k, d, reps, len(ur), full_codes is not None)
     if capacity is None:
-        capacity = _capacity_hint.get(hint_key, max(1 << 16, 2 * n))
+        capacity = _capacity_hint.get(hint_key)
+        if capacity is None:
+            # cold call: a sampled upper bound of the output (eg_msm_estimate_
+            # pairs) sizes the buffer, so the rerun below stays exceptional
+            capacity = max(1 << 16, 2 * n)
+            if n >= 1 << 16:
+                capacity = max(capacity, int(estimate_pairs(codes, d)[1]))
     ws = _ws(lib.eg_msm_workspace(n, length, reps), dev)
     counts = (ctypes_i64 * (2 * reps + 2))()
-    defer = reps > 1       # cross-replicate rule in a separate streaming pass
+    # cross-replicate rule in a separate streaming pass (and always when the
+    # prefix pairs still need the full-code filter)
+    defer = reps > 1 or full_codes is not None
+    reruns = 0
     while True:
         out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         rtag = torch.empty(max(capacity, 1), dtype=torch.int16, device=dev) if defer else None
@@ -234,7 +248,9 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
                               um.ctypes.data, len(ur), _p(out), _p(rtag), capacity,
                               ctypes_addr(counts), _p(ws), ws.numel(), _stream(dev))
         if rc == _native.EG_ERR_CAPACITY:
+            # the exact total is known now: one more pass with that capacity
             capacity = int(counts[0])
+            reruns += 1
             del out, rtag
             continue
         check(rc, "msm_pairs")
@@ -243,17 +259,36 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     _capacity_hint[hint_key] = max(1 << 16, int(total * 1.25) + 1024)
     raw = tuple(int(counts[2 + h]) for h in range(reps))
     keys = out[:total]
-    if defer:
+    xcodes = codes
+    if full_codes is not None:
+        # prefix pairs -> pairs within d on the full codes (per replicate)
+        xcodes = full_codes
+        tag = rtag[:total] if reps > 1 else None
+        keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+        rawc = torch.empty(reps, dtype=torch.int64, device=dev)
+        check(lib.eg_hamming_filter_async(_p(keys), _p(tag), total, _p(full_codes), n,
+                                          full_codes.shape[2], d, reps, _p(keep), _p(rawc),
+                                          _stream(dev)), "hamming_filter")
+        sel = keep[:total].bool()
+        keys = keys[sel]
+        if reps > 1:
+            rtag = rtag[:total][sel]
+        total = int(keys.numel())
+        raw = tuple(int(v) for v in rawc.tolist())
+    if reps > 1:
         keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
         newc = torch.empty(reps, dtype=torch.int64, device=dev)
-        check(lib.eg_xrep_filter_async(_p(keys), _p(rtag), total, _p(codes), n, W, d, reps,
-                                       _p(keep), _p(newc), _stream(dev)), "xrep_filter")
+        check(lib.eg_xrep_filter_async(_p(keys), _p(rtag), total, _p(xcodes), n,
+                                       xcodes.shape[2], d, reps, _p(keep), _p(newc),
+                                       _stream(dev)), "xrep_filter")
         # the counts reach pinned host memory behind the filter; the
         # compaction's synchronisation makes them readable
         newc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
         newc_host.copy_(newc, non_blocking=True)
         keys = compact_keys(keys, keep[:total])
         new = tuple(int(v) for v in newc_host.tolist())
+    elif full_codes is not None:
+        new = raw
     else:
         new = tuple(int(counts[2 + reps + h]) for h in range(reps))
     info = {
@@ -261,8 +296,73 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
         "max_group": int(counts[1]),
         "raw": raw,
         "new": new,
+        "capacity": capacity,
+        "reruns": reruns,
     }
     return keys, info
+
+
+def msm_view(codes: torch.Tensor, length: int, k: int, d: int):
+    """(codes view, its length, block count to plan from, full codes or None)
+    the kernels run on.  The answer {(i, j): Hamming <= d} does not depend
+    on the blocks (hamming_join.py:300-375), so k > EG_MAX_BLOCKS runs with
+    at most EG_MAX_BLOCKS blocks, and strings longer than EG_MAX_LENGTH bits
+    are enumerated on their first EG_MAX_LENGTH bits (pairs within d there
+    are a superset of the answer) and filtered by the full codes."""
+    if d >= _native.MAX_BLOCKS:
+        raise NotImplementedError(
+            f"mismatch d={d}: the enumeration needs a partition into more than d <= "
+            f"{_native.MAX_BLOCKS - 1} blocks")
+    reps, n, W = codes.shape
+    if length <= _native.MAX_LENGTH and k <= _native.MAX_BLOCKS:
+        return codes, length, k, None
+    lv = min(length, _native.MAX_LENGTH)
+    wv = -(-lv // 64)
+    view = codes[:, :, :wv].contiguous() if W > wv else codes
+    kv = max(d + 1, min(k, _native.MAX_BLOCKS, lv))
+    return view, lv, kv, (codes if lv < length else None)
+
+
+def plan_blocks(codes: torch.Tensor, length: int, k: int, d: int,
+                oversized_fraction: float = 0.25) -> int:
+    """Block count of the units (eg_msm_plan on the kernels' view)."""
+    view, lv, kv, _ = msm_view(codes, length, k, d)
+    return msm_plan(view, lv, kv, d, oversized_fraction)
+
+
+def msm_candidates(codes: torch.Tensor, length: int, k: int, d: int, *, blocks: int | None = None,
+                   select=None, oversized_fraction: float = 0.25, block_bounds=None):
+    """All (replicate, mask) units of the planned block count (or
+    ``blocks``), optionally restricted by ``select(total_units) -> indices``
+    (sharding): (candidate keys, info).  info["reference_blocks"] says
+    whether the units ran on the reference's own blocks (``block_bounds``
+    when given, else the standard partition) -- only then is
+    info["max_group"] the reference's largest group."""
+    from .bitpool import block_partition
+    view, lv, kv, full = msm_view(codes, length, k, d)
+    kk = blocks or msm_plan(view, lv, kv, d, oversized_fraction)
+    same = kk == k and full is None and lv == length
+    bounds = block_bounds if (same and block_bounds is not None) else block_partition(lv, kk)
+    ureps, umasks = units_for(range(codes.shape[0]), kk, d)
+    if select is not None:
+        sel = np.asarray(select(len(ureps)), dtype=np.int64)
+        ureps, umasks = ureps[sel], umasks[sel]
+    keys, info = msm_pairs(view, lv, bounds, d, ureps, umasks, full_codes=full)
+    info["blocks"] = kk
+    info["reference_blocks"] = same
+    return keys, info
+
+
+def estimate_pairs(codes: torch.Tensor, d: int):
+    """(point estimate, ~4-sigma upper bound) of the raw pairs the MSM units
+    emit over all replicates of ``codes`` (eg_msm_estimate_pairs)."""
+    reps, n, W = codes.shape
+    est = (ctypes.c_double * 2)()
+    ws = _ws(4096, codes.device)
+    check(_native.lib().eg_msm_estimate_pairs(_p(codes), n, W, reps, d, ctypes.addressof(est),
+                                              _p(ws), ws.numel(), _stream(codes.device)),
+          "msm_estimate_pairs")
+    return float(est[0]), float(est[1])
 
 
 def sort_pair_keys(keys: torch.Tensor, n: int) -> torch.Tensor:
@@ -333,8 +433,11 @@ def compact_keys(keys: torch.Tensor, flags: torch.Tensor) -> torch.Tensor:
     return out[:int(cnt.value)]
 
 
-def grouped_sort(codes_1: torch.Tensor, length: int, block_bounds, mask_bits: int):
-    """(perm int64 tensor, bounds int64 tensor) grouping equal masked keys."""
+def grouped_sort(codes_1: torch.Tensor, length: int, block_bounds, mask_bits: int,
+                 chunk_bits: int = 16):
+    """(perm int32 tensor, bounds int64 tensor): the reference's
+    grouped_radix_sort permutation (first-seen buckets, chunk_bits-wide
+    passes) and its equal-key run offsets."""
     dev = codes_1.device
     n, W = codes_1.shape
     k = len(block_bounds) - 1
@@ -342,12 +445,34 @@ def grouped_sort(codes_1: torch.Tensor, length: int, block_bounds, mask_bits: in
     bb = np.ascontiguousarray(block_bounds, dtype=np.int32)
     perm = torch.empty(n, dtype=torch.int32, device=dev)
     bounds = torch.empty(n + 1, dtype=torch.int64, device=dev)
-    ws = _ws(lib.eg_grouped_sort_workspace(n, length), dev)
+    ws = _ws(lib.eg_grouped_sort_workspace(n, chunk_bits), dev)
     g = ctypes_i64(0)
-    check(lib.eg_grouped_sort(_p(codes_1), n, length, bb.ctypes.data, k, mask_bits, _p(perm),
-                              _p(bounds), ctypes_addr(g), _p(ws), ws.numel(), _stream(dev)),
-          "grouped_sort")
+    check(lib.eg_grouped_sort(_p(codes_1), n, length, bb.ctypes.data, k, mask_bits, chunk_bits,
+                              _p(perm), _p(bounds), ctypes_addr(g), _p(ws), ws.numel(),
+                              _stream(dev)), "grouped_sort")
     return perm, bounds[:int(g.value) + 1]
+
+
+def edges_to_host(keys: torch.Tensor, dist: torch.Tensor | None):
+    """Device edge keys (+ distances) -> host int64 (m, 2) pairs and float64
+    distances, the boundary layout (edges.py:12-55).  The (i, j) split runs
+    on the device and both arrays land in pinned host memory (torch's
+    caching host allocator: repeated builds reuse the pinned blocks), in
+    2^27-edge chunks."""
+    m = int(keys.numel())
+    if m == 0:
+        return np.empty((0, 2), np.int64), np.empty(0, np.float64)
+    ph = torch.empty((m, 2), dtype=torch.int64, pin_memory=True)
+    dh = torch.empty(m, dtype=torch.float64, pin_memory=True) if dist is not None else None
+    step = 1 << 27
+    for lo in range(0, m, step):
+        k = keys[lo:lo + step]
+        ph[lo:lo + k.numel()].copy_(torch.stack((k >> 32, k & 0xFFFFFFFF), dim=1),
+                                    non_blocking=True)
+    if dh is not None:
+        dh.copy_(dist, non_blocking=True)
+    torch.cuda.current_stream(keys.device).synchronize()
+    return ph.numpy(), (dh.numpy() if dh is not None else None)
 
 
 def keys_to_pairs(keys_host: np.ndarray) -> np.ndarray:

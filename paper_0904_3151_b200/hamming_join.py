@@ -104,8 +104,9 @@ def _codes_on_device(pool: BitStringPool, dev):
 def grouped_radix_sort(pool: BitStringPool, mask, chunk_bits: int = 16,
                        scratch: SortScratch | None = None, *, device=None):
     """``(perm, group_bounds)`` with equal masked keys contiguous
-    (hamming_join.py:275-297).  ``chunk_bits`` is validated for API parity;
-    it does not change the GPU grouping."""
+    (hamming_join.py:275-297): the reference's own permutation (first-seen
+    buckets of chunk_bits-wide counting passes, last chunk first), computed
+    on the GPU by eg_grouped_sort."""
     if pool.count == 0:
         raise ValueError("pool is empty")
     if scratch is None:
@@ -115,7 +116,7 @@ def grouped_radix_sort(pool: BitStringPool, mask, chunk_bits: int = 16,
     dev = engine.require_device(device)
     codes = _codes_on_device(pool, dev)
     perm, bounds = engine.grouped_sort(codes[0], pool.length, pool.block_bounds,
-                                       block_mask_bits(mask))
+                                       block_mask_bits(mask), chunk_bits)
     return perm.cpu().numpy().astype(np.int64), bounds.cpu().numpy()
 
 
@@ -142,11 +143,10 @@ def enumerate_pairs(pool: BitStringPool, d: int, chunk_bits: int = 16,
     scratch.check(n, chunk_bits)
     dev = engine.require_device(device)
     codes = _codes_on_device(pool, dev)
-    kk = engine.msm_plan(codes, pool.length, k, d, oversized_fraction)
-    bounds = pool.block_bounds if kk == k else block_partition(pool.length, kk)
-    reps, bits = engine.units_for([0], kk, d)
-    keys, info = engine.msm_pairs(codes, pool.length, bounds, d, reps, bits)
-    if kk == k:      # else the plan ruled the warning out on the reference blocks
+    keys, info = engine.msm_candidates(codes, pool.length, k, d,
+                                       oversized_fraction=oversized_fraction,
+                                       block_bounds=pool.block_bounds)
+    if info["reference_blocks"]:   # else the plan ruled the warning out on the reference blocks
         warn_oversized(info["max_group"], n, oversized_fraction)
     engine.sort_pair_keys(keys, n)
     return PairSet(engine.keys_to_pairs(keys.cpu().numpy()), assume_normalized=True)

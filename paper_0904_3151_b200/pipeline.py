@@ -107,8 +107,8 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
 
     Returns a dict of device tensors (``keys`` sorted uint64 pair keys,
     ``dist`` float64) plus counters and per-stage CUDA-event timings.
-    ``units`` (optional) restricts the (replicate, mask) units, used by the
-    multi-GPU driver; ``codes`` lets a caller pass pre-gathered codes.
+    ``units`` (optional) restricts the (replicate, mask) units to these
+    indices (sharding); ``codes`` lets a caller pass pre-gathered codes.
     ``blocks`` is the block count the units use (default: ``eg_msm_plan``'s
     choice; the pair set is the same for every count).
     """
@@ -141,17 +141,13 @@ def build_graph_device(x: torch.Tensor, params: MsmParams, *, metric: str = "cos
         flags_ready.record()
     ev[1].record()
     if blocks is None:
-        blocks = engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
+        blocks = engine.plan_blocks(codes, params.length, params.blocks, params.mismatch)
     if flags_ready is not None:
         flags_ready.synchronize()
         engine.raise_bad_rows(bad)
-    bounds = _bounds(params.length, blocks)
-    if units is None:
-        ureps, umasks = engine.units_for(range(params.replicates), blocks, params.mismatch)
-    else:
-        ureps, umasks = units
-    keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, ureps, umasks)
-    info["blocks"] = blocks
+    keys, info = engine.msm_candidates(
+        codes, params.length, params.blocks, params.mismatch, blocks=blocks,
+        select=None if units is None else (lambda total: units))
     ev[2].record()
     engine.sort_pair_keys(keys, n)
     ev[3].record()
@@ -183,39 +179,60 @@ def _event_timings(ev, t_host):
 
 def build_graph(data, params: MsmParams, *, threads: int | None = None, chunk_bits: int = 16,
                 normalize: bool = False, max_pool_bytes: int = 1 << 30,
-                metric: str = "cosine", device=None) -> NeighborGraph:
-    """Construct the eps-neighbour graph (pipeline.py:242-354) on a B200.
+                metric: str = "cosine", device=None, devices=None) -> NeighborGraph:
+    """Construct the eps-neighbour graph (pipeline.py:242-354) on B200s.
 
     Arguments follow the reference; ``threads`` and ``max_pool_bytes`` are
     accepted for compatibility (all replicate pools stay resident in HBM and
     the result is identical for any value), ``chunk_bits`` is validated.
-    New: ``metric`` ('cosine' | 'euclidean') and ``device``.  ``data`` may
-    also be a torch tensor (CPU, pinned, or already on the device).
+    New: ``metric`` ('cosine' | 'euclidean'), ``device`` (one GPU) and
+    ``devices`` (a count or a list of CUDA devices: the units are sharded
+    over them, distributed.build_on_devices; same result for any list).
+    ``data`` may also be a torch tensor (CPU, pinned, or on a device).
     """
     t0 = time.perf_counter()
     if not (1 <= chunk_bits <= 24):
         raise ValueError("chunk_bits must be in [1, 24]")
     _metric_id(metric)
-    dev = engine.require_device(device)
     if isinstance(data, VectorDataset):
         rows = data.vectors
     else:
         rows = data
     if normalize:
         rows = center_normalize(rows.cpu().numpy() if isinstance(rows, torch.Tensor) else rows).vectors
-    with torch.cuda.device(dev):
-        x = engine.as_device_rows(rows, dev)
-        n = x.shape[0]
-        if n == 0:
+    if devices is not None:
+        from .distributed import _device_list, build_on_devices
+        devs = _device_list(devices)
+        engine.require_device(devs[0])
+        if len(rows) == 0:
             raise DataError("cannot build a graph over an empty dataset")
-        out = build_graph_device(x, params, metric=metric)
-        keys = out["keys"].cpu().numpy()
-        dist = out["dist"].cpu().numpy()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        with torch.cuda.device(devs[0]):
+            ev[0].record()
+        out = build_on_devices(rows, params, metric, devs)
+        n = len(rows)
         info = out["info"]
-        if info["blocks"] == params.blocks:   # else the plan ruled the warning out
-            warn_oversized(info["max_group"], n, 0.25)
-        timings = _event_timings(out["events"], 0.0)
-    edges = EdgeList(engine.keys_to_pairs(keys), dist)
+        with torch.cuda.device(devs[0]):
+            ev[1].record()
+            ev[1].synchronize()
+            pairs, dist = engine.edges_to_host(out["keys"], out["dist"])
+        timings = {"project_s": 0.0, "enumerate_s": ev[0].elapsed_time(ev[1]) / 1e3,
+                   "dedup_s": 0.0, "sort_s": 0.0, "filter_s": 0.0}
+    else:
+        dev = engine.require_device(device)
+        with torch.cuda.device(dev):
+            x = engine.as_device_rows(rows, dev)
+            n = x.shape[0]
+            if n == 0:
+                raise DataError("cannot build a graph over an empty dataset")
+            out = build_graph_device(x, params, metric=metric)
+            info = out["info"]
+            pairs, dist = engine.edges_to_host(out["keys"], out["dist"])
+            timings = _event_timings(out["events"], 0.0)
+    if info.get("reference_blocks", info["blocks"] == params.blocks):
+        # else the plan ruled the warning out on the reference blocks
+        warn_oversized(info["max_group"], n, 0.25)
+    edges = EdgeList(pairs, dist)
     timings["total_s"] = time.perf_counter() - t0
     cand = info["emitted"]
     stats = GraphStats(

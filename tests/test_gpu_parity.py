@@ -60,26 +60,31 @@ def test_random_pools_match_reference(eg, manifest):
         np.testing.assert_array_equal(got.array, g[f"pairs_{c}"], err_msg=str(case))
 
 
-def test_grouped_sort_groups(eg, manifest):
+def test_grouped_sort_reference_permutation(eg, manifest):
+    """grouped_radix_sort returns the reference's exact permutation and group
+    bounds (first-seen counting passes, hamming_join.py:52-82, 275-297)."""
     g = golden("random_pools")
-    for case in manifest["random_pools"][:24]:
+    for case in manifest["random_pools"]:
         c = case["case"]
         pool = eg.BitStringPool(g[f"words_{c}"], case["length"]).partitioned(case["k"])
         perm, bounds = eg.grouped_radix_sort(pool, case["mask"])
-        ref_bounds = g[f"gbounds_{c}"]
-        assert sorted(perm.tolist()) == list(range(pool.count))
-        assert len(bounds) == len(ref_bounds)          # same number of groups
-        kept = eg.kept_word_mask(pool.length, pool.block_bounds, case["mask"])
-        keys = [tuple(int(v) for v in (pool.words[i] & kept)) for i in range(pool.count)]
-        seen = set()
-        for a, b in zip(bounds[:-1], bounds[1:]):
-            ks = {keys[i] for i in perm[a:b]}
-            assert len(ks) == 1
-            kk = ks.pop()
-            assert kk not in seen
-            seen.add(kk)
-        # same multiset of group sizes as the reference grouping
-        assert sorted(np.diff(bounds).tolist()) == sorted(np.diff(ref_bounds).tolist())
+        np.testing.assert_array_equal(perm, g[f"perm_{c}"], err_msg=str(case))
+        np.testing.assert_array_equal(bounds, g[f"gbounds_{c}"], err_msg=str(case))
+
+
+@pytest.mark.parametrize("chunk_bits", [1, 5, 8, 16, 24])
+def test_grouped_sort_chunk_bits_vs_oracle(eg, oracle, manifest, chunk_bits):
+    """Every chunk width gives the oracle's permutation (the order depends on
+    chunk_bits; the grouping does not)."""
+    g = golden("random_pools")
+    for case in manifest["random_pools"][:20]:
+        c = case["case"]
+        pool = eg.BitStringPool(g[f"words_{c}"], case["length"]).partitioned(case["k"])
+        perm, bounds = eg.grouped_radix_sort(pool, case["mask"], chunk_bits=chunk_bits)
+        wp, wb = oracle.grouped_radix_sort(pool.words, pool.length, pool.block_bounds,
+                                           case["mask"], chunk_bits)
+        np.testing.assert_array_equal(perm, wp, err_msg=str(case))
+        np.testing.assert_array_equal(bounds, wb, err_msg=str(case))
 
 
 def test_duplicates_and_oversized_warning(eg, caplog):
@@ -624,3 +629,82 @@ def test_radix_sort_kernels(eg, native_options, classic):
         order = np.argsort(keys, kind="stable")
         np.testing.assert_array_equal(t.cpu().numpy(), keys[order])
         np.testing.assert_array_equal(vals.cpu().numpy(), order.astype(np.int32))
+
+
+# --------------------------------------------------------------- boundary
+
+def test_build_graph_devices_invariance(eg):
+    """build_graph(devices=...) shards the units over the listed devices
+    (one process); the edge list is bit-identical for any device list
+    (mirror of the reference's thread-count contract,
+    tests/test_pipeline.py:130-135).  A repeated device runs its shards one
+    after another, which exercises the sharded path on one GPU."""
+    import torch
+    from paper_0904_3151_b200 import workloads
+    x = workloads.cfg3_points(30_000, planted_rows=3_000)
+    params = eg.MsmParams(0.05, 1e-6, 48, 3, 12, 3, 0)
+    one = eg.build_graph(x, params)
+    lists = [[0, 0], [0, 0, 0]]
+    if torch.cuda.device_count() > 1:
+        lists.append(torch.cuda.device_count())
+    for devs in lists:
+        many = eg.build_graph(x, params, devices=devs)
+        assert many.edge_list == one.edge_list, devs
+        assert many.stats.per_replicate_raw == one.stats.per_replicate_raw
+        assert many.stats.per_replicate_new == one.stats.per_replicate_new
+        assert many.stats.candidate_count == one.stats.candidate_count
+    bad = x.copy()
+    bad[20_001] = 0.0
+    with pytest.raises(eg.DataError, match="row 20001 has zero norm"):
+        eg.build_graph(bad, params, devices=[0, 0, 0])
+
+
+@pytest.mark.parametrize("length,k,d", [(300, 10, 2), (257, 70, 1), (200, 100, 2), (520, 8, 3)])
+def test_long_strings_and_many_blocks(eg, oracle, length, k, d):
+    """No length / block-count caps: strings longer than the kernels' 256
+    bits run on their first 256 bits and are filtered by the full codes,
+    k > 64 runs with at most 64 blocks; pair sets equal the oracle's
+    enumerate_pairs at the reference k (hamming_join.py:300-375)."""
+    rng = np.random.default_rng(length + k)
+    n = 3000
+    base = (rng.random((n // 4, length)) < 0.5).astype(np.uint8)
+    bits = base[rng.integers(0, base.shape[0], n)]
+    flips = rng.random((n, length)) < (1.5 / length)
+    bits = bits ^ flips.astype(np.uint8)
+    words = pack_bits(bits)
+    pool = eg.BitStringPool(words, length).partitioned(k)
+    got = eg.enumerate_pairs(pool, d).array
+    want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+    np.testing.assert_array_equal(got, want)
+    assert got.shape[0] > n // 4
+
+
+def test_lsh_only_long_strings(eg, oracle):
+    """build_graph_lsh_only at a small epsilon picks a length above 256 bits
+    (pipeline.py:357-408); the build equals the oracle's."""
+    from paper_0904_3151_b200 import workloads
+    x = workloads.cfg1_points(1_000, clusters=10)
+    g = eg.build_graph_lsh_only(x, 0.001, 1e-3)
+    assert g.params.length > 256 and g.params.replicates == 300
+    ref = oracle.build_graph(x, 0.001, g.params.length, 0, 1, 300, 0)
+    assert g.stats.per_replicate_raw == ref.per_replicate_raw
+    assert g.stats.per_replicate_new == ref.per_replicate_new
+    np.testing.assert_array_equal(g.edge_list.pairs, ref.pairs)
+
+
+def test_output_estimate_sizes_cold_calls(eg):
+    """The sampled output estimate (eg_msm_estimate_pairs) bounds the MSM
+    output of a cold call, so the capacity is right the first time (no
+    rerun of the units)."""
+    import torch
+    from paper_0904_3151_b200 import engine, workloads
+    engine._capacity_hint.clear()
+    x = workloads.cfg5_points(300_000, clusters=15_000)
+    params = eg.MsmParams(0.15, 1e-6, 64, 3, 16, 2, 0)
+    out = eg.build_graph_device(torch.from_numpy(x).cuda(), params, metric="euclidean")
+    info = out["info"]
+    assert info["reruns"] == 0
+    est, hi = engine.estimate_pairs(out["codes"], 3)
+    raw = sum(info["raw"])
+    assert 0.5 * raw <= est <= 2.0 * raw
+    assert hi >= raw
