@@ -158,7 +158,6 @@ def test_cfg5_two_million(eg, metric):
     x = workloads.cfg5_points(2_000_000, clusters=100_000)
     eps = rec["epsilon_cos"] if metric == "cosine" else 0.15
     _, out = build_device(eg, x, eps, 64, 16, 3, 2, metric=metric)
-    assert rec["edge_count"] == 19_932_408
     check_build(eg, out, rec, rec["epsilon_cos"], cosine=metric == "cosine",
                 per_rep_api=metric == "cosine")
     if metric == "euclidean":
