@@ -258,6 +258,17 @@ int eg_sort_pair_keys(uint64_t *d_keys, int64_t m, int64_t n, void *d_workspace,
 /* --------------------------------------------------------------------- */
 /* Stable compaction of keys by a byte flag (keeps input order).          */
 /* --------------------------------------------------------------------- */
+/* Merge of sorted runs (the ranks' sorted edge lists in the multi-GPU    */
+/* build): d_keys[h_offsets[0] .. h_offsets[runs]) holds `runs` ascending */
+/* runs (run r = [h_offsets[r], h_offsets[r+1])) with optional 64-bit     */
+/* payloads d_vals (distance bits); on return the whole range is sorted,  */
+/* stably (merge path, log2(runs) rounds).  Asynchronous.                 */
+/* --------------------------------------------------------------------- */
+size_t eg_merge_runs_workspace(int64_t m, int with_values);
+int eg_merge_runs(uint64_t *d_keys, uint64_t *d_vals, const int64_t *h_offsets,
+                  int32_t runs, void *d_workspace, size_t workspace_bytes, void *stream);
+
+/* --------------------------------------------------------------------- */
 size_t eg_compact_workspace(int64_t m);
 int eg_compact_keys(const uint64_t *d_keys, const uint8_t *d_flags, int64_t m,
                     uint64_t *d_out, int64_t *h_count, void *d_workspace,

@@ -82,6 +82,8 @@ def _declare(lib):
         "eg_sort_workspace": ([i64, I], sz),
         "eg_sort_keys": ([P, P, i64, i32, P, sz, P], I),
         "eg_sort_pair_keys": ([P, i64, i64, P, sz, P], I),
+        "eg_merge_runs_workspace": ([i64, I], sz),
+        "eg_merge_runs": ([P, P, P, i32, P, sz, P], I),
         "eg_compact_workspace": ([i64], sz),
         "eg_compact_keys": ([P, P, i64, P, P, P, sz, P], I),
         "eg_verify_workspace": ([i64], sz),

@@ -1263,6 +1263,65 @@ int eg_sort_pair_keys(uint64_t *d_keys, int64_t m, int64_t n, void *d_workspace,
   return radix_sort(d_keys, nullptr, m, shifts, np, ar, st);
 }
 
+// ----------------------------------------------------------- merge runs
+size_t eg_merge_runs_workspace(int64_t m, int with_values) {
+  return ws_bytes(m, 8) * (with_values ? 2 : 1) + 1024;
+}
+
+int eg_merge_runs(uint64_t *d_keys, uint64_t *d_vals, const int64_t *h_offsets, int32_t runs,
+                  void *d_workspace, size_t workspace_bytes, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (runs < 1 || !h_offsets) return arg_error("eg_merge_runs: need >= 1 run");
+  const int64_t m = h_offsets[runs] - h_offsets[0];
+  if (m < 0) return arg_error("eg_merge_runs: offsets must increase");
+  for (int r = 0; r < runs; ++r)
+    if (h_offsets[r + 1] < h_offsets[r]) return arg_error("eg_merge_runs: offsets must increase");
+  if (runs == 1 || m == 0) return EG_OK;
+  Arena ar(d_workspace, workspace_bytes);
+  uint64_t *tk = ar.take<uint64_t>(m);
+  uint64_t *tv = d_vals ? ar.take<uint64_t>(m) : nullptr;
+  if (!tk || (d_vals && !tv)) {
+    set_error("eg_merge_runs: workspace too small");
+    return EG_ERR_WORKSPACE;
+  }
+  std::vector<int64_t> off(h_offsets, h_offsets + runs + 1);
+  for (int64_t &o : off) o -= h_offsets[0];
+  uint64_t *src = d_keys, *srcv = d_vals, *dst = tk, *dstv = tv;
+  while (off.size() > 2) {   // one round: merge neighbouring runs pairwise
+    std::vector<int64_t> next;
+    for (size_t r = 0; r + 1 < off.size(); r += 2) {
+      next.push_back(off[r]);
+      if (r + 2 < off.size()) {
+        const int64_t na = off[r + 1] - off[r], nb = off[r + 2] - off[r + 1];
+        const int64_t tot = na + nb;
+        const unsigned grid = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>((tot + MP_NT * MP_IT - 1) / (MP_NT * MP_IT),
+                                 (int64_t)num_sms() * 16));
+        EG_PROF(PC_SORT_DOWNSWEEP, st);
+        k_merge_path<<<grid, MP_NT, 0, st>>>(src + off[r], srcv ? srcv + off[r] : nullptr, na,
+                                             src + off[r + 1], srcv ? srcv + off[r + 1] : nullptr,
+                                             nb, dst + off[r], dstv ? dstv + off[r] : nullptr);
+      } else {   // odd run out: carried over
+        const int64_t len = off[r + 1] - off[r];
+        EG_CUDA_TRY(cudaMemcpyAsync(dst + off[r], src + off[r], len * 8, cudaMemcpyDeviceToDevice, st));
+        if (srcv)
+          EG_CUDA_TRY(cudaMemcpyAsync(dstv + off[r], srcv + off[r], len * 8,
+                                      cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    next.push_back(off.back());
+    off.swap(next);
+    std::swap(src, dst);
+    std::swap(srcv, dstv);
+  }
+  EG_LAUNCH_CHECK();
+  if (src != d_keys) {
+    EG_CUDA_TRY(cudaMemcpyAsync(d_keys, src, m * 8, cudaMemcpyDeviceToDevice, st));
+    if (d_vals) EG_CUDA_TRY(cudaMemcpyAsync(d_vals, srcv, m * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return EG_OK;
+}
+
 // ------------------------------------------------------------ compaction
 size_t eg_compact_workspace(int64_t m) { return compact_workspace(m); }
 

@@ -579,4 +579,43 @@ __host__ inline int compact(const uint64_t *keys, const V *vals, const uint8_t *
   return EG_OK;
 }
 
+// ------------------------------------------------------------ merge runs
+// Two sorted key runs (+ 64-bit payloads) -> one, by merge path: every
+// thread binary-searches its output diagonal, then merges MP_IT outputs
+// sequentially (ties: a before b, so the merge is stable).  The multi-GPU
+// build merges the ranks' sorted edge runs with log2(ranks) rounds of this
+// instead of re-sorting them.
+constexpr int MP_IT = 8, MP_NT = 256;
+__global__ void __launch_bounds__(MP_NT) k_merge_path(const uint64_t *__restrict__ a,
+                                                      const uint64_t *__restrict__ av, int64_t na,
+                                                      const uint64_t *__restrict__ b,
+                                                      const uint64_t *__restrict__ bv, int64_t nb,
+                                                      uint64_t *__restrict__ out,
+                                                      uint64_t *__restrict__ outv) {
+  const int64_t total = na + nb;
+  for (int64_t d0 = ((int64_t)blockIdx.x * MP_NT + threadIdx.x) * MP_IT; d0 < total;
+       d0 += (int64_t)gridDim.x * MP_NT * MP_IT) {
+    // i = number of a-elements among the first d0 outputs
+    int64_t lo = d0 > nb ? d0 - nb : 0, hi = d0 < na ? d0 : na;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (a[mid] <= b[d0 - mid - 1]) lo = mid + 1; else hi = mid;
+    }
+    int64_t i = lo, j = d0 - lo;
+    const int64_t end = d0 + MP_IT < total ? d0 + MP_IT : total;
+    for (int64_t o = d0; o < end; ++o) {
+      const bool take_a = j >= nb || (i < na && a[i] <= b[j]);
+      if (take_a) {
+        out[o] = a[i];
+        if (outv) outv[o] = av[i];
+        ++i;
+      } else {
+        out[o] = b[j];
+        if (outv) outv[o] = bv[j];
+        ++j;
+      }
+    }
+  }
+}
+
 }  // namespace eg

@@ -9,13 +9,13 @@ with disjoint outputs and no cross-rank dedup.
        computes its row norms and bad-row flags in the same pass
        (eg_project_rows); the flags are MIN-reduced over the ranks;
     2. codes and norms are all-gathered over NVLink (NCCL all_gather);
-    3. the block count is planned on the gathered codes (eg_msm_plan,
-       deterministic, so every rank agrees without a collective), units are
+    3. rank 0 plans the block count on the gathered codes (eg_msm_plan) and
+       broadcasts it (8 bytes), units are
        assigned cyclically (unit u -> rank u % world), each rank
        runs eg_msm_pairs on its units, sorts and verifies its candidates
        (rows are resident on every rank for the verify gathers);
-    4. per-rank sorted edge runs are gathered to rank 0 and merged by one
-       key sort.
+    4. per-rank sorted edge runs are gathered to rank 0 only and merged
+       there (merge path, log2(ranks) rounds; eg_merge_runs).
 
 The collective/merge logic is written against a small ``ops`` interface so
 the same code runs with the CUDA ops (``DeviceOps``) and, in tests, with the
@@ -79,18 +79,23 @@ class DeviceOps:
         from .pipeline import _metric_id
         return engine.verify(x, norms, keys, _metric_id(metric), eps)
 
-    def merge(self, keys, dists, n):
-        """Sort concatenated per-rank runs by key, carrying distances."""
+    def merge_runs(self, keys, dists, offsets):
+        """Concatenated sorted per-rank runs (run r = keys[offsets[r]:
+        offsets[r+1]]) -> one sorted run, distances carried (eg_merge_runs:
+        log2(runs) merge-path rounds instead of a re-sort)."""
         m = keys.numel()
-        if m <= 1:
+        if m <= 1 or len(offsets) <= 2:
             return keys, dists
-        idx = torch.arange(m, dtype=torch.int32, device=keys.device)
         from . import _native
         lib = _native.lib()
-        ws = engine._ws(lib.eg_sort_workspace(m, 1), keys.device)
-        _native.check(lib.eg_sort_keys(keys.data_ptr(), idx.data_ptr(), m, 64, ws.data_ptr(),
-                                       ws.numel(), engine._stream(keys.device)), "merge")
-        return keys, dists.index_select(0, idx.long())
+        keys = keys.contiguous()
+        vals = dists.contiguous().view(torch.int64)
+        off = np.ascontiguousarray(offsets, dtype=np.int64)
+        ws = engine._ws(lib.eg_merge_runs_workspace(m, 1), keys.device)
+        _native.check(lib.eg_merge_runs(keys.data_ptr(), vals.data_ptr(), off.ctypes.data,
+                                        len(offsets) - 1, ws.data_ptr(), ws.numel(),
+                                        engine._stream(keys.device)), "merge_runs")
+        return keys, vals.view(torch.float64)
 
 
 def _all_gather_rows(t: torch.Tensor, per: int, world: int) -> torch.Tensor:
@@ -129,24 +134,37 @@ def global_bad_rows(bad_local: torch.Tensor, row0: int) -> torch.Tensor:
 
 
 def gather_edges(keys, dists, world, rank, ops, n):
-    """Per-rank sorted edge runs -> merged sorted edges on rank 0."""
+    """Per-rank sorted edge runs -> merged sorted edges on rank 0 only: the
+    run lengths are all-gathered (8 bytes per rank), the runs themselves go
+    to rank 0 alone (one gather, keys and distance bits together), and rank
+    0 merges the sorted runs (ops.merge_runs) instead of re-sorting."""
     cnt = torch.tensor([keys.numel()], dtype=torch.int64, device=keys.device)
     counts = [torch.zeros_like(cnt) for _ in range(world)]
     tdist.all_gather(counts, cnt)
     counts = [int(c.item()) for c in counts]
     mx = max(counts) if counts else 0
     if mx == 0:
-        return keys[:0], dists[:0]
-    # keys and distance bits travel together: one all-gather
+        return (keys[:0], dists[:0]) if rank == 0 else (None, None)
     kd = torch.stack([keys, dists.contiguous().view(torch.int64)], dim=1)
     kp = torch.cat([kd, kd.new_zeros((mx - keys.numel(), 2))])
-    ka = kp.new_empty((mx * world, 2))
-    tdist.all_gather_into_tensor(ka, kp)
+    parts = [kp.new_empty((mx, 2)) for _ in range(world)] if rank == 0 else None
+    tdist.gather(kp, gather_list=parts, dst=0)
     if rank != 0:
         return None, None
-    ks = torch.cat([ka[r * mx:r * mx + counts[r], 0] for r in range(world)])
-    ds = torch.cat([ka[r * mx:r * mx + counts[r], 1] for r in range(world)])
-    return ops.merge(ks.contiguous(), ds.contiguous().view(torch.float64), n)
+    ks = torch.cat([parts[r][:counts[r], 0] for r in range(world)]).contiguous()
+    ds = torch.cat([parts[r][:counts[r], 1] for r in range(world)]).contiguous()
+    offsets = [0]
+    for c in counts:
+        offsets.append(offsets[-1] + c)
+    return ops.merge_runs(ks, ds.view(torch.float64), offsets)
+
+
+def broadcast_int(value, rank: int, device) -> int:
+    """Rank 0's integer to every rank (one 8-byte broadcast)."""
+    t = torch.tensor([int(value) if rank == 0 else 0], dtype=torch.int64, device=device)
+    if tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1:
+        tdist.broadcast(t, src=0)
+    return int(t.item())
 
 
 def build_step(x, params, metric: str, world: int, rank: int, ops=None,
@@ -178,7 +196,8 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
         codes_s = ops.project(xs, norms_s, params)
         codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
     from math import comb
-    blocks = ops.plan(codes, params)
+    # one plan (rank 0), one 8-byte broadcast: every rank runs the same units
+    blocks = broadcast_int(ops.plan(codes, params) if rank == 0 else 0, rank, codes.device)
     units = my_units(params.replicates * comb(blocks, max(0, params.mismatch)), world, rank)
     keys, info = ops.candidates(codes, params, units, blocks)
     info = dict(info, blocks=blocks)
@@ -197,6 +216,8 @@ def hamming_step(codes, params, world: int, rank: int):
     if world > 1:
         dummy = torch.zeros(keys.numel(), dtype=torch.float64, device=keys.device)
         keys, _ = gather_edges(keys, dummy, world, rank, DeviceOps(), n)
+        if rank != 0:
+            keys = None
     return {"keys": keys, "dist": None, "info": info}
 
 
@@ -334,7 +355,10 @@ def build_on_devices(rows, params, metric: str, devices):
         dev = devs[0]
         ks = torch.cat([p[0].to(dev) for p in parts])
         ds = torch.cat([p[1].to(dev) for p in parts])
-        return ops.merge(ks, ds, n)
+        offsets = [0]
+        for p in parts:
+            offsets.append(offsets[-1] + p[0].numel())
+        return ops.merge_runs(ks, ds, offsets)
     keys, dist = on(devs[0], merge)
     infos = [p[2] for p in parts if p[2] is not None]
     reps = params.replicates

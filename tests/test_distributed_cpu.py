@@ -98,9 +98,18 @@ class OracleOps:
         keep = d <= eps
         return keys[torch.from_numpy(keep)], torch.from_numpy(d[keep])
 
-    def merge(self, keys, dists, n):
-        order = torch.argsort(keys)
-        return keys[order], dists[order]
+    def merge_runs(self, keys, dists, offsets):
+        """k-way merge of the sorted runs (heapq), like eg_merge_runs."""
+        import heapq
+        runs = []
+        for r in range(len(offsets) - 1):
+            a, b = offsets[r], offsets[r + 1]
+            k = keys[a:b].tolist()
+            assert k == sorted(k), "rank runs must arrive sorted"
+            runs.append(list(zip(k, dists[a:b].tolist())))
+        merged = list(heapq.merge(*runs))
+        return (torch.tensor([m[0] for m in merged], dtype=torch.int64),
+                torch.tensor([m[1] for m in merged], dtype=torch.float64))
 
 
 def _worker(rank, world, port, out_path, blocks=None):

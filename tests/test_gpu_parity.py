@@ -708,3 +708,26 @@ def test_output_estimate_sizes_cold_calls(eg):
     raw = sum(info["raw"])
     assert 0.5 * raw <= est <= 2.0 * raw
     assert hi >= raw
+
+
+@pytest.mark.parametrize("runs", [1, 2, 3, 8, 13])
+def test_merge_runs_kernel(eg, runs):
+    """eg_merge_runs (merge path): sorted runs of ragged sizes (some empty)
+    with payloads -> one sorted run, payloads following their keys."""
+    import torch
+    from paper_0904_3151_b200.distributed import DeviceOps
+    rng = np.random.default_rng(runs)
+    sizes = rng.integers(0, 50_000, runs)
+    sizes[0] = 0 if runs > 2 else sizes[0]
+    allk = rng.choice(1 << 40, int(sizes.sum()), replace=False).astype(np.int64)
+    parts, offs = [], [0]
+    for r, sz in enumerate(sizes):
+        parts.append(np.sort(allk[offs[-1]:offs[-1] + sz]))
+        offs.append(offs[-1] + int(sz))
+    keys = np.concatenate(parts) if parts else np.empty(0, np.int64)
+    dist = (keys.astype(np.float64) * 0.5)
+    k, d = DeviceOps().merge_runs(torch.from_numpy(keys).cuda(), torch.from_numpy(dist).cuda(),
+                                  offs)
+    order = np.argsort(keys, kind="stable")
+    np.testing.assert_array_equal(k.cpu().numpy(), keys[order])
+    np.testing.assert_array_equal(d.cpu().numpy(), dist[order])
