@@ -123,9 +123,10 @@ int eg_project_rows(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
 /* writes its raw fp32 accumulator (n x replicates*length) to d_buf, so the */
 /* tests can measure the worst error against the exact fp64 product.       */
 void eg_debug_set_tc_dump(float *d_buf);
-/* Debug: MSM bucket counters [buckets, rows, candidates, groups, grouped
- * rows, pair visits] (zero unless built with -DEG_MSM_STATS=1). */
-int eg_debug_msm_stats(unsigned long long *out8, int reset);
+/* Debug: MSM counters (zero unless built with -DEG_MSM_STATS=1):          */
+/* [0..5] buckets, rows, filter candidates, groups, grouped rows, pair    */
+/* visits of the hash-table tiers; [8..15] reserved (zero).               */
+int eg_debug_msm_stats(unsigned long long *out16, int reset);
 
 /* --------------------------------------------------------------------- */
 /* Multiple-sorting-method enumeration over (replicate, mask) units.      */

@@ -65,6 +65,7 @@ def _declare(lib):
         "eg_profile_read": ([P, P, I], I),
         "eg_row_stats": ([P, I, i64, i32, P, P, P], I),
         "eg_debug_set_tc_dump": ([P], None),
+        "eg_debug_msm_stats": ([P, I], I),
         "eg_project_workspace": ([i64, i32, i32, i32], sz),
         "eg_project": ([P, I, i64, i32, P, P, P, i32, i32, P, P, sz, P, P], I),
         "eg_project_rows": ([P, I, i64, i32, P, P, P, P, i32, i32, P, P, sz, P, P], I),

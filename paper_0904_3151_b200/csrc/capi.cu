@@ -473,9 +473,10 @@ static float *g_tc_debug = nullptr;
 extern "C" void eg_debug_set_tc_dump(float *d_buf) { g_tc_debug = d_buf; }
 // Debug: copy (and optionally reset) the MSM bucket counters (all zero
 // unless the library was compiled with -DEG_MSM_STATS=1).
-extern "C" int eg_debug_msm_stats(unsigned long long *out8, int reset) {
-  if (cudaMemcpyFromSymbol(out8, eg::g_msm_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
+extern "C" int eg_debug_msm_stats(unsigned long long *out16, int reset) {
+  if (cudaMemcpyFromSymbol(out16, eg::g_msm_stats, sizeof(unsigned long long) * 8) != cudaSuccess)
     return EG_ERR_CUDA;
+  for (int i = 8; i < 16; ++i) out16[i] = 0;
   if (reset) {
     static const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (cudaMemcpyToSymbol(eg::g_msm_stats, z, sizeof(z)) != cudaSuccess) return EG_ERR_CUDA;

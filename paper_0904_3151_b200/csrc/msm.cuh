@@ -38,7 +38,10 @@ constexpr int MSM_IPT = 8;              // items per thread, hist/scatter
 constexpr int MSM_NT = 1024;            // threads, hist/scatter
 constexpr int MSM_TILE = MSM_IPT * MSM_NT;
 constexpr int MSM_SC_NT = 512;          // threads, scatter (16 items each)
-constexpr int MSM_TARGET = 3072;        // default target mean bucket size (tuned on cfg3)
+#ifndef EG_MSM_TARGET
+#define EG_MSM_TARGET 3072
+#endif
+constexpr int MSM_TARGET = EG_MSM_TARGET;   // target mean bucket size (tuned on cfg3)
 constexpr int MSM_SPILL_T = 128;        // spill tile edge
 constexpr int MSM_MAX_LGB = 14;         // at most 16384 buckets per unit
 constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to this B
@@ -932,9 +935,12 @@ struct SmallCfg {               // one CTA per bucket, several CTAs per SM
   static constexpr int MIN_CTAS = EG_SMALL_MINCTAS;
   static constexpr int MDIV = EG_SMALL_MDIV;
 };
+#ifndef EG_MEDIUM_CAP
+#define EG_MEDIUM_CAP 4096
+#endif
 template <int W>
 struct MediumCfg {
-  static constexpr int CAP = W <= 2 ? 4096 : 2048;
+  static constexpr int CAP = W <= 2 ? EG_MEDIUM_CAP : EG_MEDIUM_CAP / 2;
   static constexpr int NT = 512;
 };
 

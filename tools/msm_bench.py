@@ -59,3 +59,9 @@ print(f"{args.config} blocks={blocks} units={len(reps)} msm_ms min={min(times):.
       f"med={sorted(times)[len(times) // 2]:.3f} keys={keys.numel()} raw={info['raw']} "
       f"new={info['new']} max_group={info['max_group']} digest={dig}")
 print("  classes:", {k: round(v['ms'] / len(times), 3) for k, v in p.items()})
+if os.environ.get("EG_STATS"):
+    import ctypes
+    st = (ctypes.c_ulonglong * 16)()
+    rc = _native.lib().eg_debug_msm_stats(ctypes.addressof(st), 1)
+    assert rc == 0, rc
+    print("  stats (all iterations):", list(st))
