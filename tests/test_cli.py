@@ -47,7 +47,7 @@ def test_auto_params_match_reference(fx):
                r.cap_applied, r.achieved_bound]
         assert got[1:6] == case["report"][1:6]
         assert got[0] == pytest.approx(case["report"][0], rel=1e-15)
-        assert got[6] == pytest.approx(case["report"][6], rel=1e-9)
+        assert got[6] == case["report"][6]      # bit-identical (edge-file metadata)
 
 
 def test_usage_errors_exit_1(tmp_path):
