@@ -47,7 +47,11 @@ for it in range(args.iters + 2):
         prof.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, reps, masks)
+    if os.environ.get("EG_RAW_PAIRS"):
+        keys, info = engine.msm_pairs(codes, params.length, bounds, params.mismatch, reps, masks)
+    else:   # the build's path (balanced bit view when the plan changed the blocks)
+        keys, info = engine.msm_candidates(codes, params.length, params.blocks,
+                                           params.mismatch, blocks=blocks)
     e1.record()
     torch.cuda.synchronize()
     if it >= 2:
