@@ -600,7 +600,10 @@ static int project_impl(const void *d_x, int x_is_f64, int64_t n, int32_t dim, d
     const int64_t ntiles = (n + TC_M - 1) / TC_M;
     const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)num_sms());
     const int h16_no = 2;
-    const int h16_npad = npad;
+#ifndef EG_H16_NPAD_MIN
+#define EG_H16_NPAD_MIN 0   // experiments: pad the direction columns (MMA N) to at least this
+#endif
+    const int h16_npad = std::max(npad, EG_H16_NPAD_MIN);
     const bool h16 = tma_ok && path != 2 && h16_fits(h16_npad, h16_no);
     if (h16) {
       // kind::f16 (2-term fp16 splits): the production path for fp32 rows

@@ -149,4 +149,4 @@ def enumerate_pairs(pool: BitStringPool, d: int, chunk_bits: int = 16,
     if info["reference_blocks"]:   # else the plan ruled the warning out on the reference blocks
         warn_oversized(info["max_group"], n, oversized_fraction)
     engine.sort_pair_keys(keys, n)
-    return PairSet(engine.keys_to_pairs(keys.cpu().numpy()), assume_normalized=True)
+    return PairSet(engine.edges_to_host(keys, None)[0], assume_normalized=True)
