@@ -513,57 +513,74 @@ def main():
                              "tcgen05 fp16 screen + exact fp64 verify), untimed"}
 
     # ------------------------------------------------------------ roofline
+    # Every stage against its own bound with the SURVEY 8(d) algorithmic
+    # bytes; "roofline" is the stage with the largest time (the dominant
+    # kernel), the others are in roofline["other_stages"].
     peak, peak_kind = peaks()
     counts = distributed.last_counts(last) or {}
     blocks = counts.get("blocks") or cfg.blocks
     units_total = cfg.replicates * math.comb(blocks, cfg.mismatch)
     units_mine = len(distributed.my_units(units_total, world, rank))
-    stage = kprof.get("msm_stage", {"ms": 0.0, "count": 0})
-    roof = None
-    if stage["count"]:
-        # one "launch" = one eg_msm_pairs call: every (replicate, mask) unit
-        # of the build through hist / scan / scatter / group / tiers
-        units_per_launch = units_mine
-        avg_ms = stage["ms"] / stage["count"]
-        alg = sort_bytes_per_unit(n, cfg, blocks) * units_per_launch
-        achieved = alg / (avg_ms / 1e3) / 1e9
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "r1_traffic_planned.json")) as f:
-                tr = json.load(f).get(args.config)
-            if tr and tr.get("blocks", cfg.blocks) == blocks:
-                # measured DRAM bytes per 16-unit batch, scaled to the launch
-                traffic = tr["msm_batch_dram_bytes"] * units_per_launch / tr["units_per_batch"]
-        except Exception:
-            traffic = None
-        roof = {"kernel": "eg_msm_pairs: MSM unit pipeline (hist+scan+scatter+group+tiers) "
-                          "over all units of the build",
-                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg, blocks), "blocks": blocks,
-                "units_per_launch": units_per_launch, "avg_launch_ms": avg_ms}
-        # the same B_sort definition at the reference's own block count
-        # (independent of the kernel used; the planned count
-        # above is the conservative figure)
-        ref_units = cfg.replicates * math.comb(cfg.blocks, cfg.mismatch)
-        ref_units_mine = len(distributed.my_units(ref_units, world, rank))
-        ach_ref = sort_bytes_per_unit(n, cfg) * ref_units_mine / (avg_ms / 1e3) / 1e9
-        roof["ref_blocks"] = {"blocks": cfg.blocks, "units": ref_units_mine,
-                              "alg_bytes_per_unit": sort_bytes_per_unit(n, cfg),
-                              "achieved": ach_ref, "frac": ach_ref / peak}
-    stage_ms = {k: v["ms"] / args.steps for k, v in kprof.items()}
-    # other stages against their own bounds (SURVEY 8(d) byte definitions)
-    other = {}
-    if not hamming and "project" in kprof and kprof["project"]["count"]:
+    traffic_tab = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_traffic.json")) as f:
+            traffic_tab = json.load(f).get(args.config, {})
+    except Exception:
+        traffic_tab = {}
+
+    def entry(name, kernel, cls, alg_bytes, extra=None):
+        rec = kprof.get(cls, {"ms": 0.0, "count": 0})
+        if not rec["count"] or not alg_bytes:
+            return None
+        avg_ms = rec["ms"] / rec["count"]
+        achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+        tr = traffic_tab.get(name)
+        traffic = tr.get("dram_bytes_per_launch") if tr and tr.get("n") == n else None
+        out = {"stage": name, "kernel": kernel, "bound": "hbm", "achieved": achieved,
+               "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+               "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+               "avg_launch_ms": avg_ms}
+        out.update(extra or {})
+        return out
+
+    stages = {}
+    m_cand = int(counts.get("candidates") or 0)
+    m_edges = int(counts.get("edges") or 0)
+    stages["msm"] = entry(
+        "msm", "eg_msm_pairs: MSM unit pipeline (hist+scan+scatter+group+tiers) over the "
+        "build's units", "msm_stage", sort_bytes_per_unit(n, cfg, blocks) * units_mine,
+        {"alg_bytes_per_unit": sort_bytes_per_unit(n, cfg, blocks), "blocks": blocks,
+         "units_per_launch": units_mine,
+         "units_definition": "B_sort = n (8W + P 2 (kb + 4)), kb = P = ceil(kappa/8) at the "
+                             "planned block count"})
+    npass = 2 * -(-max(1, (n - 1).bit_length()) // 8)
+    stages["sort"] = entry(
+        "sort", "eg_sort_pair_keys: onesweep LSD over the candidate keys", "sort_stage",
+        (2 * npass + 1) * 8 * m_cand,
+        {"keys": m_cand, "passes": npass,
+         "definition": "one histogram read + per pass 8 B read + 8 B written per key"})
+    if not hamming:
+        dim = data.shape[1]
+        stages["verify"] = entry(
+            "verify", "eg_verify: exact fp64 distances of the sorted candidates + compaction",
+            "verify_stage", 8 * m_cand + 8 * dim * m_cand + 16 * m_edges,
+            {"candidates": m_cand, "edges": m_edges,
+             "definition": "8C + 8DC + 16E (SURVEY 8(d))"})
         W = max(1, -(-cfg.length // 64))
-        pb = 4 * n * data.shape[1] + 8 * n + 8 * n * cfg.replicates * W
-        pms = kprof["project"]["ms"] / kprof["project"]["count"]
-        other["projection"] = {"kernel": "k_project_h16 (tcgen05 kind::f16, fused norms)",
-                               "bound": "hbm", "alg_bytes": pb, "avg_launch_ms": pms,
-                               "achieved": pb / (pms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
-                               "frac": pb / (pms / 1e3) / 1e9 / peak}
-    if roof is not None and other:
-        roof["other_stages"] = other
+        stages["projection"] = entry(
+            "projection", "k_project_h16: tcgen05 kind::f16 projection, fused norms", "project",
+            4 * n * dim + 8 * n + 8 * n * cfg.replicates * W,
+            {"definition": "4nD + 8n + 8nrW"})
+    stages = {k: v for k, v in stages.items() if v is not None}
+    roof = None
+    if stages:
+        dom = max(stages, key=lambda k: stages[k]["avg_launch_ms"])
+        roof = dict(stages[dom])
+        roof["other_stages"] = {k: v for k, v in stages.items() if k != dom}
+    # per-class device ms per step; the MSM's internal classes are left out
+    # (they run on three streams and their events include cross-stream waits)
+    stage_ms = {k: v["ms"] / args.steps for k, v in kprof.items()
+                if not k.startswith("msm_") or k == "msm_stage"}
 
     # -------------------------------------------------------- cpu baseline
     cpu = None
@@ -586,6 +603,17 @@ def main():
                "sample": f"{args.config} generator at n={xs.shape[0]} rows, full params, "
                          f"C oracle port (oracle/), {sec:.1f} s"}
 
+    # the Gaussian directions are drawn on the host once per (length, dim,
+    # seed, replicates) and kept on the device (engine.device_directions);
+    # the reference redraws them per call -- the draw's cost, measured here
+    # untimed, is what the timed steps do not repeat
+    draw_ms = None
+    if not hamming:
+        from paper_0904_3151_b200 import engine as _eng
+        t0 = time.perf_counter()
+        for h in range(1, cfg.replicates + 1):
+            _eng.directions(cfg.length, data.shape[1], cfg.seed, h)
+        draw_ms = (time.perf_counter() - t0) * 1e3
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -597,6 +625,7 @@ def main():
             "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
             "cpu_baseline": cpu, "stage_ms": stage_ms, "quality": quality,
             "counts": distributed.last_counts(last),
+            "direction_draw_ms_untimed": draw_ms,
             "parity": parity_vs_reference(args.config, last, labels, n),
         }
         print(json.dumps(out), flush=True)

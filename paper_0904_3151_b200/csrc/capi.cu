@@ -49,7 +49,7 @@ static std::vector<cudaEvent_t> g_event_pool;
 static const char *g_prof_names[PC_COUNT] = {
     "row_stats", "project", "fixup", "msm_hist", "msm_scan", "msm_scatter", "msm_group",
     "msm_spill", "msm_batch", "sort_upsweep", "scan", "sort_downsweep", "verify", "compact",
-    "misc", "msm_stage"};
+    "misc", "msm_stage", "sort_stage", "verify_stage"};
 
 static cudaEvent_t take_event() {
   if (!g_event_pool.empty()) {
@@ -1051,7 +1051,7 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   }
   int rc = EG_OK;
   {
-    EG_PROF(PC_MSM_STAGE, st);
+    EG_PROF_GROUP(PC_MSM_STAGE, st);
     switch (W) {
       case 1: rc = msm_run<1>(sets, lay, batches, st); break;
       case 2: rc = msm_run<2>(sets, lay, batches, st); break;
@@ -1264,6 +1264,7 @@ int eg_sort_pair_keys(uint64_t *d_keys, int64_t m, int64_t n, void *d_workspace,
   int shifts[8];
   int np = pair_key_shifts(n, shifts);
   Arena ar(d_workspace, workspace_bytes);
+  EG_PROF_GROUP(PC_SORT_STAGE, st);
   return radix_sort(d_keys, nullptr, m, shifts, np, ar, st);
 }
 
@@ -1356,6 +1357,7 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   double *dist = ar.take<double>(m);
   unsigned long long *bad = ar.take<unsigned long long>(1);
   if (!flags || !dist || !bad) return EG_ERR_WORKSPACE;
+  EG_PROF_GROUP(PC_VERIFY_STAGE, st);
   EG_CUDA_TRY(cudaMemsetAsync(bad, 0xff, 8, st));
   unsigned grid = (unsigned)std::min<int64_t>((m + 7) / 8, (int64_t)num_sms() * 64);
   {

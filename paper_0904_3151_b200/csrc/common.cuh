@@ -31,7 +31,7 @@ void set_error(const char *fmt, ...);
 enum ProfClass {
   PC_ROW_STATS, PC_PROJECT, PC_FIXUP, PC_MSM_HIST, PC_MSM_SCAN, PC_MSM_SCATTER, PC_MSM_GROUP,
   PC_MSM_SPILL, PC_MSM_BATCH, PC_SORT_UPSWEEP, PC_SCAN, PC_SORT_DOWNSWEEP, PC_VERIFY,
-  PC_COMPACT, PC_MISC, PC_MSM_STAGE, PC_COUNT
+  PC_COMPACT, PC_MISC, PC_MSM_STAGE, PC_SORT_STAGE, PC_VERIFY_STAGE, PC_COUNT
 };
 void prof_begin(int cls, cudaStream_t st, int launches);
 void prof_end(int cls, cudaStream_t st);
