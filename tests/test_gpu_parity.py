@@ -756,7 +756,7 @@ def test_cluster_ordered_verify_identical(eg, native_options, metric):
     np.testing.assert_array_equal(res[0][0], res[1][0])
     np.testing.assert_array_equal(res[0][1], res[1][1])
     bad = cand.clone()
-    bad[5] = ((200_000 + 5) << 32) | 3
+    bad[5] = (1 << 40) | 3
     for vr in (0, 1):
         with _native.options(verify_runs=vr):
             with pytest.raises(IndexError):
