@@ -284,11 +284,6 @@ int eg_compact_keys(const uint64_t *d_keys, const uint8_t *d_flags, int64_t m,
 /* Keys must satisfy i, j < n (checked; EG_ERR_ARG on violation).         */
 /* --------------------------------------------------------------------- */
 size_t eg_verify_workspace(int64_t m);
-/* Workspace that also allows the cluster-ordered path for n rows (large  */
-/* clustered outputs: the (i, j)-sorted candidates are verified run by    */
-/* run in the order of each run's first j, so rows of one cluster share   */
-/* their j rows in L2; same per-pair arithmetic, same results).           */
-size_t eg_verify_workspace_n(int64_t m, int64_t n);
 int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim,
               const double *d_norms, const uint64_t *d_keys, int64_t m,
               int32_t metric, double eps, uint64_t *d_out_keys, double *d_out_dist,

@@ -88,7 +88,6 @@ def _declare(lib):
         "eg_compact_workspace": ([i64], sz),
         "eg_compact_keys": ([P, P, i64, P, P, P, sz, P], I),
         "eg_verify_workspace": ([i64], sz),
-        "eg_verify_workspace_n": ([i64, i64], sz),
         "eg_verify": ([P, I, i64, i32, P, P, i64, i32, dbl, P, P, P, P, sz, P], I),
         "eg_bf_cosine_workspace": ([i64, i32], sz),
         "eg_bf_cosine_candidates": ([P, I, i64, i32, P, dbl, P, i64, P, P, sz, P], I),

@@ -361,7 +361,6 @@ int eg_set_option(const char *name, long long value) {
   else if (!strcmp(name, "msm_streams") && (value == 1 || value == 2)) o.msm_streams = (int)value;
   else if (!strcmp(name, "verify_wide")) o.verify_wide = value != 0;
   else if (!strcmp(name, "sort_path") && value >= -1 && value <= 1) o.sort_path = (int)value;
-  else if (!strcmp(name, "verify_runs") && value >= -1 && value <= 1) o.verify_runs = (int)value;
   else return arg_error("eg_set_option: unknown option or value out of range");
   return EG_OK;
 }
@@ -1344,17 +1343,6 @@ size_t eg_verify_workspace(int64_t m) {
   return ws_bytes(m, 1) + ws_bytes(m, 8) + ws_bytes(1, 8) + compact_workspace(m) + 1024;
 }
 
-// cluster-ordered path (k_verify8_runs): per-row run bounds, run keys and
-// their sort, chunk prefix
-static size_t verify_runs_bytes(int64_t n) {
-  return 2 * ws_bytes(n, 4) + ws_bytes(n, 8) + radix_workspace(n, false) + ws_bytes(n + 1, 4) +
-         ws_bytes(n + 1, 4) + scan_workspace(n + 1) + ws_bytes(1, 8) + 4096;
-}
-
-size_t eg_verify_workspace_n(int64_t m, int64_t n) {
-  return eg_verify_workspace(m) + verify_runs_bytes(n);
-}
-
 int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const double *d_norms,
               const uint64_t *d_keys, int64_t m, int32_t metric, double eps, uint64_t *d_out_keys,
               double *d_out_dist, int64_t *h_count, void *d_workspace, size_t workspace_bytes,
@@ -1376,49 +1364,7 @@ int eg_verify(const void *d_x, int x_is_f64, int64_t n, int32_t dim, const doubl
   EG_PROF(PC_VERIFY, st);
   const int vu = (!x_is_f64 && dim % 4 == 0 && dim <= 128 * VER_VU) ? (dim + 127) / 128 : 0;
   const bool narrow = !x_is_f64 && dim % 4 == 0 && dim <= 128 && !options().verify_wide;
-  // clustered outputs: many candidates per row -> runs in first-j order
-  const int vr = options().verify_runs;
-  const bool runs = narrow && n < (1ll << 32) && vr != 0 &&
-                    (vr == 1 || (m >= (1ll << 22) && m >= 4 * n)) &&
-                    ar.size - ar.used >= verify_runs_bytes(n) + compact_workspace(m);
-  if (runs) {
-    const size_t mark = ar.used;
-    uint32_t *rs = ar.take<uint32_t>(n);
-    uint32_t *re = ar.take<uint32_t>(n);
-    uint64_t *rk = ar.take<uint64_t>(n);
-    unsigned long long *rcount = ar.take<unsigned long long>(1);
-    uint32_t *nch = ar.take<uint32_t>(n + 1);
-    uint32_t *cst = ar.take<uint32_t>(n + 1);
-    EG_CUDA_TRY(cudaMemsetAsync(rs, 0xff, (size_t)n * 4, st));
-    EG_CUDA_TRY(cudaMemsetAsync(rcount, 0, 8, st));
-    const unsigned gm = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 32);
-    const unsigned gn = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 32);
-    k_run_bounds<<<gm, 256, 0, st>>>(d_keys, m, n, rs, re, bad);
-    k_run_keys<<<gn, 256, 0, st>>>(d_keys, rs, n, rk, rcount);
-    EG_LAUNCH_CHECK();
-    unsigned long long R = 0;
-    EG_CUDA_TRY(cudaMemcpyAsync(&R, rcount, 8, cudaMemcpyDeviceToHost, st));
-    EG_CUDA_TRY(cudaStreamSynchronize(st));
-    int shifts[8];
-    const int np = pair_key_shifts(n, shifts);
-    int rc = radix_sort(rk, nullptr, (int64_t)R, shifts, np, ar, st);
-    if (rc) return rc;
-    k_run_chunks<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(((int64_t)R + 255) / 256,
-                                                                   (int64_t)num_sms() * 32)),
-                   256, 0, st>>>(rk, (int64_t)R, rs, re, nch);
-    EG_CUDA_TRY(cudaMemsetAsync(nch + R, 0, 4, st));
-    rc = scan_exclusive_u32(nch, cst, (int64_t)R + 1, ar, st);
-    if (rc) return rc;
-    const int v8 = (dim / 4 + 7) / 8;
-    const unsigned gv = (unsigned)num_sms() * 8;
-#define EG_VR(V)                                                                              \
-  k_verify8_runs<8, V><<<gv, 256, 0, st>>>((const float *)d_x, n, dim, d_norms, d_keys, rk,   \
-                                           cst, (int64_t)R, rs, re, metric, eps, flags, dist)
-    if (v8 <= 1) EG_VR(1); else if (v8 == 2) EG_VR(2); else if (v8 == 3) EG_VR(3); else EG_VR(4);
-#undef EG_VR
-    EG_LAUNCH_CHECK();
-    ar.used = mark;
-  } else if (narrow) {
+  if (narrow) {
     // eight lanes per pair, four pairs per warp step (measured: 4 lanes per
     // pair is slower on configs 4 and 5)
     const int lp = 8;

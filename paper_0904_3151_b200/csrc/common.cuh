@@ -57,7 +57,6 @@ struct Options {
   int msm_streams = 2;           // 1: batches run on the caller's stream only
   int verify_wide = 0;           // 1: warp-per-pair verify even for dim <= 128
   int sort_path = -1;            // -1 auto, 0 onesweep, 1 classic LSD passes
-  int verify_runs = -1;          // -1 auto, 0 never, 1 whenever the shape allows
 };
 Options &options();
 

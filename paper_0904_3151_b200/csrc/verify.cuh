@@ -232,135 +232,4 @@ __global__ void __launch_bounds__(256) k_verify8(const float *__restrict__ x, in
   }
 }
 
-// ------------------------------------------------- cluster-ordered verify
-// Large clustered outputs (configs 4 and 5): the candidates of one row i
-// (a "run" of the (i, j)-sorted keys) mostly pair i with the members of its
-// cluster, and the runs of a cluster's rows share those j rows -- but
-// consecutive i's belong to unrelated clusters (row ids are a random
-// permutation), so the sorted-order sweep above streams every cluster's
-// rows through L2 over and over (config 4: 109 GB of DRAM per build).
-// Here the runs are visited in the order of their first j (equal for the
-// rows of one cluster) in CH-pair chunks dealt grid-stride, so the groups
-// resident at any moment work on the same few clusters and the j rows are
-// served from L2.  Per-pair arithmetic is k_verify8's (same lanes, same
-// slices, same butterfly): identical distances, written at the pairs'
-// sorted positions.
-constexpr int VR_CH = 256;        // pairs per work chunk
-
-// run bounds per row: start[i] = first position of i's run, end[i] = one
-// past its last (start preset to ~0 = no run)
-__global__ void k_run_bounds(const uint64_t *__restrict__ keys, int64_t m, int64_t n,
-                             uint32_t *__restrict__ start, uint32_t *__restrict__ end,
-                             unsigned long long *__restrict__ bad) {
-  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < m;
-       p += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = (uint32_t)(keys[p] >> 32);
-    if ((int64_t)i >= n || (int64_t)(keys[p] & 0xffffffffu) >= n) {
-      atomicMin(bad, (unsigned long long)p);
-      continue;
-    }
-    if (p == 0 || (uint32_t)(keys[p - 1] >> 32) != i) start[i] = (uint32_t)p;
-    if (p == m - 1 || (uint32_t)(keys[p + 1] >> 32) != i) end[i] = (uint32_t)(p + 1);
-  }
-}
-
-// rows with a run -> (first j << 32 | i) run keys, appended in any order
-__global__ void k_run_keys(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ start,
-                           int64_t n, uint64_t *__restrict__ rkeys,
-                           unsigned long long *__restrict__ count) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = start[i];
-    const bool has = s != 0xffffffffu;
-    const unsigned long long slot = warp_append(has, count);
-    if (has) rkeys[slot] = ((keys[s] & 0xffffffffull) << 32) | (uint64_t)i;
-  }
-}
-
-// chunks of each sorted run (inclusive prefix, for the work-item search)
-__global__ void k_run_chunks(const uint64_t *__restrict__ rkeys, int64_t R,
-                             const uint32_t *__restrict__ start, const uint32_t *__restrict__ end,
-                             uint32_t *__restrict__ nch) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R;
-       r += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = (uint32_t)rkeys[r];
-    nch[r] = (end[i] - start[i] + VR_CH - 1) / VR_CH;
-  }
-}
-
-template <int LP, int VU8>
-__global__ void __launch_bounds__(256) k_verify8_runs(
-    const float *__restrict__ x, int64_t n, int dim, const double *__restrict__ norms,
-    const uint64_t *__restrict__ keys, const uint64_t *__restrict__ rkeys,
-    const uint32_t *__restrict__ cstart /* exclusive chunk prefix, R + 1 */, int64_t R,
-    const uint32_t *__restrict__ start, const uint32_t *__restrict__ end, int metric, double eps,
-    uint8_t *__restrict__ flags, double *__restrict__ dist) {
-  const int lane = threadIdx.x & 31, gl = lane & (LP - 1);
-  const int64_t groups = (int64_t)gridDim.x * (256 / LP);
-  const int64_t gid = ((int64_t)blockIdx.x * 256 + threadIdx.x) / LP;
-  const int d4 = dim / 4;
-  const int64_t T = cstart[R];
-  for (int64_t t = gid; t < T; t += groups) {
-    // run r with cstart[r] <= t < cstart[r + 1]
-    int64_t lo = 0, hi = R;
-    while (hi - lo > 1) {
-      const int64_t mid = (lo + hi) >> 1;
-      if ((int64_t)cstart[mid] <= t) lo = mid; else hi = mid;
-    }
-    const uint32_t i = (uint32_t)rkeys[lo];
-    const int64_t p0 = (int64_t)start[i] + (t - cstart[lo]) * VR_CH;
-    const int64_t p1 = min((int64_t)end[i], p0 + VR_CH);
-    float4 a[VU8];
-    const float4 *xi = reinterpret_cast<const float4 *>(x + (int64_t)i * dim);
-#pragma unroll
-    for (int u = 0; u < VU8; ++u) {
-      const int q = gl + LP * u;
-      a[u] = q < d4 ? __ldg(xi + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    const double ni = norms[i];
-    for (int64_t p = p0; p < p1; ++p) {   // uniform within the LP-lane group
-      const int64_t j = (int64_t)(keys[p] & 0xffffffffu);
-      float4 b[VU8];
-      const float4 *xj = reinterpret_cast<const float4 *>(x + j * dim);
-#pragma unroll
-      for (int u = 0; u < VU8; ++u) {
-        const int q = gl + LP * u;
-        b[u] = q < d4 ? __ldg(xj + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      double acc = 0.0;
-#pragma unroll
-      for (int u = 0; u < VU8; ++u) {
-        if (gl + LP * u >= d4) break;
-        if (metric == EG_METRIC_COSINE) {
-          acc = fma((double)a[u].x, (double)b[u].x, acc);
-          acc = fma((double)a[u].y, (double)b[u].y, acc);
-          acc = fma((double)a[u].z, (double)b[u].z, acc);
-          acc = fma((double)a[u].w, (double)b[u].w, acc);
-        } else {
-          double tt;
-          tt = (double)a[u].x - (double)b[u].x; acc = fma(tt, tt, acc);
-          tt = (double)a[u].y - (double)b[u].y; acc = fma(tt, tt, acc);
-          tt = (double)a[u].z - (double)b[u].z; acc = fma(tt, tt, acc);
-          tt = (double)a[u].w - (double)b[u].w; acc = fma(tt, tt, acc);
-        }
-      }
-      // the LP lanes of a group share p: the butterfly stays within the group
-      const unsigned gmask = (LP == 32 ? 0xffffffffu : ((1u << LP) - 1u)) << (lane & ~(LP - 1));
-#pragma unroll
-      for (int o = LP / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(gmask, acc, o);
-      if (gl == 0) {
-        double dd;
-        if (metric == EG_METRIC_COSINE) {
-          dd = 1.0 - acc / (ni * norms[j]);
-          dd = dd < 0.0 ? 0.0 : (dd > 2.0 ? 2.0 : dd);
-        } else {
-          dd = sqrt(acc);
-        }
-        dist[p] = dd;
-        flags[p] = dd <= eps;
-      }
-    }
-  }
-}
-
 }  // namespace eg

@@ -395,7 +395,7 @@ def verify(x: torch.Tensor, norms: torch.Tensor, keys: torch.Tensor, metric: int
     if m == 0:
         return out_k[:0], out_d[:0]
     lib = _native.lib()
-    ws = _ws(lib.eg_verify_workspace_n(m, n), dev)
+    ws = _ws(lib.eg_verify_workspace(m), dev)
     cnt = ctypes_i64(0)
     rc = lib.eg_verify(_p(x), int(x.dtype == torch.float64), n, dim, _p(norms), _p(keys), m,
                        metric, float(eps), _p(out_k), _p(out_d), ctypes_addr(cnt), _p(ws),

@@ -731,33 +731,3 @@ def test_merge_runs_kernel(eg, runs):
     order = np.argsort(keys, kind="stable")
     np.testing.assert_array_equal(k.cpu().numpy(), keys[order])
     np.testing.assert_array_equal(d.cpu().numpy(), dist[order])
-
-
-@pytest.mark.parametrize("metric", ["cosine", "euclidean"])
-def test_cluster_ordered_verify_identical(eg, native_options, metric):
-    """The cluster-ordered verify (runs in first-j order) gives bit-identical
-    distances and the same edges as the sorted sweep, on a clustered pool
-    and on candidates with invalid indices (IndexError either way)."""
-    import torch
-    from paper_0904_3151_b200 import _native, engine, workloads
-    x = workloads.cfg4_points(200_000, largest=4_000)
-    xd = torch.from_numpy(x).cuda()
-    params = eg.MsmParams(0.08 if metric == "cosine" else 0.4, 1e-6, 64, 2, 16, 1, 0)
-    out = eg.build_graph_device(xd, params, metric=metric)
-    cand = out["candidates"]
-    norms = out["norms"]
-    mid = _native.METRIC_COSINE if metric == "cosine" else _native.METRIC_EUCLIDEAN
-    res = {}
-    for vr in (0, 1):
-        with _native.options(verify_runs=vr):
-            k, d = engine.verify(xd, norms, cand.clone(), mid, params.epsilon)
-        res[vr] = (k.cpu().numpy(), d.cpu().numpy())
-    assert res[0][0].shape[0] > 100_000
-    np.testing.assert_array_equal(res[0][0], res[1][0])
-    np.testing.assert_array_equal(res[0][1], res[1][1])
-    bad = cand.clone()
-    bad[5] = (1 << 40) | 3
-    for vr in (0, 1):
-        with _native.options(verify_runs=vr):
-            with pytest.raises(IndexError):
-                engine.verify(xd, norms, bad, mid, params.epsilon)
