@@ -771,11 +771,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   }
   __syncthreads();
   // 5. every in-group pair once (load-balanced over the CTA)
-#if EG_EXP_NOPAIRS   // timing experiment only: skip the pair loop
-  const uint32_t P = 0;
-#else
   const uint32_t P = S.pp[R];
-#endif
   if (P > pair_limit) {    // uniform: hand the bucket to the sliced medium tier
     __syncthreads();
     return false;
