@@ -168,12 +168,28 @@ size_t eg_msm_workspace(int64_t n, int32_t length, int32_t replicates);
 /* reference partition (first L % k' blocks one bit wider).  Synchronous. */
 /* h_cost (optional, 2 doubles): modelled ms of the chosen and of k.      */
 /* Option "msm_blocks" (eg_set_option): >0 forces that k', -1 forces k.    */
+/*                                                                       */
+/* Covering designs.  The complete family of C(k',d) masks is one way to  */
+/* make every pair within d share a masked key in some unit; any family   */
+/* of masked block sets that contains every d-subset of the blocks does   */
+/* (each member masks m >= d blocks), with far fewer units at the same    */
+/* key width (48 bits, d = 3: 20 units of 26 kept bits from C(11,5,3)     */
+/* instead of 35 units of 27 bits from k' = 7).  The plan also probes the */
+/* built-in table (eg_msm_design) and returns the plan code               */
+/* 10000 + 100 v + m for the design (v blocks, m masked per unit) when it */
+/* is the cheapest; such units run through eg_msm_pairs_design.  Option   */
+/* "msm_designs" = 0 restricts the plan to complete designs; "msm_blocks" */
+/* also accepts a plan code.                                              */
 /* --------------------------------------------------------------------- */
 size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d);
 int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k,
                 int32_t d, double oversized_fraction, int32_t *h_k_out,
                 double *h_cost, void *d_workspace, size_t workspace_bytes,
                 void *stream);
+/* Built-in covering design C(v, m, t): writes min(count, capacity) block */
+/* masks (bit b = block b masked) to h_masks (may be null) and returns    */
+/* the member count, 0 when the table has no such design.                 */
+int eg_msm_design(int32_t v, int32_t m, int32_t t, uint64_t *h_masks, int32_t capacity);
 /* Output-size estimate for eg_msm_pairs' capacity: pairs with Hamming    */
 /* <= d among a strided sample of min(n, 8192) rows of (up to 4 of) the   */
 /* replicates, scaled by n(n-1)/(S(S-1)) and replicates/probed.            */
@@ -189,6 +205,22 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length,
                  int64_t n_units, uint64_t *d_out_keys, uint16_t *d_out_rep,
                  int64_t capacity, int64_t *h_counts, void *d_workspace,
                  size_t workspace_bytes, void *stream);
+
+/* eg_msm_pairs for the units of a covering design: h_design[n_design]     */
+/* (<= 64) is the ordered family of masked block sets every replicate     */
+/* runs (each >= d blocks; every d-subset of the k blocks inside a member, */
+/* checked); every h_unit_mask must be a member (any subset of the units: */
+/* sharding).  A pair is emitted by the FIRST member under which it is    */
+/* grouped (the role of the reference's earlier-mask search,              */
+/* hamming_join.py:130-141), so the emitted set is again exactly          */
+/* {(i,j): popcount(c_i^c_j) <= d}.  n_design = 0: eg_msm_pairs.          */
+int eg_msm_pairs_design(const uint64_t *d_codes, int64_t n, int32_t length,
+                        int32_t replicates, const int32_t *h_block_bounds, int32_t k,
+                        int32_t d, const int32_t *h_unit_rep, const uint64_t *h_unit_mask,
+                        int64_t n_units, const uint64_t *h_design, int32_t n_design,
+                        uint64_t *d_out_keys, uint16_t *d_out_rep, int64_t capacity,
+                        int64_t *h_counts, void *d_workspace, size_t workspace_bytes,
+                        void *stream);
 
 /* Deferred cross-replicate first-witness rule (pipeline.py:286-314) over  */
 /* pairs emitted by eg_msm_pairs with d_out_rep: d_keep[p] = 1 iff the     */

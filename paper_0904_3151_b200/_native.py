@@ -74,6 +74,9 @@ def _declare(lib):
         "eg_msm_plan": ([P, i64, i32, i32, i32, dbl, P, P, P, sz, P], I),
         "eg_msm_estimate_pairs": ([P, i64, i32, i32, i32, P, P, sz, P], I),
         "eg_msm_pairs": ([P, i64, i32, i32, P, i32, i32, P, P, i64, P, P, i64, P, P, sz, P], I),
+        "eg_msm_pairs_design": ([P, i64, i32, i32, P, i32, i32, P, P, i64, P, i32, P, P, i64, P, P,
+                                 sz, P], I),
+        "eg_msm_design": ([i32, i32, i32, P, i32], I),
         "eg_xrep_filter": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),
         "eg_xrep_filter_async": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),
         "eg_hamming_filter_async": ([P, P, i64, P, i64, i32, i32, i32, P, P, P], I),

@@ -357,7 +357,10 @@ int eg_set_option(const char *name, long long value) {
   if (!strcmp(name, "project_path") && value >= 0 && value <= 4) o.project_path = (int)value;
   else if (!strcmp(name, "fixup_force_seq")) o.fixup_force_seq = value != 0;
   else if (!strcmp(name, "fixup_cap") && value >= 0) o.fixup_cap = value;
-  else if (!strcmp(name, "msm_blocks") && value >= -1 && value <= EG_MAX_BLOCKS) o.msm_blocks = (int)value;
+  else if (!strcmp(name, "msm_blocks") &&
+           ((value >= -1 && value <= EG_MAX_BLOCKS) || (value >= 10000 && value < 20000)))
+    o.msm_blocks = (int)value;
+  else if (!strcmp(name, "msm_designs") && (value == 0 || value == 1)) o.msm_designs = (int)value;
   else if (!strcmp(name, "msm_streams") && (value == 1 || value == 2)) o.msm_streams = (int)value;
   else if (!strcmp(name, "verify_wide")) o.verify_wide = value != 0;
   else if (!strcmp(name, "sort_path") && value >= -1 && value <= 1) o.sort_path = (int)value;
@@ -730,13 +733,32 @@ static void plan_kept(int length, int kk, uint64_t dropped_blocks, uint64_t kept
 }
 
 
+#include "designs.inc"
+constexpr int PLAN_DESIGN_BASE = 10000;   // plan code of a table design: BASE + 100 v + m
+
+static const DesignEntry *find_design(int v, int m, int t) {
+  for (const DesignEntry &e : kDesigns)
+    if (e.v == v && e.m == m && e.t == t) return &e;
+  return nullptr;
+}
+
+int eg_msm_design(int32_t v, int32_t m, int32_t t, uint64_t *h_masks, int32_t capacity) {
+  const DesignEntry *e = find_design(v, m, t);
+  if (!e) return 0;
+  if (h_masks)
+    for (int i = 0; i < e->count && i < capacity; ++i) h_masks[i] = kDesignMasks[e->offset + i];
+  return e->count;
+}
+
 constexpr int PLAN_REF_MAX = 4096;     // reference masks probed for the oversize check
 constexpr int PLAN_PER_K = 12;         // masks probed per candidate block count
+constexpr int PLAN_PER_DESIGN = 8;     // members probed per candidate design
 constexpr int PLAN_MIN_ROWS = 65536;   // smaller pools keep the reference blocks
 
 size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d) {
   (void)length; (void)k; (void)d;
-  const size_t P = PLAN_REF_MAX + PLAN_PER_K * EG_MAX_BLOCKS;
+  const size_t P = PLAN_REF_MAX + PLAN_PER_K * EG_MAX_BLOCKS +
+                   PLAN_PER_DESIGN * (sizeof(kDesigns) / sizeof(kDesigns[0]));
   return ws_bytes(P * 4, 8) + ws_bytes(P, 8) + ws_bytes(P, 4) + ws_bytes(P, 4) + 1024;
 }
 
@@ -755,6 +777,10 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   const int forced = options().msm_blocks;
   if (forced > 0) {
     if (forced > d && forced <= kmax) *h_k_out = forced;
+    if (forced >= PLAN_DESIGN_BASE) {
+      const int fv = (forced - PLAN_DESIGN_BASE) / 100, fm = (forced - PLAN_DESIGN_BASE) % 100;
+      if (fv <= kmax && find_design(fv, fm, d)) *h_k_out = forced;
+    }
     return EG_OK;
   }
   if (forced < 0 || n < PLAN_MIN_ROWS) return EG_OK;
@@ -767,11 +793,11 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   // every candidate block count
   std::vector<uint64_t> kept;
   std::vector<int> probe_k;
-  auto add = [&](int kk, uint64_t dropped) {
+  auto add = [&](int kk, uint64_t dropped, int label = 0) {
     uint64_t kw[4];
     plan_kept(length, kk, dropped, kw);
     kept.insert(kept.end(), kw, kw + 4);
-    probe_k.push_back(kk);
+    probe_k.push_back(label ? label : kk);
   };
   {
     std::vector<int> c(d);
@@ -822,6 +848,24 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
         seen.push_back(m);
         add(kk, m);
       }
+    }
+  }
+  // covering designs of the table (t = d): fewer units than the complete
+  // design of similar key width; PLAN_PER_DESIGN members probed each
+  std::vector<double> design_units;      // by plan code - PLAN_DESIGN_BASE
+  if (d >= 1 && options().msm_designs) {
+    const double lgn = std::log2((double)n);
+    for (const DesignEntry &e : kDesigns) {
+      if (e.t != d || e.v > kmax) continue;
+      const double kept_bits = (double)length * (e.v - e.m) / e.v;
+      if (kept_bits < lgn - 2.0 || kept_bits > lgn + 14.0) continue;
+      const int code = PLAN_DESIGN_BASE + 100 * e.v + e.m;
+      const int np = std::min<int>(e.count, PLAN_PER_DESIGN);
+      for (int i = 0; i < np; ++i)
+        add(e.v, kDesignMasks[e.offset + (int64_t)i * e.count / np], code);
+      if ((int)design_units.size() <= code - PLAN_DESIGN_BASE)
+        design_units.resize(code - PLAN_DESIGN_BASE + 1, 0.0);
+      design_units[code - PLAN_DESIGN_BASE] = e.count;
     }
   }
   const int P = (int)probe_k.size();
@@ -881,7 +925,9 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     int cnt = 0;
     for (; p < P && probe_k[p] == kk; ++p, ++cnt) sum += (double)pairs[p];
     const double est_pairs = sum / cnt * scale;
-    const double cost = comb_sat(kk, d) * ((double)n * ce + est_pairs * cp);
+    const double units =
+        kk >= PLAN_DESIGN_BASE ? design_units[kk - PLAN_DESIGN_BASE] : comb_sat(kk, d);
+    const double cost = units * ((double)n * ce + est_pairs * cp);
     if (kk == k) ref_cost = cost;
     if (best < 0 || cost < best) {
       best = cost;
@@ -941,7 +987,39 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
                  const uint64_t *h_unit_mask, int64_t n_units, uint64_t *d_out_keys,
                  uint16_t *d_out_rep, int64_t capacity, int64_t *h_counts, void *d_workspace,
                  size_t workspace_bytes, void *stream) {
+  return eg_msm_pairs_design(d_codes, n, length, replicates, h_block_bounds, k, d, h_unit_rep,
+                             h_unit_mask, n_units, nullptr, 0, d_out_keys, d_out_rep, capacity,
+                             h_counts, d_workspace, workspace_bytes, stream);
+}
+
+// Does every d-subset of the k blocks lie inside a member of the family?
+static bool design_covers(const uint64_t *fam, int nf, int k, int d) {
+  if (d == 0) return nf > 0;
+  std::vector<int> c(d);
+  for (int i = 0; i < d; ++i) c[i] = i;
+  while (true) {
+    uint64_t m = 0;
+    for (int i = 0; i < d; ++i) m |= 1ull << c[i];
+    bool ok = false;
+    for (int q = 0; q < nf && !ok; ++q) ok = (fam[q] & m) == m;
+    if (!ok) return false;
+    int i = d - 1;
+    while (i >= 0 && c[i] == k - d + i) --i;
+    if (i < 0) return true;
+    ++c[i];
+    for (int j = i + 1; j < d; ++j) c[j] = c[j - 1] + 1;
+  }
+}
+
+int eg_msm_pairs_design(const uint64_t *d_codes, int64_t n, int32_t length, int32_t replicates,
+                        const int32_t *h_block_bounds, int32_t k, int32_t d,
+                        const int32_t *h_unit_rep, const uint64_t *h_unit_mask, int64_t n_units,
+                        const uint64_t *h_design, int32_t n_design, uint64_t *d_out_keys,
+                        uint16_t *d_out_rep, int64_t capacity, int64_t *h_counts,
+                        void *d_workspace, size_t workspace_bytes, void *stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (n_design < 0 || n_design > MSM_MAXDESIGN || (n_design > 0 && !h_design))
+    return arg_error("eg_msm_pairs: design of more than 64 members (or null)");
   if (n < 1 || n >= (1ll << 32)) return arg_error("eg_msm_pairs: need 1 <= n < 2^32");
   if (length < 1 || length > EG_MAX_LENGTH)
     return arg_error("eg_msm_pairs: length outside [1, 256]");
@@ -961,6 +1039,20 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
   }
   uint64_t all_bits[4] = {0, 0, 0, 0};
   for (int t = 0; t < length; ++t) all_bits[t >> 6] |= 1ull << (t & 63);
+  auto kept_of = [&](uint64_t mb, unsigned long long *kept) {
+    for (int w = 0; w < 4; ++w) kept[w] = all_bits[w];
+    for (int b = 0; b < k; ++b)
+      if (mb >> b & 1)
+        for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t)
+          kept[t >> 6] &= ~(1ull << (t & 63));
+  };
+  if (n_design > 0) {
+    for (int q = 0; q < n_design; ++q)
+      if (__builtin_popcountll(h_design[q]) < d || (k < 64 && (h_design[q] >> k)))
+        return arg_error("eg_msm_pairs: design members must mask >= d of the k blocks");
+    if (comb_sat(k, d) > 1048576.0 || !design_covers(h_design, n_design, k, d))
+      return arg_error("eg_msm_pairs: the design does not cover every d-subset of the blocks");
+  }
 
   MsmLayout lay = msm_layout(n, replicates);
   Arena ar(d_workspace, workspace_bytes);
@@ -1019,19 +1111,23 @@ int eg_msm_pairs(const uint64_t *d_codes, int64_t n, int32_t length, int32_t rep
     UnitBatch ub;
     memset(&ub, 0, sizeof(ub));
     ub.count = (int)std::min<int64_t>(per_batch, n_units - u0);
+    ub.ndesign = n_design;
+    for (int q = 0; q < n_design; ++q) kept_of(h_design[q], ub.dkept[q]);
     for (int j = 0; j < ub.count; ++j) {
       const int rep = h_unit_rep[u0 + j];
       const uint64_t mb = h_unit_mask[u0 + j];
       if (rep < 0 || rep >= replicates) return arg_error("eg_msm_pairs: unit replicate out of range");
-      if (__builtin_popcountll(mb) != d || (k < 64 && (mb >> k)))
+      if (n_design > 0) {
+        const uint64_t *hit = std::find(h_design, h_design + n_design, mb);
+        if (hit == h_design + n_design)
+          return arg_error("eg_msm_pairs: unit mask is not a member of the design");
+        ub.dq[j] = (uint8_t)(hit - h_design);
+      } else if (__builtin_popcountll(mb) != d || (k < 64 && (mb >> k))) {
         return arg_error("eg_msm_pairs: unit mask must select exactly d of the k blocks");
+      }
       ub.rep[j] = rep;
       ub.maskbits[j] = mb;
-      for (int w = 0; w < 4; ++w) ub.kept[j][w] = all_bits[w];
-      for (int b = 0; b < k; ++b)
-        if (mb >> b & 1)
-          for (int t = h_block_bounds[b]; t < h_block_bounds[b + 1]; ++t)
-            ub.kept[j][t >> 6] &= ~(1ull << (t & 63));
+      kept_of(mb, ub.kept[j]);
       ub.salt[j] = 0x2545f4914f6cdd1dULL * (uint64_t)(u0 + j + 1);
       // tail blocks: masked blocks above the lowest kept block
       int lowest_kept = 0;

@@ -53,7 +53,8 @@ struct Options {
   int project_path = 0;          // 0 auto, 1 SIMT, 2 kind::tf32, 3 unfused norms, 4 non-TMA tc
   int fixup_force_seq = 0;       // 1: every band entry by the sequential fallback
   long long fixup_cap = 0;       // > 0: cap the fix-up entry list (overflow path)
-  int msm_blocks = 0;            // > 0: force the block count; < 0: keep the reference's
+  int msm_blocks = 0;            // > 0: force the block count (or a design's plan code); < 0: keep the reference's
+  int msm_designs = 1;           // 0: the plan considers complete designs only
   int msm_streams = 2;           // 1: batches run on the caller's stream only
   int verify_wide = 0;           // 1: warp-per-pair verify even for dim <= 128
   int sort_path = -1;            // -1 auto, 0 onesweep, 1 classic LSD passes

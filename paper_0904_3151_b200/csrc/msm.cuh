@@ -17,9 +17,10 @@
 //  4. k_msm_group   : one CTA per bucket, entirely in shared memory: counting
 //                     sort on the next hash digits, run detection (equal
 //                     keys are exactly the runs), code gather for multi-row
-//                     runs only, then a flattened, load-balanced pair loop
-//                     with popcount <= d, the O(1) canonical-mask rule and
-//                     the cross-replicate rule, warp-aggregated emission.
+//                     runs only, then a member-parallel pair loop (lane =
+//                     grouped row, circulant partner order) with popcount
+//                     <= d, the O(1) canonical-mask rule (or a covering
+//                     design's first-member rule), staged emission.
 //  5. k_msm_spill   : buckets larger than the shared-memory capacity (giant
 //                     groups) are enumerated by 128x128 tile pairs.
 // Equal masked keys always share a bucket and a run, so every reference
@@ -51,6 +52,7 @@ constexpr int MSM_STAGE_MAX_B = 4096;   // scatter stages runs in smem up to thi
 constexpr uint32_t MSM_PAIR_SPLIT = EG_PAIR_SPLIT;  // small-tier buckets with more pairs -> medium
 
 constexpr int MSM_MAXT = 4;             // tail blocks of the O(1) canonical test
+constexpr int MSM_MAXDESIGN = 64;       // members of a covering design (units per replicate)
 #ifndef EG_TAIL_REGS
 #define EG_TAIL_REGS 0   // 1: tail masks in registers (measured slower: register pressure)
 #endif
@@ -70,6 +72,14 @@ struct UnitBatch {
   uint8_t ntail[MSM_MAXU];
   uint16_t tail_lo[MSM_MAXU][MSM_MAXT];
   uint16_t tail_hi[MSM_MAXU][MSM_MAXT];
+  // Covering-design units (ndesign > 0): the units of a replicate are the
+  // ndesign members of an ordered family of masked block sets (each of >= d
+  // blocks, every d-subset of blocks inside at least one member); a pair is
+  // owned by the FIRST member whose kept bits it agrees on.  dq = the unit's
+  // position in the family, dkept = the kept bits of every member.
+  int ndesign;
+  uint8_t dq[MSM_MAXU];
+  unsigned long long dkept[MSM_MAXDESIGN][4];
 };
 
 struct MsmArgs {
@@ -340,12 +350,16 @@ __device__ __forceinline__ uint64_t canonical_mask(const uint64_t (&x)[W], const
 template <int W>
 struct TailTest {
   int nt;                          // tail blocks; > MSM_MAXT: general path
+  int dq;                          // >= 0: covering-design unit at this position
+  const unsigned long long *dk;    // [MSM_MAXDESIGN][4] kept bits of the design members
   uint64_t maskbits;
   const uint64_t *m;               // [MSM_MAXT][W] masks in shared memory
   // every thread calls load (same u); the masks are written by the first
   // MSM_MAXT * W threads -- the caller synchronises before the first ok()
   __device__ __forceinline__ void load(const UnitBatch &ub, int u, uint64_t *sm) {
     nt = ub.ntail[u];
+    dq = ub.ndesign > 0 ? (int)ub.dq[u] : -1;
+    dk = &ub.dkept[0][0];
     maskbits = ub.maskbits[u];
     m = sm;
     const int i = threadIdx.x;
@@ -368,6 +382,17 @@ struct TailTest {
 #endif
   __device__ __forceinline__ bool ok(const uint64_t (&x)[W], int pc, const uint8_t *b2b, int k,
                                      int d) const {
+    if (dq >= 0) {
+      // design units: an earlier member that keeps none of the differing bits
+      // groups the pair too, and owns it (uniform loop, uniform loads)
+      for (int q = 0; q < dq; ++q) {
+        uint64_t any = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) any |= x[w] & dk[q * 4 + w];
+        if (!any) return false;
+      }
+      return true;
+    }
     if (nt > MSM_MAXT) return canonical_mask<W>(x, b2b, k, d) == maskbits;
     if (nt > pc) return false;       // every tail block needs a differing bit
 #if EG_TAIL_REGS
@@ -455,35 +480,20 @@ __device__ __forceinline__ int pair_verdict_rows(const uint64_t (&ca)[W], const 
   return 2;
 }
 
-__device__ __forceinline__ void tri_decode(uint32_t q, uint32_t c, uint32_t &ia, uint32_t &ib) {
-  // pairs (0,1),(0,2),..,(0,c-1),(1,2),...; T(a) = a*c - a*(a+1)/2
-  float disc = (float)(2 * c - 1) * (float)(2 * c - 1) - 8.0f * (float)q;
-  int ai = (int)floorf(((float)(2 * c - 1) - sqrtf(fmaxf(disc, 0.f))) * 0.5f);
-  ai = max(0, min(ai, (int)c - 2));
-  auto T = [c](int x) { return (uint32_t)x * c - (uint32_t)x * (uint32_t)(x + 1) / 2; };
-  while (ai > 0 && T(ai) > q) --ai;
-  while (ai + 1 <= (int)c - 2 && T(ai + 1) <= q) ++ai;
-  ia = (uint32_t)ai;
-  ib = q - T(ai) + ai + 1;
-}
-
 // ------------------------------------------------------------------ 4
 // Bucket processing, entirely in shared memory.  An open-addressing table
 // keyed by the 32-bit secondary hash groups the bucket's rows exactly by
 // (h2), which is the masked key up to 2^-32 collisions (filtered later by an
 // exact key compare).  Only rows of multi-row groups are materialised
 // (rows + gathered codes, grouped contiguously); singletons -- the vast
-// majority -- cost one table insert.  A flattened, load-balanced pair loop
-// then visits every in-group pair once (the reference's group visits,
+// majority -- cost one table insert.  A member-parallel pair loop then
+// visits every in-group pair once (the reference's group visits,
 // hamming_join.py:116-122) and applies pair_verdict.
 #ifndef EG_SMALL_MDIV
 #define EG_SMALL_MDIV 1
 #endif
 #ifndef EG_GROUP_FILTER
 #define EG_GROUP_FILTER 1
-#endif
-#ifndef EG_PAIR_WARPVOTE
-#define EG_PAIR_WARPVOTE 0
 #endif
 #ifndef EG_RANK_ATOMIC32
 #define EG_RANK_ATOMIC32 1
@@ -507,10 +517,10 @@ struct HGroupSmem {
   alignas(16) unsigned char big[OVERLAY ? TAB_BYTES : TAB_BYTES + MEM_BYTES];
   uint32_t mslot[GCAP];      // slots holding >= 2 rows (one entry per group)
   uint32_t runs[GCAP];       // (start << 16) | len, one per group
-  uint32_t pp[GCAP + 1];     // pair prefix per group
+  uint16_t mgid[MCAP];       // group of every grouped row (index into runs)
   uint8_t b2b[EG_MAX_LENGTH];
   unsigned long long sw[NT / 32];
-  uint32_t nruns, maxrun, raw, neu, ncand, nout;
+  uint32_t nruns, maxrun, raw, neu, ncand, nout, chunk;
   unsigned long long obase;
   uint64_t tmask[MSM_MAXT * W];    // tail masks of the bucket's unit (TailTest)
   // Emitted pairs are staged here during the pair loop (the table is dead
@@ -583,7 +593,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   for (uint32_t i = threadIdx.x * 8; i < FS; i += NT * 8)
     *reinterpret_cast<uint4 *>(&F[i]) = make_uint4(~0u, ~0u, ~0u, ~0u);
   if (threadIdx.x == 0) {
-    S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; S.nout = 0;
+    S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; S.nout = 0; S.chunk = 0;
   }
   __syncthreads();
 #pragma unroll
@@ -644,7 +654,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     if (threadIdx.x + j * NT < s) cand |= 1u << j;
   const uint32_t ncand = s;
   if (threadIdx.x == 0) {
-    S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; S.nout = 0;
+    S.nruns = 0; S.maxrun = 1; S.raw = 0; S.neu = 0; S.ncand = 0; S.nout = 0; S.chunk = 0;
   }
   if (ncand == 0) {
     __syncthreads();
@@ -732,14 +742,12 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     const uint32_t r = threadIdx.x * RP + q;
     if (r < R) {
       const uint32_t off = (uint32_t)(run >> 32);
-      S.tab()[S.mslot[r]] = ((unsigned long long)off << 32) | c_my[q];
+      S.tab()[S.mslot[r]] = ((unsigned long long)r << 48) | ((unsigned long long)off << 32) | c_my[q];
       S.runs[r] = (off << 16) | c_my[q];
-      S.pp[r] = (uint32_t)run;
       atomicMax(&S.maxrun, c_my[q]);
       run += ((unsigned long long)c_my[q] << 32) | (c_my[q] * (c_my[q] - 1) / 2);
     }
   }
-  if (threadIdx.x == 0) S.pp[R] = (uint32_t)tot;
 #if EG_MSM_STATS
   if (threadIdx.x == 0) {
     atomicAdd(&g_msm_stats[0], 1ull);
@@ -753,125 +761,96 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   __syncthreads();
   // member positions out of the table first; then the (possibly overlaid)
   // member arrays are written
+  // (group index << 16) | member position
 #pragma unroll
   for (int j = 0; j < PT; ++j)
-    if (grouped >> j & 1)
-      slr[j] = (uint32_t)(S.tab()[slr[j] >> 16] >> 32) + (slr[j] & 0xffffu);
+    if (grouped >> j & 1) {
+      const uint32_t og = (uint32_t)(S.tab()[slr[j] >> 16] >> 32);
+      slr[j] = (og & 0xffff0000u) | ((og & 0xffffu) + (slr[j] & 0xffffu));
+    }
   uint64_t *mcodes = S.codes();
   uint32_t *mrows = S.members();
   if (HGroupSmem<W, CAP, NT, MDIV>::OVERLAY) __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     if (grouped >> j & 1) {
-      const uint32_t pos = slr[j];
+      const uint32_t pos = slr[j] & 0xffffu;
       mrows[pos] = (uint32_t)e[j];
+      S.mgid[pos] = (uint16_t)(slr[j] >> 16);
 #pragma unroll
       for (int w = 0; w < W; ++w) mcodes[pos * W + w] = cg[j][w];
     }
   }
   __syncthreads();
-  // 5. every in-group pair once (load-balanced over the CTA)
-  const uint32_t P = S.pp[R];
+  // 5. every in-group pair once.  Warps take chunks of 32 consecutive
+  //    grouped rows (members of a group are contiguous); lane = one member
+  //    with its code in registers.  Member i of a group of L visits
+  //    (i + t) mod L for t = 1 .. L/2 (for even L the last step only from
+  //    the lower half): every unordered pair exactly once, the same trip
+  //    count for every member of a group (no divergence inside large
+  //    groups, no per-pair bookkeeping), partners at consecutive addresses.
+  const uint32_t P = (uint32_t)tot;
   if (P > pair_limit) {    // uniform: hand the bucket to the sliced medium tier
     __syncthreads();
     return false;
   }
+  const uint32_t M = (uint32_t)(tot >> 32);
   const unsigned long long *kept = ub.kept[u];
   TailTest<W> tt;
   tt.load(ub, u, S.tmask);
   __syncthreads();
   tt.fetch();
   uint32_t my_raw = 0, my_new = 0;
-  // Each thread takes a contiguous range of the flattened pair index and
-  // walks it incrementally (one group lookup + triangular decode per thread).
-  const uint32_t chunk = (P + NT - 1) / NT;
-  uint32_t p = threadIdx.x * chunk;
-  const uint32_t pend = min(P, p + chunk);
-  if (p < pend) {
-    uint32_t lo = 0, hi = R;  // r with pp[r] <= p < pp[r+1]
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (S.pp[mid] <= p) lo = mid; else hi = mid;
-    }
-    uint32_t r = lo;
-    uint32_t rr = S.runs[r];
-    uint32_t start = rr >> 16, len = rr & 0xffffu;
-    uint32_t ia, ib;
-    tri_decode(p - S.pp[r], len, ia, ib);
+  const uint32_t lane = threadIdx.x & 31;
+  while (true) {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(&S.chunk, 1u);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c * 32 >= M) break;
+    const uint32_t pos = c * 32 + lane;
+    uint32_t start = 0, len = 0, idx = 0, ra = 0;
     uint64_t ca[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) ca[w] = mcodes[(start + ia) * W + w];
-    uint32_t ra = mrows[start + ia];
-    for (; p < pend; ++p) {
-      uint64_t cb[W];
+    for (int w = 0; w < W; ++w) ca[w] = 0;
+    if (pos < M) {
+      const uint32_t rr = S.runs[S.mgid[pos]];
+      start = rr >> 16;
+      len = rr & 0xffffu;
+      idx = pos - start;
+      ra = mrows[pos];
 #pragma unroll
-      for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + ib) * W + w];
-#if EG_PAIR_WARPVOTE
-      const uint32_t rb = mrows[start + ib];
-      const int v = pair_verdict<W>(ca, cb, ra, rb, a, tt, kept, rep, S.b2b);
-      my_raw += v > 0;
-      my_new += v == 2;
-      const bool emit = v == 2;
-      const unsigned active = __activemask();
-      const unsigned mask = __ballot_sync(active, emit);
-      if (mask) {   // stage in shared memory (global only on overflow)
-        const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-        const uint32_t so = smem_append(active, mask, &S.nout);
-        const bool spill = emit && so >= OUTCAP;
-        if (emit && !spill) S.outbuf()[so] = key;
-        const unsigned smask = __ballot_sync(active, spill);
-        if (smask) {
-          const int lane = threadIdx.x & 31, leader = __ffs(smask) - 1;
-          unsigned long long slot = 0;
-          if (lane == leader) slot = atomicAdd(&a.ctr[0], (unsigned long long)__popc(smask));
-          slot = __shfl_sync(active, slot, leader) + __popc(smask & ((1u << lane) - 1u));
-          if (spill && slot < a.out_cap) {
-            a.out_keys[slot] = key;
-            if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
-          }
-        }
-      }
-#else
-      // Emits are rare next to visits (a few per thousand at the planned
-      // block count): no per-visit warp vote; an emitting lane takes its
-      // staging slot with its own shared-memory atomic, and the row index
-      // is read only then.
-      const int v = pair_verdict_rows<W>(ca, cb, ra, mrows, start + ib, a, tt, kept, rep, S.b2b);
-      if (v) {
-        my_raw += 1;
-        if (v == 2) {
-          ++my_new;
-          const uint32_t rb = mrows[start + ib];
-          const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-          const uint32_t so = atomicAdd(&S.nout, 1u);
-          if (so < OUTCAP) {
-            S.outbuf()[so] = key;
-          } else {
-            const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
-            if (slot < a.out_cap) {
-              a.out_keys[slot] = key;
-              if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
+      for (int w = 0; w < W; ++w) ca[w] = mcodes[pos * W + w];
+    }
+    // trips of this member: t*2 < len, plus t*2 == len from the lower half
+    const uint32_t trips =
+        pos < M ? (len >> 1) - ((len & 1u) == 0 && idx * 2 >= len ? 1u : 0u) : 0u;
+    const uint32_t maxtrips = __reduce_max_sync(0xffffffffu, trips);
+    uint32_t jb = idx;
+    for (uint32_t t = 1; t <= maxtrips; ++t) {
+      if (t <= trips) {
+        if (++jb == len) jb = 0;
+        uint64_t cb[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + jb) * W + w];
+        const int v = pair_verdict_rows<W>(ca, cb, ra, mrows, start + jb, a, tt, kept, rep, S.b2b);
+        if (v) {
+          my_raw += 1;
+          if (v == 2) {
+            ++my_new;
+            const uint32_t rb = mrows[start + jb];
+            const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+            const uint32_t so = atomicAdd(&S.nout, 1u);
+            if (so < OUTCAP) {
+              S.outbuf()[so] = key;
+            } else {
+              const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
+              if (slot < a.out_cap) {
+                a.out_keys[slot] = key;
+                if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
+              }
             }
           }
         }
-      }
-#endif
-      // advance (ia, ib) in (0,1),(0,2),..,(1,2),.. order, crossing groups
-      if (++ib == len) {
-        if (++ia == len - 1) {
-          do {
-            ++r;
-          } while (r < R && S.pp[r + 1] == S.pp[r]);
-          if (r >= R) break;
-          rr = S.runs[r];
-          start = rr >> 16;
-          len = rr & 0xffffu;
-          ia = 0;
-        }
-        ib = ia + 1;
-#pragma unroll
-        for (int w = 0; w < W; ++w) ca[w] = mcodes[(start + ia) * W + w];
-        ra = mrows[start + ia];
       }
     }
   }

@@ -68,6 +68,10 @@ class DeviceOps:
         rank holding the gathered codes picks the same one)."""
         return engine.plan_blocks(codes, params.length, params.blocks, params.mismatch)
 
+    def unit_count(self, blocks, mismatch):
+        """Units per replicate of a plan code (block count or design)."""
+        return engine.unit_count(blocks, mismatch)
+
     def candidates(self, codes, params, units, blocks):
         return engine.msm_candidates(codes, params.length, params.blocks, params.mismatch,
                                      blocks=blocks, select=lambda total: units)
@@ -195,10 +199,9 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
         norms_s = ops.norms(xs)
         codes_s = ops.project(xs, norms_s, params)
         codes, norms = gather_codes(codes_s, norms_s, n, world, rank)
-    from math import comb
     # one plan (rank 0), one 8-byte broadcast: every rank runs the same units
     blocks = broadcast_int(ops.plan(codes, params) if rank == 0 else 0, rank, codes.device)
-    units = my_units(params.replicates * comb(blocks, max(0, params.mismatch)), world, rank)
+    units = my_units(params.replicates * ops.unit_count(blocks, params.mismatch), world, rank)
     keys, info = ops.candidates(codes, params, units, blocks)
     info = dict(info, blocks=blocks)
     keys = ops.sort(keys, n)
@@ -263,7 +266,6 @@ def build_on_devices(rows, params, metric: str, devices):
     same for any device list (the mirror of the reference's thread-count
     contract, tests/test_pipeline.py:130-135)."""
     from concurrent.futures import ThreadPoolExecutor
-    from math import comb
 
     from .pipeline import _metric_id
     devs = _device_list(devices)
@@ -335,7 +337,7 @@ def build_on_devices(rows, params, metric: str, devices):
     blocks = on(devs[0], lambda: engine.plan_blocks(full[devs[0]][0], params.length,
                                                     params.blocks, params.mismatch))
     ops = DeviceOps()
-    total_units = params.replicates * comb(blocks, params.mismatch)
+    total_units = params.replicates * engine.unit_count(blocks, params.mismatch)
 
     def shard_build(s):
         dev = devs[s]

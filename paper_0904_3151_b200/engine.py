@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import itertools
 import math
+from math import comb
 
 import numpy as np
 import torch
@@ -168,17 +169,46 @@ def masks_for(k: int, d: int):
     return list(itertools.combinations(range(k), d))
 
 
-def units_for(replicates, k: int, d: int):
-    """(replicate index, block bitmask) for every unit, in reference order."""
-    reps, bits = [], []
-    for h in replicates:
-        for m in masks_for(k, d):
+DESIGN_BASE = 10000   # plan codes >= this name a covering design: BASE + 100 v + m
+
+
+def plan_design(plan: int, d: int):
+    """(block count, ordered masked-block bitmasks of one replicate's units,
+    is_design) of a plan code: a block count k' (the complete family of
+    d-subsets, reference order) or DESIGN_BASE + 100 v + m (the library's
+    covering design C(v, m, d), eg_msm_design)."""
+    if plan < DESIGN_BASE:
+        bits = []
+        for m in masks_for(plan, d):
             b = 0
             for blk in m:
                 b |= 1 << blk
-            reps.append(h)
             bits.append(b)
-    return np.asarray(reps, dtype=np.int32), np.asarray(bits, dtype=np.uint64)
+        return plan, np.asarray(bits, dtype=np.uint64), False
+    v, m = divmod(plan - DESIGN_BASE, 100)
+    lib = _native.lib()
+    count = lib.eg_msm_design(v, m, d, None, 0)
+    if count <= 0:
+        raise ValueError(f"no covering design C({v}, {m}, {d}) in the library's table")
+    out = np.zeros(count, dtype=np.uint64)
+    lib.eg_msm_design(v, m, d, out.ctypes.data, count)
+    return v, out, True
+
+
+def unit_count(plan: int, d: int) -> int:
+    """Units per replicate of a plan code."""
+    if plan < DESIGN_BASE:
+        return comb(plan, max(0, d))
+    return len(plan_design(plan, d)[1])
+
+
+def units_for(replicates, k: int, d: int):
+    """(replicate index, block bitmask) for every unit, in reference order
+    (``k``: a block count or a design's plan code)."""
+    _, family, _ = plan_design(k, d)
+    reps = np.repeat(np.asarray(list(replicates), dtype=np.int32), len(family))
+    bits = np.tile(family, len(reps) // max(1, len(family)))
+    return reps, bits
 
 
 def msm_plan(codes: torch.Tensor, length: int, k: int, d: int,
@@ -208,8 +238,12 @@ _last_plan: dict = {}
 
 
 def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps, unit_masks,
-              capacity: int | None = None, full_codes: torch.Tensor | None = None):
+              capacity: int | None = None, full_codes: torch.Tensor | None = None,
+              design=None):
     """Run the MSM units; returns (keys tensor, counts dict).
+
+    ``design`` (covering-design units): the ordered family of masked block
+    sets the unit masks are members of (eg_msm_pairs_design).
 
     ``full_codes`` (strings longer than the kernels' EG_MAX_LENGTH bits):
     ``codes`` is then a prefix view of them; the units emit the pairs within
@@ -226,6 +260,7 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     bb = np.ascontiguousarray(block_bounds, dtype=np.int32)
     ur = np.ascontiguousarray(unit_reps, dtype=np.int32)
     um = np.ascontiguousarray(unit_masks, dtype=np.uint64)
+    dm = None if design is None else np.ascontiguousarray(design, dtype=np.uint64)
     hint_key = (n, length, k, d, reps, len(ur), full_codes is not None)
     if capacity is None:
         capacity = _capacity_hint.get(hint_key)
@@ -244,9 +279,11 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     while True:
         out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         rtag = torch.empty(max(capacity, 1), dtype=torch.int16, device=dev) if defer else None
-        rc = lib.eg_msm_pairs(_p(codes), n, length, reps, bb.ctypes.data, k, d, ur.ctypes.data,
-                              um.ctypes.data, len(ur), _p(out), _p(rtag), capacity,
-                              ctypes_addr(counts), _p(ws), ws.numel(), _stream(dev))
+        rc = lib.eg_msm_pairs_design(_p(codes), n, length, reps, bb.ctypes.data, k, d,
+                                     ur.ctypes.data, um.ctypes.data, len(ur),
+                                     None if dm is None else dm.ctypes.data,
+                                     0 if dm is None else len(dm), _p(out), _p(rtag), capacity,
+                                     ctypes_addr(counts), _p(ws), ws.numel(), _stream(dev))
         if rc == _native.EG_ERR_CAPACITY:
             # the exact total is known now: one more pass with that capacity
             capacity = int(counts[0])
@@ -340,15 +377,19 @@ def msm_candidates(codes: torch.Tensor, length: int, k: int, d: int, *, blocks: 
     info["max_group"] the reference's largest group."""
     from .bitpool import block_partition
     view, lv, kv, full = msm_view(codes, length, k, d)
-    kk = blocks or msm_plan(view, lv, kv, d, oversized_fraction)
-    same = kk == k and full is None and lv == length
+    plan = blocks or msm_plan(view, lv, kv, d, oversized_fraction)
+    kk, family, is_design = plan_design(plan, d)
+    same = kk == k and not is_design and full is None and lv == length
     bounds = block_bounds if (same and block_bounds is not None) else block_partition(lv, kk)
-    ureps, umasks = units_for(range(codes.shape[0]), kk, d)
+    ureps, umasks = units_for(range(codes.shape[0]), plan, d)
     if select is not None:
         sel = np.asarray(select(len(ureps)), dtype=np.int64)
         ureps, umasks = ureps[sel], umasks[sel]
-    keys, info = msm_pairs(view, lv, bounds, d, ureps, umasks, full_codes=full)
+    keys, info = msm_pairs(view, lv, bounds, d, ureps, umasks, full_codes=full,
+                           design=family if is_design else None)
     info["blocks"] = kk
+    info["plan"] = plan
+    info["units"] = int(len(ureps))
     info["reference_blocks"] = same
     return keys, info
 

@@ -62,13 +62,21 @@ class OracleOps:
         # the block count is a cost knob: any k' > d gives the same pairs
         return self.blocks or params.blocks
 
+    def unit_count(self, blocks, mismatch):
+        from paper_0904_3151_b200 import engine
+        return engine.unit_count(blocks, mismatch)
+
     def candidates(self, codes, params, units, blocks):
-        """Pairs owned by `units`: owner = (replicate, canonical mask of the
-        differing blocks) -- the rule the CUDA kernels implement."""
+        """Pairs owned by `units`: owner = (replicate, first member of the
+        plan's family whose masked blocks contain the differing blocks) --
+        for a block count that is the canonical mask; the rule the CUDA
+        kernels implement."""
+        from paper_0904_3151_b200 import engine
         orc = self.orc
         words = [c.numpy().view(np.uint64) for c in codes]
+        blocks, family, _ = engine.plan_design(blocks, params.mismatch)
+        family = [int(f) for f in family]
         bounds = orc.block_partition(params.length, blocks)
-        masks = list(itertools.combinations(range(blocks), params.mismatch))
         blk = np.zeros(params.length, dtype=np.int64)
         for b in range(blocks):
             blk[bounds[b]:bounds[b + 1]] = b
@@ -79,10 +87,12 @@ class OracleOps:
             keep = orc.first_witness(pairs, words[:h], params.mismatch)
             for (i, j) in pairs[keep]:
                 x = int(words[h][i, 0] ^ words[h][j, 0])
-                delta = sorted({int(blk[t]) for t in range(params.length) if x >> t & 1})
-                fill = [b for b in range(blocks) if b not in delta]
-                canon = tuple(sorted(delta + fill[:params.mismatch - len(delta)]))
-                unit = h * len(masks) + masks.index(canon)
+                delta = 0
+                for t in range(params.length):
+                    if x >> t & 1:
+                        delta |= 1 << int(blk[t])
+                owner = next(q for q, f in enumerate(family) if f & delta == delta)
+                unit = h * len(family) + owner
                 if unit in mine:
                     keys.append((int(i) << 32) | int(j))
         return torch.tensor(keys, dtype=torch.int64), {}
@@ -131,7 +141,7 @@ def _worker(rank, world, port, out_path, blocks=None):
     tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("blocks", [None, 3, 6])
+@pytest.mark.parametrize("blocks", [None, 3, 6, 10703])
 def test_two_rank_build_equals_single_process(oracle, tmp_path, blocks):
     """Sharded build == single-process reference, for the reference block
     count and for planned counts k' != k (the pair set is independent of k)."""

@@ -37,7 +37,7 @@ else:
     del x
 n = codes.shape[1]
 blocks = args.blocks or engine.msm_plan(codes, params.length, params.blocks, params.mismatch)
-bounds = block_partition(params.length, blocks)
+bounds = block_partition(params.length, engine.plan_design(blocks, params.mismatch)[0])
 reps, masks = engine.units_for(range(codes.shape[0]), blocks, params.mismatch)
 prof = _native.Profile()
 times = []
