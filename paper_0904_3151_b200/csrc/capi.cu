@@ -263,14 +263,22 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
   // batch i concurrently with the small-tier group kernel of batch i+1:
   // the tails occupy few SMs (a handful of heavy buckets) and would
   // otherwise serialise behind it.
-  static cudaStream_t side[64], tail[64];
+  // Priorities: the partition stream (hist / scan / scatter of the next
+  // batch) and the tail stream outrank the group stream, so their CTAs take
+  // the SM slots the group kernel frees first -- the next batch is ready
+  // when the group kernel ends, and a batch's heavy buckets do not queue
+  // behind the next group kernel.
+  static cudaStream_t side[64], tail[64], part[64];
   static cudaEvent_t ev_scat[64][2], ev_grp[64][2], ev_done[64][2], ev_end[64];
   int dev = 0;
   cudaGetDevice(&dev);
   const bool two = lay.sets == 2;
   if (two && !side[dev]) {
-    EG_CUDA_TRY(cudaStreamCreateWithFlags(&side[dev], cudaStreamNonBlocking));
-    EG_CUDA_TRY(cudaStreamCreateWithFlags(&tail[dev], cudaStreamNonBlocking));
+    int prio_lo = 0, prio_hi = 0;
+    EG_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    EG_CUDA_TRY(cudaStreamCreateWithPriority(&side[dev], cudaStreamNonBlocking, prio_lo));
+    EG_CUDA_TRY(cudaStreamCreateWithPriority(&tail[dev], cudaStreamNonBlocking, prio_hi));
+    EG_CUDA_TRY(cudaStreamCreateWithPriority(&part[dev], cudaStreamNonBlocking, prio_hi));
     for (int i = 0; i < 2; ++i) {
       EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_scat[dev][i], cudaEventDisableTiming));
       EG_CUDA_TRY(cudaEventCreateWithFlags(&ev_grp[dev][i], cudaEventDisableTiming));
@@ -280,11 +288,26 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
   }
   cudaStream_t gs = two ? side[dev] : st;
   cudaStream_t ts = two ? tail[dev] : st;
+  cudaStream_t ps = two ? part[dev] : st;
   if (two) {   // the side streams start after everything already on st
     EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][0], st));
     EG_CUDA_TRY(cudaStreamWaitEvent(gs, ev_scat[dev][0], 0));
     EG_CUDA_TRY(cudaStreamWaitEvent(ts, ev_scat[dev][0], 0));
+    EG_CUDA_TRY(cudaStreamWaitEvent(ps, ev_scat[dev][0], 0));
   }
+#ifdef EG_MSM_TIMELINE
+  std::vector<std::pair<const char *, cudaEvent_t>> tl;
+  auto mark = [&](const char *what, cudaStream_t s) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    tl.push_back({what, e});
+  };
+  mark("start", st);
+#define EG_TL(what, s) mark(what, s)
+#else
+#define EG_TL(what, s)
+#endif
   for (size_t bi = 0; bi < batches.size(); ++bi) {
     const UnitBatch &ub = batches[bi];
     const int si = two ? (int)(bi & 1) : 0;
@@ -292,29 +315,32 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     x.hist_smem = a.hist_smem;
     x.scatter_staged = a.scatter_staged;
     x.gcnt_min = a.gcnt_min;
-    if (two && bi >= 2) EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_done[dev][si], 0));
+    if (two && bi >= 2) EG_CUDA_TRY(cudaStreamWaitEvent(ps, ev_done[dev][si], 0));
     dim3 g1(tiles, ub.count);
     {
-      EG_PROF(PC_MSM_HIST, st);
-      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, st>>>(x, ub);
+      EG_PROF(PC_MSM_HIST, ps);
+      k_msm_hist<W><<<tiles, MSM_NT, smem_hist, ps>>>(x, ub);
     }
     {
-      EG_PROF(PC_MSM_SCAN, st);
-      k_msm_scan<<<ub.count, 1024, 0, st>>>(x);
+      EG_PROF(PC_MSM_SCAN, ps);
+      k_msm_scan<<<ub.count, 1024, 0, ps>>>(x);
     }
     {
-      EG_PROF(PC_MSM_SCATTER, st);
-      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, st>>>(x, ub);
+      EG_PROF(PC_MSM_SCATTER, ps);
+      k_msm_scatter<W><<<g1, MSM_SC_NT, smem_scatter, ps>>>(x, ub);
     }
+    EG_TL("scatter_end", ps);
     if (two) {
-      EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][si], st));
+      EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][si], ps));
       EG_CUDA_TRY(cudaStreamWaitEvent(gs, ev_scat[dev][si], 0));
     }
     dim3 g4(lay.B, ub.count);
+    EG_TL("group_start", gs);
     {
       EG_PROF(PC_MSM_GROUP, gs);
       k_msm_group<W><<<g4, SmallCfg<W>::NT, smem_group, gs>>>(x, ub);
     }
+    EG_TL("group_end", gs);
     if (two) {
       EG_CUDA_TRY(cudaEventRecord(ev_grp[dev][si], gs));
       EG_CUDA_TRY(cudaStreamWaitEvent(ts, ev_grp[dev][si], 0));
@@ -323,10 +349,12 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
       EG_PROF(PC_MSM_SPILL, ts);
       k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, ts>>>(x, ub);
     }
+    EG_TL("medium_end", ts);
     {
       EG_PROF(PC_MSM_SPILL, ts);
       k_msm_spill<W><<<spill_grid, MSM_SPILL_T, 0, ts>>>(x, ub);
     }
+    EG_TL("spill_end", ts);
     {
       EG_PROF(PC_MSM_SPILL, ts);
       k_msm_spill_maxgroup<<<64, 256, 0, ts>>>(x);
@@ -340,6 +368,16 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     EG_CUDA_TRY(cudaEventRecord(ev_end[dev], gs));
     EG_CUDA_TRY(cudaStreamWaitEvent(st, ev_end[dev], 0));
   }
+#ifdef EG_MSM_TIMELINE
+  mark("joined", st);
+  cudaStreamSynchronize(st);
+  for (size_t i = 1; i < tl.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tl[0].second, tl[i].second);
+    fprintf(stderr, "[msm timeline] %-12s %.3f ms\n", tl[i].first, ms);
+  }
+  for (auto &t : tl) cudaEventDestroy(t.second);
+#endif
   return EG_OK;
 }
 
@@ -362,6 +400,7 @@ int eg_set_option(const char *name, long long value) {
     o.msm_blocks = (int)value;
   else if (!strcmp(name, "msm_designs") && (value == 0 || value == 1)) o.msm_designs = (int)value;
   else if (!strcmp(name, "msm_streams") && (value == 1 || value == 2)) o.msm_streams = (int)value;
+  else if (!strcmp(name, "msm_batches") && value >= 0 && value <= 64) o.msm_batches = (int)value;
   else if (!strcmp(name, "verify_wide")) o.verify_wide = value != 0;
   else if (!strcmp(name, "sort_path") && value >= -1 && value <= 1) o.sort_path = (int)value;
   else return arg_error("eg_set_option: unknown option or value out of range");
@@ -1106,6 +1145,8 @@ int eg_msm_pairs_design(const uint64_t *d_codes, int64_t n, int32_t length, int3
   int64_t nbatch = (n_units + lay.U - 1) / lay.U;
   if (lay.sets == 2 && n_units >= 4)
     nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(2, n_units / 2));
+  if (options().msm_batches > 0)
+    nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(options().msm_batches, n_units));
   const int64_t per_batch = nbatch > 0 ? (n_units + nbatch - 1) / nbatch : lay.U;
   for (int64_t u0 = 0; u0 < n_units; u0 += per_batch) {
     UnitBatch ub;

@@ -448,38 +448,6 @@ __device__ __forceinline__ int pair_verdict(const uint64_t (&ca)[W], const uint6
   return 2;
 }
 
-// pair_verdict with the second row read lazily (only the in-kernel
-// cross-replicate rule needs it).
-template <int W>
-__device__ __forceinline__ int pair_verdict_rows(const uint64_t (&ca)[W], const uint64_t (&cb)[W],
-                                                 uint32_t ra, const uint32_t *mrows, uint32_t ib,
-                                                 const MsmArgs &a, const TailTest<W> &tt,
-                                                 const unsigned long long *kept, int rep,
-                                                 const uint8_t *b2b) {
-  uint64_t x[W];
-  int pc = 0;
-  uint64_t keydiff = 0;
-#pragma unroll
-  for (int w = 0; w < W; ++w) {
-    x[w] = ca[w] ^ cb[w];
-    pc += __popcll(x[w]);
-    keydiff |= x[w] & kept[w];
-  }
-  if (keydiff || pc > a.d) return 0;
-  if (!tt.ok(x, pc, b2b, a.k, a.d)) return 0;
-  if (a.out_rep) return 2;
-  const uint32_t rb = mrows[ib];
-  for (int g = 0; g < rep; ++g) {
-    const uint64_t *cg = a.codes + (int64_t)g * a.n * W;
-    int pg = 0;
-#pragma unroll
-    for (int w = 0; w < W; ++w)
-      pg += __popcll(__ldg(cg + (int64_t)ra * W + w) ^ __ldg(cg + (int64_t)rb * W + w));
-    if (pg <= a.d) return 1;
-  }
-  return 2;
-}
-
 // ------------------------------------------------------------------ 4
 // Bucket processing, entirely in shared memory.  An open-addressing table
 // keyed by the 32-bit secondary hash groups the bucket's rows exactly by
@@ -494,6 +462,9 @@ __device__ __forceinline__ int pair_verdict_rows(const uint64_t (&ca)[W], const 
 #endif
 #ifndef EG_GROUP_FILTER
 #define EG_GROUP_FILTER 1
+#endif
+#ifndef EG_PAIR_UNROLL
+#define EG_PAIR_UNROLL 2
 #endif
 #ifndef EG_RANK_ATOMIC32
 #define EG_RANK_ATOMIC32 1
@@ -802,56 +773,117 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   tt.fetch();
   uint32_t my_raw = 0, my_new = 0;
   const uint32_t lane = threadIdx.x & 31;
+  // loop invariants pinned in registers (ptxas otherwise re-reads them from
+  // the constant bank and recomputes the shared window base every visit)
+  uint64_t kp[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    kp[w] = kept[w];
+    asm volatile("" : "+l"(kp[w]));
+  }
+  uint32_t dmax = (uint32_t)a.d;
+  uint32_t mc_s = (uint32_t)__cvta_generic_to_shared(mcodes);
+  asm volatile("" : "+r"(dmax), "+r"(mc_s));
+  constexpr uint32_t CB = 8 * W;   // bytes per code
   while (true) {
     uint32_t c = 0;
     if (lane == 0) c = atomicAdd(&S.chunk, 1u);
     c = __shfl_sync(0xffffffffu, c, 0);
     if (c * 32 >= M) break;
     const uint32_t pos = c * 32 + lane;
-    uint32_t start = 0, len = 0, idx = 0, ra = 0;
+    uint32_t trips = 0, ra = 0, p = 0, p_first = 0, p_end = 0;
     uint64_t ca[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) ca[w] = 0;
     if (pos < M) {
       const uint32_t rr = S.runs[S.mgid[pos]];
-      start = rr >> 16;
-      len = rr & 0xffffu;
-      idx = pos - start;
+      const uint32_t start = rr >> 16, len = rr & 0xffffu, idx = pos - start;
       ra = mrows[pos];
 #pragma unroll
       for (int w = 0; w < W; ++w) ca[w] = mcodes[pos * W + w];
+      // trips of this member: t*2 < len, plus t*2 == len from the lower half
+      trips = (len >> 1) - ((len & 1u) == 0 && idx * 2 >= len ? 1u : 0u);
+      p_first = mc_s + start * CB;
+      p_end = p_first + len * CB;
+      p = mc_s + pos * CB;
     }
-    // trips of this member: t*2 < len, plus t*2 == len from the lower half
-    const uint32_t trips =
-        pos < M ? (len >> 1) - ((len & 1u) == 0 && idx * 2 >= len ? 1u : 0u) : 0u;
-    const uint32_t maxtrips = __reduce_max_sync(0xffffffffu, trips);
-    uint32_t jb = idx;
-    for (uint32_t t = 1; t <= maxtrips; ++t) {
-      if (t <= trips) {
-        if (++jb == len) jb = 0;
-        uint64_t cb[W];
+    // one visit: partner code at shared address q; returns false when the
+    // pair is rejected by the key / Hamming test (the common case)
+    auto reject = [&](uint32_t q, uint64_t (&x)[W], uint32_t &pc) -> bool {
+      uint64_t keydiff = 0;
+      pc = 0;
 #pragma unroll
-        for (int w = 0; w < W; ++w) cb[w] = mcodes[(start + jb) * W + w];
-        const int v = pair_verdict_rows<W>(ca, cb, ra, mrows, start + jb, a, tt, kept, rep, S.b2b);
-        if (v) {
-          my_raw += 1;
-          if (v == 2) {
-            ++my_new;
-            const uint32_t rb = mrows[start + jb];
-            const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
-            const uint32_t so = atomicAdd(&S.nout, 1u);
-            if (so < OUTCAP) {
-              S.outbuf()[so] = key;
-            } else {
-              const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
-              if (slot < a.out_cap) {
-                a.out_keys[slot] = key;
-                if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
-              }
-            }
+      for (int w = 0; w < W; ++w) {
+        uint64_t cbw;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(cbw) : "r"(q + 8 * w));
+        x[w] = ca[w] ^ cbw;
+        pc += __popcll(x[w]);
+        keydiff |= x[w] & kp[w];
+      }
+      return keydiff != 0 || pc > dmax;
+    };
+    // rare: within d on equal keys -- ownership, then the replicate rule
+    auto accept = [&](uint32_t q, const uint64_t (&x)[W], uint32_t pc) {
+      if (!tt.ok(x, (int)pc, S.b2b, a.k, a.d)) return;
+      const uint32_t rb = mrows[(q - mc_s) / CB];
+      int v = 2;
+      if (!a.out_rep) {
+        for (int g = 0; g < rep && v == 2; ++g) {
+          const uint64_t *cg2 = a.codes + (int64_t)g * a.n * W;
+          int pg = 0;
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            pg += __popcll(__ldg(cg2 + (int64_t)ra * W + w) ^ __ldg(cg2 + (int64_t)rb * W + w));
+          if (pg <= a.d) v = 1;
+        }
+      }
+      my_raw += 1;
+      if (v == 2) {
+        ++my_new;
+        const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
+        const uint32_t so = atomicAdd(&S.nout, 1u);
+        if (so < OUTCAP) {
+          S.outbuf()[so] = key;
+        } else {
+          const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
+          if (slot < a.out_cap) {
+            a.out_keys[slot] = key;
+            if (a.out_rep) a.out_rep[slot] = (uint16_t)rep;
           }
         }
       }
+    };
+    // EG_PAIR_UNROLL partners per step: independent load / xor / popcount
+    // chains (the loop is latency-bound, not issue-bound)
+    constexpr int PU = EG_PAIR_UNROLL;
+    for (; trips >= (uint32_t)PU; trips -= PU) {
+      uint32_t q[PU];
+      uint64_t x[PU][W];
+      uint32_t pc[PU];
+      bool any = false;
+      bool rj[PU];
+#pragma unroll
+      for (int i = 0; i < PU; ++i) {
+        p += CB;
+        if (p == p_end) p = p_first;
+        q[i] = p;
+      }
+#pragma unroll
+      for (int i = 0; i < PU; ++i) {
+        rj[i] = reject(q[i], x[i], pc[i]);
+        any |= !rj[i];
+      }
+      if (!any) continue;
+#pragma unroll
+      for (int i = 0; i < PU; ++i)
+        if (!rj[i]) accept(q[i], x[i], pc[i]);
+    }
+    for (; trips; --trips) {
+      p += CB;
+      if (p == p_end) p = p_first;
+      uint64_t x1[W];
+      uint32_t pc1;
+      if (!reject(p, x1, pc1)) accept(p, x1, pc1);
     }
   }
   if (my_raw) atomicAdd(&S.raw, my_raw);

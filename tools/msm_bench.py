@@ -23,7 +23,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--blocks", type=int, default=0)
+ap.add_argument("--opt", action="append", default=[], help="name=value for eg_set_option")
 args = ap.parse_args()
+for o in args.opt:
+    k, v = o.split("=")
+    assert _native.lib().eg_set_option(k.encode(), int(v)) == 0, o
 cfg = CONFIGS[args.config]
 params = bench.params_for(cfg, eg)
 data, _ = bench.make_inputs(args.config)

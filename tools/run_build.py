@@ -19,7 +19,11 @@ from paper_0904_3151_b200.workloads import CONFIGS  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--plan", type=int, default=0, help="force a block count / design plan code")
 args = ap.parse_args()
+if args.plan:
+    from paper_0904_3151_b200 import _native as _nat
+    assert _nat.lib().eg_set_option(b"msm_blocks", args.plan) == 0
 cfg = CONFIGS[args.config]
 params = bench.params_for(cfg, eg)
 data, _ = bench.make_inputs(args.config)
