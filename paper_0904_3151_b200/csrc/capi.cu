@@ -400,6 +400,7 @@ int eg_set_option(const char *name, long long value) {
     o.msm_blocks = (int)value;
   else if (!strcmp(name, "msm_designs") && (value == 0 || value == 1)) o.msm_designs = (int)value;
   else if (!strcmp(name, "msm_streams") && (value == 1 || value == 2)) o.msm_streams = (int)value;
+  else if (!strcmp(name, "plan_debug")) o.plan_debug = value != 0;
   else if (!strcmp(name, "msm_batches") && value >= 0 && value <= 64) o.msm_batches = (int)value;
   else if (!strcmp(name, "verify_wide")) o.verify_wide = value != 0;
   else if (!strcmp(name, "sort_path") && value >= -1 && value <= 1) o.sort_path = (int)value;
@@ -791,7 +792,7 @@ int eg_msm_design(int32_t v, int32_t m, int32_t t, uint64_t *h_masks, int32_t ca
 
 constexpr int PLAN_REF_MAX = 4096;     // reference masks probed for the oversize check
 constexpr int PLAN_PER_K = 12;         // masks probed per candidate block count
-constexpr int PLAN_PER_DESIGN = 8;     // members probed per candidate design
+constexpr int PLAN_PER_DESIGN = 16;    // members probed per candidate design
 constexpr int PLAN_MIN_ROWS = 65536;   // smaller pools keep the reference blocks
 
 size_t eg_msm_plan_workspace(int32_t length, int32_t k, int32_t d) {
@@ -897,7 +898,7 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     for (const DesignEntry &e : kDesigns) {
       if (e.t != d || e.v > kmax) continue;
       const double kept_bits = (double)length * (e.v - e.m) / e.v;
-      if (kept_bits < lgn - 2.0 || kept_bits > lgn + 14.0) continue;
+      if (kept_bits < lgn - 1.0 || kept_bits > lgn + 10.0) continue;
       const int code = PLAN_DESIGN_BASE + 100 * e.v + e.m;
       const int np = std::min<int>(e.count, PLAN_PER_DESIGN);
       for (int i = 0; i < np; ++i)
@@ -953,8 +954,11 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   } else if (oversized_fraction * SR < 200 || rmax >= 0.5 * oversized_fraction * SR) {
     return EG_OK;
   }
-  const double ce = 18.5e-12;   // s per row per unit (measured, cfg3)
-  const double cp = 3.0e-12;    // s per visited in-group pair
+  // s per row per unit and per visited in-group pair: marginal costs fitted
+  // on config 3 over the complete and the covering designs (tools/
+  // design_sweep.sh; the member-parallel pair loop made visits cheap)
+  const double ce = 14.0e-12;
+  const double cp = 1.2e-12;
   const double scale = S > 1 ? (double)n * (double)(n - 1) / ((double)S * (double)(S - 1)) : 0;
   double best = -1, ref_cost = -1;
   int best_k = k;
@@ -967,6 +971,9 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
     const double units =
         kk >= PLAN_DESIGN_BASE ? design_units[kk - PLAN_DESIGN_BASE] : comb_sat(kk, d);
     const double cost = units * ((double)n * ce + est_pairs * cp);
+    if (options().plan_debug)
+      fprintf(stderr, "[msm plan] code %d units %.0f probes %d est_pairs/unit %.3g cost %.3f ms\n",
+              kk, units, cnt, est_pairs, cost * 1e3);
     if (kk == k) ref_cost = cost;
     if (best < 0 || cost < best) {
       best = cost;

@@ -56,6 +56,7 @@ struct Options {
   int msm_blocks = 0;            // > 0: force the block count (or a design's plan code); < 0: keep the reference's
   int msm_designs = 1;           // 0: the plan considers complete designs only
   int msm_streams = 2;           // 1: batches run on the caller's stream only
+  int plan_debug = 0;            // 1: eg_msm_plan prints its candidates to stderr
   int msm_batches = 0;           // > 0: at least this many launch batches
   int verify_wide = 0;           // 1: warp-per-pair verify even for dim <= 128
   int sort_path = -1;            // -1 auto, 0 onesweep, 1 classic LSD passes

@@ -503,11 +503,13 @@ def test_sharded_path_over_nccl_single_rank(eg, oracle):
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("blocks", [4, 5, 7, 9, 16, 48])
+@pytest.mark.parametrize("blocks", [4, 5, 7, 9, 16, 48, 10604, 10804, 11105, 11106, 11406])
 def test_forced_block_counts_same_pairs(eg, oracle, manifest, native_options, blocks):
-    """The pair set does not depend on the block count the units run with
-    (hamming_join.py:300-375): every forced k' > d reproduces the
-    reference-k pairs, per-replicate raw/new counts and edges."""
+    """The pair set does not depend on the units' partition
+    (hamming_join.py:300-375): every forced k' > d -- and every covering
+    design of the library's table (plan codes 10000 + 100 v + m, first-member
+    ownership) -- reproduces the reference-k pairs, per-replicate raw/new
+    counts and edges."""
     native_options(msm_blocks=blocks)
     rng = np.random.default_rng(blocks)
     n, length, k, d = 5000, 48, 12, 3
@@ -521,7 +523,8 @@ def test_forced_block_counts_same_pairs(eg, oracle, manifest, native_options, bl
     g = golden("small_build")
     rec = manifest["small_build"]
     pp = rec["params"]
-    if pp["mismatch"] < blocks <= pp["length"]:
+    v = blocks if blocks < 10000 else (blocks - 10000) // 100
+    if pp["mismatch"] < v <= pp["length"]:
         params = eg.MsmParams(epsilon=pp["epsilon"], gamma=1e-3, length=pp["length"],
                               mismatch=pp["mismatch"], blocks=pp["blocks"],
                               replicates=pp["replicates"], seed=pp["seed"])
@@ -567,7 +570,24 @@ def test_block_plan_keeps_reference_when_oversized(eg, caplog):
     assert len(codes_pairs) >= (n // 3) * (n // 3 - 1) // 2
 
 
-@pytest.mark.parametrize("blocks", [4, 5, 6])
+@pytest.mark.parametrize("plan,length,d", [(10703, 100, 2), (10905, 100, 2), (11304, 64, 2),
+                                           (10906, 130, 4), (11207, 64, 4)])
+def test_design_units_wide_codes(eg, oracle, native_options, plan, length, d):
+    """Covering-design units on 2- and 3-word codes and for d = 2 and 4."""
+    native_options(msm_blocks=plan)
+    rng = np.random.default_rng(plan)
+    n = 6000
+    base = (rng.random((n // 4, length)) < 0.4).astype(np.uint8)
+    bits = base[rng.integers(0, base.shape[0], n)] ^ (rng.random((n, length)) < 0.012)
+    words = pack_bits(bits.astype(np.uint8))
+    pool = eg.BitStringPool(words, length).partitioned(8)
+    got = eg.enumerate_pairs(pool, d)
+    want, _ = oracle.enumerate_pairs(words, length, pool.block_bounds, d)
+    assert len(want) > 1000
+    np.testing.assert_array_equal(got.array, want)
+
+
+@pytest.mark.parametrize("blocks", [4, 5, 6, 10604, 10705])
 def test_coarse_blocks_all_tiers_deterministic(eg, oracle, native_options, blocks):
     """Coarse forced block counts on skewed bits send buckets through every
     tier (small, pair-heavy -> medium, giant -> tiles); the pair set must

@@ -94,6 +94,36 @@ def test_canonical_mask_rule_matches_first_witness():
             assert tuple(sorted(delta | set(fill))) == first
 
 
+def test_design_table_covers_every_subset():
+    """Every covering design of the library's table (eg_msm_design): members
+    mask m of the v blocks, and every t-subset of the blocks lies inside a
+    member -- so every pair differing in <= t blocks shares a masked key in
+    some unit, and the first such member owns it exactly once."""
+    import itertools
+    found = 0
+    for t in (2, 3, 4):
+        for v in range(t + 2, 17):
+            for m in range(t + 1, v):
+                try:
+                    vv, fam, is_design = engine.plan_design(engine.DESIGN_BASE + 100 * v + m, t)
+                except ValueError:
+                    continue
+                found += 1
+                fam = [int(f) for f in fam]
+                assert vv == v and is_design and len(fam) == engine.unit_count(
+                    engine.DESIGN_BASE + 100 * v + m, t)
+                assert len(fam) < len(list(itertools.combinations(range(v), t)))
+                assert all(bin(f).count("1") == m and f < (1 << v) for f in fam)
+                for c in itertools.combinations(range(v), t):
+                    s = sum(1 << b for b in c)
+                    owners = [q for q, f in enumerate(fam) if f & s == s]
+                    assert owners, (v, m, t, c)
+    assert found >= 20
+    reps, bits = engine.units_for([0, 1], engine.DESIGN_BASE + 804, 3)
+    assert len(bits) == 28 and reps.tolist() == [0] * 14 + [1] * 14
+    assert (bits[:14] == bits[14:]).all()
+
+
 def test_pair_key_round_trip():
     pairs = np.array([[0, 1], [5, 9], [2**31, 2**32 - 1]], dtype=np.int64)
     np.testing.assert_array_equal(engine.keys_to_pairs(engine.pairs_to_keys(pairs)), pairs)
