@@ -88,16 +88,17 @@ def params_for(cfg, eg):
                         replicates=cfg.replicates, seed=cfg.seed)
 
 
-def sort_bytes_per_unit(n: int, cfg, blocks: int | None = None) -> int:
+def sort_bytes_per_unit(n: int, cfg, blocks: int | None = None, masked: int | None = None) -> int:
     """B_sort = n (8W + P * 2 (kb + 4)), kb = P = ceil(kappa/8),
     kappa = masked-key bits of a unit under ``blocks`` blocks (the planned
     block count; the reference's ``cfg.blocks`` by default)."""
     k = blocks or cfg.blocks
     W = max(1, -(-cfg.length // 64))
     base, rem = divmod(cfg.length, k)
-    # kappa = length - the d narrowest blocks (worst case over the masks)
+    # kappa = length - the narrowest masked blocks (worst case over the
+    # masks): d of them, or m for the units of a covering design C(k, m, d)
     kappa = cfg.length - sum(sorted([base + (1 if b < rem else 0) for b in range(k)])
-                             [:cfg.mismatch])
+                             [:masked or cfg.mismatch])
     kb = -(-kappa // 8)
     return n * (8 * W + kb * 2 * (kb + 4))
 
@@ -519,7 +520,11 @@ def main():
     peak, peak_kind = peaks()
     counts = distributed.last_counts(last) or {}
     blocks = counts.get("blocks") or cfg.blocks
-    units_total = cfg.replicates * math.comb(blocks, cfg.mismatch)
+    plan = counts.get("plan") or blocks
+    # a covering design's units mask m >= d blocks each (plan code 10000 + 100 v + m)
+    masked = (plan - 10000) % 100 if plan >= 10000 else cfg.mismatch
+    from paper_0904_3151_b200 import engine as _engine
+    units_total = cfg.replicates * _engine.unit_count(plan, cfg.mismatch)
     units_mine = len(distributed.my_units(units_total, world, rank))
     traffic_tab = {}
     try:
@@ -548,11 +553,14 @@ def main():
     m_edges = int(counts.get("edges") or 0)
     stages["msm"] = entry(
         "msm", "eg_msm_pairs: MSM unit pipeline (hist+scan+scatter+group+tiers) over the "
-        "build's units", "msm_stage", sort_bytes_per_unit(n, cfg, blocks) * units_mine,
-        {"alg_bytes_per_unit": sort_bytes_per_unit(n, cfg, blocks), "blocks": blocks,
+        "build's units", "msm_stage", sort_bytes_per_unit(n, cfg, blocks, masked) * units_mine,
+        {"alg_bytes_per_unit": sort_bytes_per_unit(n, cfg, blocks, masked), "blocks": blocks,
+         "plan": plan, "masked_blocks_per_unit": masked,
          "units_per_launch": units_mine,
-         "units_definition": "B_sort = n (8W + P 2 (kb + 4)), kb = P = ceil(kappa/8) at the "
-                             "planned block count"})
+         "units_reference": cfg.replicates * math.comb(cfg.blocks, cfg.mismatch),
+         "units_definition": "B_sort = n (8W + P 2 (kb + 4)), kb = P = ceil(kappa/8) for the "
+                             "planned units (block count, or covering design C(v, m, d): "
+                             "plan = 10000 + 100 v + m)"})
     npass = 2 * -(-max(1, (n - 1).bit_length()) // 8)
     stages["sort"] = entry(
         "sort", "eg_sort_pair_keys: onesweep LSD over the candidate keys", "sort_stage",

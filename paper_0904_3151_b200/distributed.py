@@ -203,7 +203,7 @@ def build_step(x, params, metric: str, world: int, rank: int, ops=None,
     blocks = broadcast_int(ops.plan(codes, params) if rank == 0 else 0, rank, codes.device)
     units = my_units(params.replicates * ops.unit_count(blocks, params.mismatch), world, rank)
     keys, info = ops.candidates(codes, params, units, blocks)
-    info = dict(info, blocks=blocks)
+    info = dict(info, plan=blocks)
     keys = ops.sort(keys, n)
     ek, ed = ops.verify(x, norms, keys, metric, params.epsilon)
     mk, md = gather_edges(ek, ed, world, rank, ops, n)
@@ -231,7 +231,8 @@ def last_counts(res):
     keys = res.get("keys")
     return {"candidates": info.get("emitted"), "raw": info.get("raw"), "new": info.get("new"),
             "edges": int(keys.numel()) if keys is not None else None,
-            "max_group": info.get("max_group"), "blocks": info.get("blocks")}
+            "max_group": info.get("max_group"), "blocks": info.get("blocks"),
+            "plan": info.get("plan"), "units": info.get("units")}
 
 
 # ------------------------------------------------ one process, many devices
