@@ -516,7 +516,8 @@ constexpr unsigned long long HG_EMPTY = ~0ull;
 
 // Optional per-bucket counters (compile with -DEG_MSM_STATS=1): buckets
 // reaching the group stage, rows, filter candidates, groups, grouped rows,
-// in-group pair visits.  Read with eg_debug_msm_stats.
+// in-group pair visits, buckets re-queued for too many groups / too many
+// grouped rows.  Read with eg_debug_msm_stats.
 #ifndef EG_MSM_STATS
 #define EG_MSM_STATS 0
 #endif
@@ -675,6 +676,9 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     return true;
   }
   if (R > GCAP) {
+#if EG_MSM_STATS
+    if (threadIdx.x == 0) atomicAdd(&g_msm_stats[6], 1ull);   // re-queued: too many groups
+#endif
     __syncthreads();
     return false;
   }
@@ -705,6 +709,9 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   unsigned long long tot;
   unsigned long long run = block_exclusive_scan64<NT>(loc, tot, S.sw);
   if ((uint32_t)(tot >> 32) > MCAP) {     // uniform: too many grouped rows
+#if EG_MSM_STATS
+    if (threadIdx.x == 0) atomicAdd(&g_msm_stats[7], 1ull);   // re-queued: too many grouped rows
+#endif
     __syncthreads();
     return false;
   }

@@ -653,14 +653,18 @@ def test_radix_sort_kernels(eg, native_options, classic):
 
 # --------------------------------------------------------------- boundary
 
-def test_build_graph_devices_invariance(eg):
+@pytest.mark.parametrize("plan", [0, 10804])
+def test_build_graph_devices_invariance(eg, native_options, plan):
     """build_graph(devices=...) shards the units over the listed devices
     (one process); the edge list is bit-identical for any device list
     (mirror of the reference's thread-count contract,
     tests/test_pipeline.py:130-135).  A repeated device runs its shards one
-    after another, which exercises the sharded path on one GPU."""
+    after another, which exercises the sharded path on one GPU.  plan =
+    10804: the units of the covering design C(8,4,3), dealt over the shards."""
     import torch
     from paper_0904_3151_b200 import workloads
+    if plan:
+        native_options(msm_blocks=plan)
     x = workloads.cfg3_points(30_000, planted_rows=3_000)
     params = eg.MsmParams(0.05, 1e-6, 48, 3, 12, 3, 0)
     one = eg.build_graph(x, params)

@@ -9,7 +9,6 @@ import argparse
 import os
 import sys
 import time
-from math import comb
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np  # noqa: E402
@@ -24,7 +23,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--world", type=int, default=8)
 ap.add_argument("--config", default="cfg3")
 ap.add_argument("--reps", type=int, default=5)
-ap.add_argument("--ranks", type=int, default=3)
+ap.add_argument("--ranks", type=int, default=8)
+ap.add_argument("--nvlink-gbs", type=float, default=700.0,
+                help="effective all-gather bandwidth per GPU (NVLink 5: 900 GB/s per direction)")
+ap.add_argument("--coll-latency-us", type=float, default=20.0)
 a = ap.parse_args()
 cfg = CONFIGS[a.config]
 params = bench.params_for(cfg, eg)
@@ -35,6 +37,17 @@ full_codes, _ = engine.project_codes(x, engine.validate_rows(x), params.length, 
                                      list(range(1, params.replicates + 1)))
 full_norms = engine.validate_rows(x)
 torch.cuda.synchronize()
+# single-GPU build in the same process (the denominator of the speed-up)
+one = []
+for _ in range(a.reps + 2):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    distributed.build_step(x, params, cfg.metric, 1, 0)
+    e1.record()
+    torch.cuda.synchronize()
+    one.append(e0.elapsed_time(e1))
+one_ms = min(one[2:])
+totals, edge_counts = [], []
 for r in range(min(a.world, a.ranks)):
     best = None
     for _ in range(a.reps):
@@ -46,7 +59,8 @@ for r in range(min(a.world, a.ranks)):
         e[1].record()
         blocks = ops.plan(full_codes, params)
         e[2].record()
-        units = distributed.my_units(params.replicates * comb(blocks, params.mismatch), a.world, r)
+        units = distributed.my_units(params.replicates * ops.unit_count(blocks, params.mismatch),
+                                     a.world, r)
         keys, info = ops.candidates(full_codes, params, units, blocks)
         e[3].record()
         keys = ops.sort(keys, n)
@@ -60,3 +74,18 @@ for r in range(min(a.world, a.ranks)):
     print(f"world={a.world} rank={r} units={len(units)} total={sum(best):.3f} ms  "
           f"project={best[0]:.3f} plan={best[1]:.3f} msm={best[2]:.3f} sort={best[3]:.3f} "
           f"verify={best[4]:.3f} edges={ek.numel()}", flush=True)
+    totals.append(sum(best))
+    edge_counts.append(int(ek.numel()))
+# collectives of distributed.build_step, modelled (no second GPU here): one
+# all-gather of codes + norms, an 8-byte plan broadcast, one gather of the
+# ranks' sorted edge runs to rank 0 and its merge rounds
+W = full_codes.shape[2]
+gather_bytes = (a.world - 1) / a.world * (params.replicates * n * W * 8 + n * 8)
+edge_bytes = sum(edge_counts) / max(1, len(edge_counts)) * (a.world - 1) * 16
+coll_ms = (gather_bytes + edge_bytes) / (a.nvlink_gbs * 1e9) * 1e3 + 3 * a.coll_latency_us / 1e3
+merge_ms = 0.02 * max(1, (a.world - 1).bit_length())
+crit = max(totals) + coll_ms + merge_ms
+print(f"single GPU {one_ms:.3f} ms; world={a.world}: slowest rank {max(totals):.3f} ms + collectives "
+      f"{coll_ms:.3f} ms ({(gather_bytes + edge_bytes) / 1e6:.1f} MB at {a.nvlink_gbs:.0f} GB/s, "
+      f"3 x {a.coll_latency_us:.0f} us) + merge {merge_ms:.3f} ms = {crit:.3f} ms -> modelled speed-up "
+      f"{one_ms / crit:.2f}x")
