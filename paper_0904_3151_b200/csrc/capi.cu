@@ -860,9 +860,14 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   const int nref_probes = (int)probe_k.size();
   // candidates: d < k' <= k + 2 (finer blocks than the reference's only pay
   // off marginally; coarser ones are where skewed or clustered codes win)
+  const double lgn = std::log2((double)n);
+  auto width_fits = [&](double kept_bits) {   // key widths worth a probe
+    return kept_bits >= lgn - 1.0 && kept_bits <= lgn + 10.0;
+  };
   for (int kk = d + 1; kk <= std::min(kmax, k + 2); ++kk) {
     const double units = comb_sat(kk, d);
     if (units > 8192) break;
+    if (kk != k && !width_fits((double)length * (kk - d) / kk)) continue;
     if (units <= PLAN_PER_K) {
       std::vector<int> c(d);
       for (int i = 0; i < d; ++i) c[i] = i;
@@ -897,11 +902,9 @@ int eg_msm_plan(const uint64_t *d_codes, int64_t n, int32_t length, int32_t k, i
   // design of similar key width; PLAN_PER_DESIGN members probed each
   std::vector<double> design_units;      // by plan code - PLAN_DESIGN_BASE
   if (d >= 1 && options().msm_designs) {
-    const double lgn = std::log2((double)n);
     for (const DesignEntry &e : kDesigns) {
       if (e.t != d || e.v > kmax) continue;
-      const double kept_bits = (double)length * (e.v - e.m) / e.v;
-      if (kept_bits < lgn - 1.0 || kept_bits > lgn + 10.0) continue;
+      if (!width_fits((double)length * (e.v - e.m) / e.v)) continue;
       const int code = PLAN_DESIGN_BASE + 100 * e.v + e.m;
       const int np = std::min<int>(e.count, PLAN_PER_DESIGN);
       for (int i = 0; i < np; ++i)

@@ -16,11 +16,11 @@
 
 namespace eg {
 
-constexpr int PLAN_SAMPLE = 12288;         // rows per cost probe (max)
+constexpr int PLAN_SAMPLE = 6144;          // rows per cost probe (max)
 constexpr int PLAN_REF_SAMPLE = 2048;      // rows per oversize probe (max)
-constexpr int PLAN_TABLE = 16384;          // load factor <= 0.75
+constexpr int PLAN_TABLE = 8192;           // load factor <= 0.75; 96 KB: two probe CTAs per SM
 #ifndef EG_PLAN_NT
-#define EG_PLAN_NT 1024   // 12 sampled rows per thread: the probe is latency-bound (106 -> 77 us)
+#define EG_PLAN_NT 1024   // 6 sampled rows per thread: the probe is latency-bound
 #endif
 constexpr int PLAN_NT = EG_PLAN_NT;
 constexpr uint64_t PLAN_SALT = 0x6a09e667f3bcc909ULL;
