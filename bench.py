@@ -558,6 +558,12 @@ def main():
          "plan": plan, "masked_blocks_per_unit": masked,
          "units_per_launch": units_mine,
          "units_reference": cfg.replicates * math.comb(cfg.blocks, cfg.mismatch),
+         # the same call expressed on the reference's own C(k, d) masks (what a
+         # sort-per-mask build of this configuration would move): the plan
+         # removes work, it does not move bytes faster -- reported beside the
+         # planned-units figure, never instead of it
+         "reference_units_bytes": sort_bytes_per_unit(n, cfg) * cfg.replicates *
+                                  math.comb(cfg.blocks, cfg.mismatch),
          "units_definition": "B_sort = n (8W + P 2 (kb + 4)), kb = P = ceil(kappa/8) for the "
                              "planned units (block count, or covering design C(v, m, d): "
                              "plan = 10000 + 100 v + m)"})
