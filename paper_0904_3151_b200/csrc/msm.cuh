@@ -746,9 +746,20 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
       const uint32_t og = (uint32_t)(S.tab()[slr[j] >> 16] >> 32);
       slr[j] = (og & 0xffff0000u) | ((og & 0xffffu) + (slr[j] & 0xffffu));
     }
+  // Overlay layout sized by the bucket's own member count M (uniform): M
+  // codes, M rows, and everything behind them stages emitted pairs -- a
+  // dense pool (config 5: ~1700 pairs per bucket) then rarely overflows
+  // into per-pair reservations on the global output counter.
+  constexpr bool OVL = HGroupSmem<W, CAP, NT, MDIV>::OVERLAY;
+  const uint32_t Mrows = (uint32_t)(tot >> 32);
   uint64_t *mcodes = S.codes();
-  uint32_t *mrows = S.members();
-  if (HGroupSmem<W, CAP, NT, MDIV>::OVERLAY) __syncthreads();
+  uint32_t *mrows = OVL ? reinterpret_cast<uint32_t *>(S.big + (size_t)8 * W * Mrows) : S.members();
+  const uint32_t out_off = ((uint32_t)(8 * W + 4) * Mrows + 7u) & ~7u;
+  unsigned long long *const obuf =
+      OVL ? reinterpret_cast<unsigned long long *>(S.big + out_off) : S.outbuf();
+  const uint32_t ocap =
+      OVL ? (uint32_t)((HGroupSmem<W, CAP, NT, MDIV>::TAB_BYTES - out_off) / 8) : OUTCAP;
+  if (OVL) __syncthreads();
 #pragma unroll
   for (int j = 0; j < PT; ++j) {
     if (grouped >> j & 1) {
@@ -849,8 +860,8 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
         ++my_new;
         const unsigned long long key = ((unsigned long long)min(ra, rb) << 32) | max(ra, rb);
         const uint32_t so = atomicAdd(&S.nout, 1u);
-        if (so < OUTCAP) {
-          S.outbuf()[so] = key;
+        if (so < ocap) {
+          obuf[so] = key;
         } else {
           const unsigned long long slot = atomicAdd(&a.ctr[0], 1ull);
           if (slot < a.out_cap) {
@@ -896,7 +907,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
   if (my_raw) atomicAdd(&S.raw, my_raw);
   if (my_new) atomicAdd(&S.neu, my_new);
   __syncthreads();
-  const uint32_t nst = min(S.nout, OUTCAP);
+  const uint32_t nst = min(S.nout, ocap);
   if (threadIdx.x == 0) {
     if (S.raw) atomicAdd(&a.ctr[3 + rep], (unsigned long long)S.raw);
     if (S.neu) atomicAdd(&a.ctr[3 + a.reps + rep], (unsigned long long)S.neu);
@@ -908,7 +919,7 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     const unsigned long long base = S.obase;
     for (uint32_t i = threadIdx.x; i < nst; i += NT) {
       if (base + i < a.out_cap) {
-        a.out_keys[base + i] = S.outbuf()[i];
+        a.out_keys[base + i] = obuf[i];
         if (a.out_rep) a.out_rep[base + i] = (uint16_t)rep;
       }
     }
