@@ -350,7 +350,10 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     }
     {
       EG_PROF(PC_MSM_SPILL, ts);
-      k_msm_medium<W><<<(unsigned)num_sms(), MediumCfg<W>::NT, smem_medium, ts>>>(x, ub);
+      // persistent CTAs: as many as are resident (two per SM when the
+      // tier's shared memory fits twice)
+      const unsigned per_sm = smem_medium * 2 + 2048 <= (size_t)227 * 1024 ? EG_MEDIUM_MINCTAS : 1;
+      k_msm_medium<W><<<(unsigned)num_sms() * per_sm, MediumCfg<W>::NT, smem_medium, ts>>>(x, ub);
     }
     EG_TL("medium_end", ts);
     {

@@ -1022,7 +1022,10 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
 // Medium buckets (SmallCfg::CAP < s <= MediumCfg::CAP) from the spill list,
 // persistent CTAs.
 template <int W>
-__global__ void __launch_bounds__(MediumCfg<W>::NT) k_msm_medium(
+#ifndef EG_MEDIUM_MINCTAS
+#define EG_MEDIUM_MINCTAS 2   // two 512-thread CTAs per SM where shared memory allows (W <= 2)
+#endif
+__global__ void __launch_bounds__(MediumCfg<W>::NT, EG_MEDIUM_MINCTAS) k_msm_medium(
     const __grid_constant__ MsmArgs a, const __grid_constant__ UnitBatch ub) {
   extern __shared__ __align__(16) unsigned char smraw[];
   using Smem = HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>;
