@@ -564,6 +564,10 @@ def main():
          # planned-units figure, never instead of it
          "reference_units_bytes": sort_bytes_per_unit(n, cfg) * cfg.replicates *
                                   math.comb(cfg.blocks, cfg.mismatch),
+         "note": "algorithmic bytes follow the planned units: a covering design emits the same "
+                 "pair set from fewer, narrower-keyed units, so the bytes charged fall faster "
+                 "than the time (DESIGN.md section 4 table); the stage is latency-bound in "
+                 "k_msm_group, its DRAM traffic is in `traffic`",
          "units_definition": "B_sort = n (8W + P 2 (kb + 4)), kb = P = ceil(kappa/8) for the "
                              "planned units (block count, or covering design C(v, m, d): "
                              "plan = 10000 + 100 v + m)"})
