@@ -227,7 +227,7 @@ static MsmLayout msm_layout(int64_t n, int reps) {
   b += ws_bytes(EG_MAX_LENGTH, 1);                // bit2blk
   b += ws_bytes(3 + 2 * (size_t)reps, 8);         // counters
   b += ws_bytes((size_t)l.U * (l.B + 1) * 9, 4);  // spill list (<= 3 entries/bucket)
-  b += ws_bytes(1, 8);                            // spill counter
+  b += ws_bytes(2, 8);                            // spill counters
   l.bytes = (b + 4096) * l.sets;
   return l;
 }
@@ -318,12 +318,14 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     x.hist_smem = a.hist_smem;
     x.scatter_staged = a.scatter_staged;
     x.gcnt_min = a.gcnt_min;
+    x.small_cap = SmallCfg<W>::CAP;
     if (two && bi >= 2) EG_CUDA_TRY(cudaStreamWaitEvent(ps, ev_done[dev][si], 0));
     dim3 g1(tiles, ub.count);
     {
       EG_PROF(PC_MSM_HIST, ps);
       k_msm_hist<W><<<tiles, MSM_NT, smem_hist, ps>>>(x, ub);
     }
+    EG_CUDA_TRY(cudaMemsetAsync(x.spill_ctr, 0, 16, ps));   // spill list reset for this batch
     {
       EG_PROF(PC_MSM_SCAN, ps);
       k_msm_scan<<<ub.count, 1024, 0, ps>>>(x);
@@ -336,6 +338,15 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     if (two) {
       EG_CUDA_TRY(cudaEventRecord(ev_scat[dev][si], ps));
       EG_CUDA_TRY(cudaStreamWaitEvent(gs, ev_scat[dev][si], 0));
+    }
+    // persistent medium-tier CTAs: as many as are resident (two per SM when
+    // the tier's shared memory fits twice)
+    const unsigned per_sm = smem_medium * 2 + 2048 <= (size_t)227 * 1024 ? EG_MEDIUM_MINCTAS : 1;
+    const unsigned medium_grid = (unsigned)num_sms() * per_sm;
+    if (two) EG_CUDA_TRY(cudaStreamWaitEvent(ts, ev_scat[dev][si], 0));
+    {   // oversized buckets: beside the small tier, not behind it
+      EG_PROF(PC_MSM_SPILL, ts);
+      k_msm_medium<W><<<medium_grid, MediumCfg<W>::NT, smem_medium, ts>>>(x, ub, 0);
     }
     dim3 g4(lay.B, ub.count);
     EG_TL("group_start", gs);
@@ -350,10 +361,7 @@ static int msm_run(MsmArgs *sets, const MsmLayout &lay, const std::vector<UnitBa
     }
     {
       EG_PROF(PC_MSM_SPILL, ts);
-      // persistent CTAs: as many as are resident (two per SM when the
-      // tier's shared memory fits twice)
-      const unsigned per_sm = smem_medium * 2 + 2048 <= (size_t)227 * 1024 ? EG_MEDIUM_MINCTAS : 1;
-      k_msm_medium<W><<<(unsigned)num_sms() * per_sm, MediumCfg<W>::NT, smem_medium, ts>>>(x, ub);
+      k_msm_medium<W><<<medium_grid, MediumCfg<W>::NT, smem_medium, ts>>>(x, ub, 1);
     }
     EG_TL("medium_end", ts);
     {
@@ -1143,7 +1151,7 @@ int eg_msm_pairs_design(const uint64_t *d_codes, int64_t n, int32_t length, int3
     x.elems = ar.take<uint64_t>((size_t)lay.U * n);
     x.gcnt = ar.take<uint32_t>((size_t)lay.U * n);
     x.spill = ar.take<uint32_t>((size_t)lay.U * (lay.B + 1) * 9);
-    x.spill_ctr = ar.take<unsigned long long>(1);
+    x.spill_ctr = ar.take<unsigned long long>(2);
     if (!x.counts || !x.starts || !x.cursor || !x.elems || !x.gcnt || !x.spill || !x.spill_ctr) {
       set_error("eg_msm_pairs: workspace too small (%zu < %zu)", workspace_bytes, lay.bytes);
       return EG_ERR_WORKSPACE;

@@ -97,7 +97,9 @@ struct MsmArgs {
   unsigned long long out_cap;
   unsigned long long *ctr;       // [0] emitted, [1] max group, [2] unused,
                                  // [3..3+reps) raw, [3+reps..) new
-  unsigned long long *spill_ctr; // [0] entries on this scratch set's spill list
+  unsigned long long *spill_ctr; // [0] entries on this scratch set's spill list,
+                                 // [1] how many of them k_msm_scan listed (oversized buckets)
+  int small_cap;                 // SmallCfg<W>::CAP: larger buckets are listed by k_msm_scan
   uint32_t *spill;               // [MAXU * (B+1)][3]: unit slot, start, size
   int64_t spill_cap;
   int gcnt_min;                  // spilled buckets above this size count groups
@@ -201,11 +203,21 @@ __global__ void __launch_bounds__(1024) k_msm_scan(const __grid_constant__ MsmAr
       st[b] = run;
       cur[b] = run;
       cnt[b] = 0;
+      // buckets above the small tier's capacity are known here, before any
+      // grouping: listed now, the medium tier takes them while the small
+      // tier runs instead of after it (spill_ctr was zeroed before this kernel)
+      if (c > (uint32_t)a.small_cap) {
+        const unsigned long long slot = atomicAdd(&a.spill_ctr[0], 1ull);
+        if ((int64_t)slot < a.spill_cap) {
+          a.spill[slot * 3 + 0] = (uint32_t)u;
+          a.spill[slot * 3 + 1] = run;
+          a.spill[slot * 3 + 2] = c;
+        }
+      }
       run += c;
     }
   }
   if (threadIdx.x == 0) st[B] = tot;
-  if (u == 0 && threadIdx.x == 0) a.spill_ctr[0] = 0;   // spill list reset for this batch
 }
 
 // ------------------------------------------------------------------ 3
@@ -228,6 +240,9 @@ __global__ void __launch_bounds__(MSM_SC_NT, 2) k_msm_scatter(const __grid_const
   uint32_t *gbase = staged ? tstart + B : hist + B;                       // [B]
   __shared__ uint32_t sw[MSM_SC_NT / 32];
   for (int i = threadIdx.x; i < B; i += MSM_SC_NT) hist[i] = 0;
+  // the scan kernel before this one listed the oversized buckets; nothing
+  // else is appended until the group kernel (which waits for this kernel)
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) a.spill_ctr[1] = a.spill_ctr[0];
   __syncthreads();
   const uint64_t *codes = a.codes + (int64_t)ub.rep[u] * a.n * W;
   const unsigned long long *kept = ub.kept[u];
@@ -986,15 +1001,7 @@ __global__ void __launch_bounds__(SmallCfg<W>::NT, SmallCfg<W>::MIN_CTAS) k_msm_
   const uint32_t s = st[b + 1] - s0;
   const uint64_t *src = a.elems + (int64_t)u * a.n + s0;
   if (s < 2) return;
-  if (s > CAP) {
-    if (threadIdx.x == 0) {
-      const unsigned long long slot = atomicAdd(&a.spill_ctr[0], 1ull);
-      if ((int64_t)slot < a.spill_cap) {
-        a.spill[slot * 3 + 0] = (uint32_t)u;
-        a.spill[slot * 3 + 1] = s0;
-        a.spill[slot * 3 + 2] = s;
-      }
-    }
+  if (s > CAP) {   // listed by k_msm_scan for the medium / tile tiers
     if (s > (uint32_t)MediumCfg<W>::CAP && (int64_t)s * 4 > a.n) {
       uint32_t *g = spill_gcnt(a, u, s0);   // group counts for the warning
       for (uint32_t i = threadIdx.x; i < s; i += NT) g[i] = 0;
@@ -1026,13 +1033,18 @@ template <int W>
 #define EG_MEDIUM_MINCTAS 2   // two 512-thread CTAs per SM where shared memory allows (W <= 2)
 #endif
 __global__ void __launch_bounds__(MediumCfg<W>::NT, EG_MEDIUM_MINCTAS) k_msm_medium(
-    const __grid_constant__ MsmArgs a, const __grid_constant__ UnitBatch ub) {
+    const __grid_constant__ MsmArgs a, const __grid_constant__ UnitBatch ub, const int phase) {
   extern __shared__ __align__(16) unsigned char smraw[];
   using Smem = HGroupSmem<W, MediumCfg<W>::CAP, MediumCfg<W>::NT, 1>;
   Smem &S = *reinterpret_cast<Smem *>(smraw);
-  const unsigned long long nspill = min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
+  // phase 0 (beside the small tier): the oversized buckets k_msm_scan listed;
+  // phase 1 (after it): the buckets the small tier re-queued
+  const unsigned long long listed = min(a.spill_ctr[1], (unsigned long long)a.spill_cap);
+  const unsigned long long first = phase == 0 ? 0ull : listed;
+  const unsigned long long nspill =
+      phase == 0 ? listed : min(a.spill_ctr[0], (unsigned long long)a.spill_cap);
   for (int i = threadIdx.x; i < a.L; i += MediumCfg<W>::NT) S.b2b[i] = a.bit2blk[i];
-  for (unsigned long long sb = blockIdx.x; sb < nspill; sb += gridDim.x) {
+  for (unsigned long long sb = first + blockIdx.x; sb < nspill; sb += gridDim.x) {
     const uint32_t s = a.spill[sb * 3 + 2];
     const uint32_t tag = a.spill[sb * 3];
     const bool requeued = tag & SPILL_FROM_SMALL;     // small tier ran out of member room
