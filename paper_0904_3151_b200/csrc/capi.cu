@@ -1166,11 +1166,12 @@ int eg_msm_pairs_design(const uint64_t *d_codes, int64_t n, int32_t length, int3
   // units (a sharded rank's share), so the second batch's hist / scatter
   // overlap the first batch's grouping on the side stream
   std::vector<UnitBatch> batches;
-  int64_t nbatch = (n_units + lay.U - 1) / lay.U;
+  const int64_t min_batches = (n_units + lay.U - 1) / lay.U;   // scratch capacity
+  int64_t nbatch = min_batches;
   if (lay.sets == 2 && n_units >= 4)
     nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(2, n_units / 2));
   if (options().msm_batches > 0)
-    nbatch = std::max<int64_t>(nbatch, std::min<int64_t>(options().msm_batches, n_units));
+    nbatch = std::max<int64_t>(min_batches, std::min<int64_t>(options().msm_batches, n_units));
   const int64_t per_batch = nbatch > 0 ? (n_units + nbatch - 1) / nbatch : lay.U;
   for (int64_t u0 = 0; u0 < n_units; u0 += per_batch) {
     UnitBatch ub;

@@ -27,7 +27,12 @@ ap.add_argument("--ranks", type=int, default=8)
 ap.add_argument("--nvlink-gbs", type=float, default=700.0,
                 help="effective all-gather bandwidth per GPU (NVLink 5: 900 GB/s per direction)")
 ap.add_argument("--coll-latency-us", type=float, default=20.0)
+ap.add_argument("--opt", action="append", default=[], help="name=value for eg_set_option")
 a = ap.parse_args()
+for o in a.opt:
+    from paper_0904_3151_b200 import _native
+    k_, v_ = o.split("=")
+    assert _native.lib().eg_set_option(k_.encode(), int(v_)) == 0, o
 cfg = CONFIGS[a.config]
 params = bench.params_for(cfg, eg)
 x = torch.from_numpy(bench.make_inputs(a.config)[0]).cuda()
