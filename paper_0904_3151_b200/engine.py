@@ -276,6 +276,14 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     # prefix pairs still need the full-code filter)
     defer = reps > 1 or full_codes is not None
     reruns = 0
+    # buffers of the cross-replicate pass, made before the units run: the
+    # device idles between eg_msm_pairs' final synchronisation and the next
+    # launch for as long as the host takes to get there
+    xkeep = xnewc = xnewc_host = None
+    if reps > 1 and full_codes is None:
+        xkeep = torch.empty(max(capacity, 1), dtype=torch.uint8, device=dev)
+        xnewc = torch.empty(reps, dtype=torch.int64, device=dev)
+        xnewc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
     while True:
         out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         rtag = torch.empty(max(capacity, 1), dtype=torch.int16, device=dev) if defer else None
@@ -313,14 +321,17 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
         total = int(keys.numel())
         raw = tuple(int(v) for v in rawc.tolist())
     if reps > 1:
-        keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
-        newc = torch.empty(reps, dtype=torch.int64, device=dev)
+        if xkeep is not None and xkeep.numel() >= max(total, 1):
+            keep, newc, newc_host = xkeep, xnewc, xnewc_host
+        else:
+            keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
+            newc = torch.empty(reps, dtype=torch.int64, device=dev)
+            newc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
         check(lib.eg_xrep_filter_async(_p(keys), _p(rtag), total, _p(xcodes), n,
                                        xcodes.shape[2], d, reps, _p(keep), _p(newc),
                                        _stream(dev)), "xrep_filter")
         # the counts reach pinned host memory behind the filter; the
         # compaction's synchronisation makes them readable
-        newc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
         newc_host.copy_(newc, non_blocking=True)
         keys = compact_keys(keys, keep[:total])
         new = tuple(int(v) for v in newc_host.tolist())
