@@ -850,8 +850,10 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
     }
     // one visit: partner code at shared address q; returns false when the
     // pair is rejected by the key / Hamming test (the common case)
+    // (the exact key compare -- distinct keys sharing h2, 2^-32 per pair --
+    // waits for the rare path: a colliding pair almost never passes the
+    // popcount test)
     auto reject = [&](uint32_t q, uint64_t (&x)[W], uint32_t &pc) -> bool {
-      uint64_t keydiff = 0;
       pc = 0;
 #pragma unroll
       for (int w = 0; w < W; ++w) {
@@ -859,13 +861,15 @@ __device__ __forceinline__ bool process_bucket(HGroupSmem<W, CAP, NT, MDIV> &S,
         asm volatile("ld.shared.u64 %0, [%1];" : "=l"(cbw) : "r"(q + 8 * w));
         x[w] = ca[w] ^ cbw;
         pc += __popcll(x[w]);
-        keydiff |= x[w] & kp[w];
       }
-      return keydiff != 0 || pc - plo > dmax;
+      return pc - plo > dmax;
     };
     // rare: within d on equal keys -- ownership, then the replicate rule
     auto accept = [&](uint32_t q, const uint64_t (&x)[W], uint32_t pc) {
-      if (!tt.ok(x, (int)pc, S.b2b, a.k, a.d)) return;
+      uint64_t keydiff = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) keydiff |= x[w] & kp[w];
+      if (keydiff != 0 || !tt.ok(x, (int)pc, S.b2b, a.k, a.d)) return;
       const uint32_t rb = mrows[(q - mc_s) / CB];
       int v = 2;
       if (!a.out_rep) {
