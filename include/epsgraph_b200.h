@@ -232,6 +232,10 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
                    void *stream);
 /* Same, without synchronising: the survivor counts go to device memory   */
 /* d_new_counts[replicates] (valid once the stream reaches this point).   */
+/* d_keep may be null: the keys of dropped pairs are then overwritten     */
+/* with ~0 in place (d_keys must be writable), so that one sort of the    */
+/* whole array leaves the sum(d_new_counts) survivors in front -- the     */
+/* build's path when few pairs can be dropped (no compaction pass).       */
 int eg_xrep_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
                          const uint64_t *d_codes, int64_t n, int32_t W, int32_t d,
                          int32_t replicates, uint8_t *d_keep, uint64_t *d_new_counts,

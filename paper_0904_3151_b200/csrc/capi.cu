@@ -1246,7 +1246,8 @@ int eg_xrep_filter_async(const uint64_t *d_keys, const uint16_t *d_reps, int64_t
   if (m > 0) {
     unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
     EG_PROF(PC_MISC, st);
-    k_xrep_filter<<<grid, 256, 0, st>>>(d_keys, d_reps, m, d_codes, n, W, d, replicates, d_keep,
+    k_xrep_filter<<<grid, 256, 0, st>>>(const_cast<uint64_t *>(d_keys), d_reps, m, d_codes, n, W,
+                                        d, replicates, d_keep,
                                         (unsigned long long *)d_new_counts);
     EG_LAUNCH_CHECK();
   }
@@ -1273,8 +1274,8 @@ int eg_xrep_filter(const uint64_t *d_keys, const uint16_t *d_reps, int64_t m,
   if (m > 0) {
     unsigned grid = (unsigned)std::min<int64_t>((m + 255) / 256, (int64_t)num_sms() * 16);
     EG_PROF(PC_MISC, st);
-    k_xrep_filter<<<grid, 256, 0, st>>>(d_keys, d_reps, m, d_codes, n, W, d, replicates, d_keep,
-                                        nc);
+    k_xrep_filter<<<grid, 256, 0, st>>>(const_cast<uint64_t *>(d_keys), d_reps, m, d_codes, n, W,
+                                        d, replicates, d_keep, nc);
     EG_LAUNCH_CHECK();
   }
   std::vector<unsigned long long> h(replicates);

@@ -1233,7 +1233,10 @@ __global__ void k_msm_spill_maxgroup(const __grid_constant__ MsmArgs a) {
 // h survives iff its Hamming distance exceeds d in every replicate g < h.
 // Counts survivors per replicate (per_replicate_new).
 constexpr int XREP_SMEM_REPS = 1024;   // replicates counted in shared memory
-__global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint16_t *__restrict__ reps,
+// keep == nullptr: a dropped pair's key is overwritten with ~0 instead (it
+// then sorts behind every real key; the caller sorts the whole array and
+// keeps the first sum(new_counts) keys -- no compaction pass).
+__global__ void k_xrep_filter(uint64_t *__restrict__ keys, const uint16_t *__restrict__ reps,
                               int64_t m, const uint64_t *__restrict__ codes, int64_t n, int W,
                               int d, int nreps, uint8_t *__restrict__ keep,
                               unsigned long long *__restrict__ new_counts) {
@@ -1252,7 +1255,8 @@ __global__ void k_xrep_filter(const uint64_t *__restrict__ keys, const uint16_t 
       for (int w = 0; w < W; ++w) pc += __popcll(__ldg(cg + i * W + w) ^ __ldg(cg + j * W + w));
       ok = pc > d;
     }
-    keep[p] = ok;
+    if (keep) keep[p] = ok;
+    else if (!ok) keys[p] = ~0ull;
     if (ok) {
       if (h < XREP_SMEM_REPS) atomicAdd(&cnt[h], 1u);
       else atomicAdd(&new_counts[h], 1ull);

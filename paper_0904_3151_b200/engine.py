@@ -327,14 +327,28 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
             keep = torch.empty(max(total, 1), dtype=torch.uint8, device=dev)
             newc = torch.empty(reps, dtype=torch.int64, device=dev)
             newc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
+        # Few droppable pairs and a small set: drop them IN PLACE (key ~0)
+        # and sort the whole array at once -- the dropped keys end up behind
+        # the sum(new) survivors, so no compaction pass and no host round
+        # trip between the units, the filter and the sort.
+        in_place = (full_codes is None and 1 < total <= (1 << 24)
+                    and 5 * sum(raw[1:]) <= 2 * total)
         check(lib.eg_xrep_filter_async(_p(keys), _p(rtag), total, _p(xcodes), n,
-                                       xcodes.shape[2], d, reps, _p(keep), _p(newc),
+                                       xcodes.shape[2], d, reps,
+                                       None if in_place else _p(keep), _p(newc),
                                        _stream(dev)), "xrep_filter")
         # the counts reach pinned host memory behind the filter; the
-        # compaction's synchronisation makes them readable
+        # synchronisation below (or the compaction's) makes them readable
         newc_host.copy_(newc, non_blocking=True)
-        keys = compact_keys(keys, keep[:total])
-        new = tuple(int(v) for v in newc_host.tolist())
+        if in_place:
+            sort_pair_keys(keys, n)
+            torch.cuda.current_stream(dev).synchronize()
+            new = tuple(int(v) for v in newc_host.tolist())
+            keys = keys[:sum(new)]
+            keys._eg_sorted = True      # sort_pair_keys(keys, n) is a no-op on this tensor
+        else:
+            keys = compact_keys(keys, keep[:total])
+            new = tuple(int(v) for v in newc_host.tolist())
     elif full_codes is not None:
         new = raw
     else:
@@ -419,6 +433,8 @@ def estimate_pairs(codes: torch.Tensor, d: int):
 
 def sort_pair_keys(keys: torch.Tensor, n: int) -> torch.Tensor:
     m = keys.numel()
+    if getattr(keys, "_eg_sorted", False):     # msm_pairs' in-place path sorted it already
+        return keys
     if m > 1:
         lib = _native.lib()
         ws = _ws(lib.eg_sort_workspace(m, 0), keys.device)
