@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import itertools
 import math
+import threading
 from math import comb
 
 import numpy as np
@@ -176,7 +177,21 @@ def plan_design(plan: int, d: int):
     """(block count, ordered masked-block bitmasks of one replicate's units,
     is_design) of a plan code: a block count k' (the complete family of
     d-subsets, reference order) or DESIGN_BASE + 100 v + m (the library's
-    covering design C(v, m, d), eg_msm_design)."""
+    covering design C(v, m, d), eg_msm_design).  A pure function of its
+    arguments, memoised: it runs between the plan and the first unit kernel,
+    where host time is device idle time."""
+    hit = _plan_cache.get((plan, d))
+    if hit is None:
+        v, masks, is_design = _plan_design(int(plan), int(d))
+        masks.setflags(write=False)
+        hit = _plan_cache[(plan, d)] = (v, masks, is_design)
+    return hit
+
+
+_plan_cache: dict = {}
+
+
+def _plan_design(plan: int, d: int):
     if plan < DESIGN_BASE:
         bits = []
         for m in masks_for(plan, d):
@@ -205,10 +220,22 @@ def unit_count(plan: int, d: int) -> int:
 def units_for(replicates, k: int, d: int):
     """(replicate index, block bitmask) for every unit, in reference order
     (``k``: a block count or a design's plan code)."""
-    _, family, _ = plan_design(k, d)
-    reps = np.repeat(np.asarray(list(replicates), dtype=np.int32), len(family))
-    bits = np.tile(family, len(reps) // max(1, len(family)))
-    return reps, bits
+    key = (tuple(int(h) for h in replicates), int(k), int(d))
+    hit = _units_cache.get(key)
+    if hit is None:
+        _, family, _ = plan_design(k, d)
+        reps = np.repeat(np.asarray(key[0], dtype=np.int32), len(family))
+        bits = np.tile(family, len(reps) // max(1, len(family)))
+        reps.setflags(write=False)
+        bits.setflags(write=False)
+        if len(_units_cache) >= 64:
+            _units_cache.clear()
+        hit = _units_cache[key] = (reps, bits)
+    return hit
+
+
+_units_cache: dict = {}
+_xrep_scratch: dict = {}
 
 
 def msm_plan(codes: torch.Tensor, length: int, k: int, d: int,
@@ -281,9 +308,17 @@ def msm_pairs(codes: torch.Tensor, length: int, block_bounds, d: int, unit_reps,
     # launch for as long as the host takes to get there
     xkeep = xnewc = xnewc_host = None
     if reps > 1 and full_codes is None:
-        xkeep = torch.empty(max(capacity, 1), dtype=torch.uint8, device=dev)
-        xnewc = torch.empty(reps, dtype=torch.int64, device=dev)
-        xnewc_host = torch.empty(reps, dtype=torch.int64, pin_memory=True)
+        # per-(device, thread) scratch kept between calls (stream-ordered reuse)
+        skey = (str(dev), threading.get_ident())
+        hit = _xrep_scratch.get(skey)
+        if hit is None or hit[0].numel() < max(capacity, 1) or hit[1].numel() != reps:
+            hit = (torch.empty(max(capacity, 1), dtype=torch.uint8, device=dev),
+                   torch.empty(reps, dtype=torch.int64, device=dev),
+                   torch.empty(reps, dtype=torch.int64, pin_memory=True))
+            if len(_xrep_scratch) >= 16:
+                _xrep_scratch.clear()
+            _xrep_scratch[skey] = hit
+        xkeep, xnewc, xnewc_host = hit
     while True:
         out = torch.empty(max(capacity, 1), dtype=torch.int64, device=dev)
         rtag = torch.empty(max(capacity, 1), dtype=torch.int16, device=dev) if defer else None
