@@ -52,9 +52,13 @@ const char *eg_last_error(void);
 /* environment).  Names: "project_path" (0 auto, 1 SIMT, 2 kind::tf32,    */
 /* 3 unfused norms, 4 non-TMA tensor-core kernel), "fixup_force_seq",     */
 /* "fixup_cap" (> 0 caps the band-entry list: overflow path),            */
-/* "msm_blocks" (> 0 forces the block count, -1 keeps the reference's),   */
-/* "msm_streams" (1 or 2), "verify_wide", "sort_path" (-1 auto, 0         */
-/* onesweep, 1 classic).  EG_ERR_ARG for an unknown name or value.        */
+/* "msm_blocks" (> 0 forces the block count or a design's plan code      */
+/* 10000 + 100 v + m, -1 keeps the reference's), "msm_designs" (0: the    */
+/* plan considers complete designs only), "msm_batches" (> 0: launch      */
+/* batches per eg_msm_pairs call), "plan_debug" (1: eg_msm_plan prints    */
+/* its candidates to stderr), "msm_streams" (1 or 2), "verify_wide",      */
+/* "sort_path" (-1 auto, 0 onesweep, 1 classic).  EG_ERR_ARG for an       */
+/* unknown name or value.                                                 */
 /* Process-wide; not synchronised with calls in flight.                   */
 int eg_set_option(const char *name, long long value);
 void eg_reset_options(void);
